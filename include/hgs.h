@@ -1,0 +1,166 @@
+/*
+ * hgs.h — C ABI of the B200 bulk ShaDow sampler ("hitgnn gpu sampler").
+ *
+ * This is the drop-in boundary for the reference hot path
+ *   hitgnn::bulk_shadow      /root/reference/proj/include/hitgnn/sampler.hpp:88-91
+ *                            (src/sampler.cpp:123-201)
+ *   hitgnn::shadow_reference sampler.hpp:75-76 (sampler.cpp:88-121)
+ *   hitgnn::gather_features  sampler.hpp:102   (sampler.cpp:211-243)
+ *   hitgnn::symmetrize_pattern sparse.hpp:97   (sparse.cpp:260-272)
+ *   hitgnn::Rng::derive      rng.hpp:31-32     (rng.cpp:76-85)
+ * Plain pointers and sizes only; no C++ or torch types. Host-side C++
+ * (include/hitgnn/*.hpp, libhitgnn_gpu.so) and Python (ctypes) sit above it.
+ *
+ * Errors: every int-returning call returns HGS_OK (0) or an HGS_E* code; the
+ * message is in hgs_last_error() (thread-local). HGS_EINVAL carries the
+ * reference's std::invalid_argument text verbatim where one exists (e.g.
+ * "sampler: duplicate root 17", sampler.cpp:18).
+ *
+ * Threading: a graph handle is bound to one CUDA device. A sample handle is
+ * a reusable device workspace + output set bound to one graph and one CUDA
+ * stream; calls on one sample handle must not overlap. Different sample
+ * handles (e.g. one per host thread / GPU) are independent.
+ *
+ * Device output layout of one call (all int32 unless noted; V, E = totals
+ * over all batches of the call; k = n_batches, R = roots):
+ *   l2g[V]          local_to_global, components back to back, each sorted
+ *   roots_local[R]  batch-local index of each root
+ *   comp_off[R+k]   per batch b: its R_b+1 batch-local component offsets
+ *   batch_voff[k+1], batch_eoff[k+1]  call-level vertex / edge offsets
+ *   e_row[E], e_col[E]  batch-local endpoints (row-major, columns ascending)
+ *   e_gid[E]        edge id = CSR position in the input A (make_edge_id_matrix
+ *                   value - 1, sampler.cpp:203-209)
+ *   root_voff[R+1], root_eoff[R+1]  call-level offsets of every component
+ *   xv[V*f_v] (f64), ye[E*f_e] (f64), lab[E] (u8)   when gather != 0
+ *   draws[R], decisions[R] (u32) RNG draws / choose() calls consumed per root
+ */
+#ifndef HGS_H
+#define HGS_H
+
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+#define HGS_ABI_VERSION 1
+
+enum {
+    HGS_OK = 0,
+    HGS_EINVAL = 1,   /* std::invalid_argument in the reference            */
+    HGS_ECUDA = 2,    /* CUDA / runtime failure (std::runtime_error)        */
+    HGS_ERANGE = 3    /* size limit of this implementation exceeded        */
+};
+
+enum {
+    HGS_RNG_XOSHIRO = 0, /* PerRootChoiceSource: xoshiro256** per root stream */
+    HGS_RNG_PHILOX = 1   /* PhiloxChoiceSource: counter-based per decision     */
+};
+
+typedef struct hgs_graph hgs_graph;
+typedef struct hgs_sample hgs_sample;
+
+/* SamplerConfig (sampler.hpp:16-24) plus device options. batch_size and
+ * bulk_batches are validated like the reference but do not change results. */
+typedef struct {
+    int64_t depth;        /* d >= 1 */
+    int64_t fanout;       /* s >= 1 */
+    int64_t batch_size;   /* b >= 1 (validated only) */
+    int64_t bulk_batches; /* k >= 1 (validated only) */
+    int32_t symmetrize;   /* walk on pattern(A ∪ Aᵀ) */
+    int32_t rng;          /* HGS_RNG_* */
+    int32_t gather;       /* also gather node/edge features + labels */
+    int32_t profile;      /* record per-kernel CUDA event times */
+} hgs_config;
+
+/* Host destinations for hgs_sample_copy_to_host (any pointer may be NULL). */
+typedef struct {
+    int32_t* batch_voff;  /* k+1 */
+    int32_t* batch_eoff;  /* k+1 */
+    int32_t* comp_off;    /* R+k */
+    int32_t* l2g;         /* V   */
+    int32_t* roots_local; /* R   */
+    int32_t* e_row;       /* E   */
+    int32_t* e_col;       /* E   */
+    int32_t* e_gid;       /* E   */
+    double* xv;           /* V*f_v */
+    double* ye;           /* E*f_e */
+    uint8_t* lab;         /* E   */
+    uint32_t* draws;      /* R   */
+    uint32_t* decisions;  /* R   */
+} hgs_host_out;
+
+/* Device pointers of the last call's outputs (valid until the next run or
+ * destroy on the same sample handle). */
+typedef struct {
+    const int32_t *batch_voff, *batch_eoff, *comp_off, *l2g, *roots_local;
+    const int32_t *e_row, *e_col, *e_gid, *root_voff, *root_eoff;
+    const double *xv, *ye;
+    const uint8_t* lab;
+    const uint32_t *draws, *decisions;
+    const int32_t *touched, *touched_count; /* expand scratch: per root, stride touched_stride */
+    const int32_t* level_counts;            /* [R][depth+1] frontier rows per level */
+    int64_t touched_stride;
+} hgs_device_views;
+
+const char* hgs_last_error(void);
+int hgs_abi_version(void);
+int hgs_device_count(int* count);
+
+/* ---- graph store ---------------------------------------------------------
+ * A in the reference's CsrMatrix layout (int64 row_ptr[n_rows+1],
+ * col_idx[nnz], optional double values[nnz]; NULL values = edge-id matrix).
+ * Requires n < 2^31, nnz < 2^31, columns within [0, n_cols). */
+int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                     const int64_t* col_idx, const double* values, hgs_graph** out);
+/* EventGraph features (data.hpp:17-27): node_feat[n*f_v], edge_feat[nnz*f_e]
+ * in canonical edge (= CSR) order, labels[nnz]. */
+int hgs_graph_attach_features(hgs_graph* g, const double* node_feat, int64_t f_v,
+                              const double* edge_feat, int64_t f_e, const uint8_t* labels);
+/* info: [0]=n_rows [1]=n_cols [2]=nnz [3]=walk nnz (sym) [4]=max walk degree (sym)
+ *       [5]=max out-degree [6]=f_v [7]=f_e */
+int hgs_graph_info(hgs_graph* g, int64_t* info);
+/* Copy the device walk CSR (K0 output when symmetrize) to host int64 arrays:
+ * row_ptr[n+1], col_idx[walk nnz]. */
+int hgs_graph_walk(hgs_graph* g, int32_t symmetrize, int64_t* row_ptr, int64_t* col_idx);
+int hgs_graph_destroy(hgs_graph* g);
+
+/* ---- sampling ------------------------------------------------------------- */
+/* stream: a cudaStream_t (NULL = a stream owned by the handle). */
+int hgs_sample_create(hgs_graph* g, void* stream, hgs_sample** out);
+int hgs_sample_destroy(hgs_sample* s);
+
+/* bulk_shadow over batches given as flat roots[batch_off[n_batches]] with
+ * batch_off[0] = 0 (host pointers). seeds[R]: per-root stream seeds
+ * (PerRootChoiceSource / PhiloxChoiceSource seeds, root ordinal = flat index).
+ * rng_state (nullable): resumes non-fresh sources — xoshiro: 4 u64 state
+ * words per root; philox: 1 u64 per root = decisions already consumed.
+ * Blocks until the results are ready. */
+int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
+                   const int64_t* batch_off, int64_t n_batches, const uint64_t* seeds,
+                   const uint64_t* rng_state);
+/* Same, with device-resident int32 roots[n_roots], int64 batch_off[n_batches+1]
+ * and u64 seeds; enqueued asynchronously on the handle's stream. Roots are
+ * range-checked on the device (reported by hgs_sample_wait); per-batch
+ * distinctness is the caller's contract on this entry point. */
+int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d_roots,
+                          const int64_t* d_batch_off, int64_t n_roots, int64_t n_batches,
+                          const uint64_t* d_seeds);
+/* Wait for the last run; fills counts[0..3] = R, k, V, E (may be NULL). */
+int hgs_sample_wait(hgs_sample* s, int64_t* counts);
+int hgs_sample_copy_to_host(hgs_sample* s, const hgs_host_out* out);
+int hgs_sample_device_views(hgs_sample* s, hgs_device_views* out);
+/* Per-kernel times (ms) of the last profiled run: [0]=expand [1]=extract
+ * [2]=finalize [3]=total; returns HGS_EINVAL if the run was not profiled. */
+int hgs_sample_kernel_times(hgs_sample* s, float* ms4);
+/* Number of kernels the last run launched (for gpu_launches accounting). */
+int hgs_sample_launches(hgs_sample* s, int64_t* n);
+
+/* ---- RNG helpers (host, no GPU needed) -------------------------------------- */
+uint64_t hgs_derive(uint64_t seed, const uint64_t* path, int32_t len);
+void hgs_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

@@ -1,0 +1,432 @@
+// abi.cu — the C ABI (include/hgs.h) over the device graph store and the
+// sampling pipeline. Host work here is input validation with the reference's
+// error semantics, graph ingest (int64 -> int32 narrowing, explicit-zero and
+// negative-value bookkeeping) and host<->device copies; all sampling
+// arithmetic runs in the kernels of sampler.cu / graph.cu.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+#include <string>
+#include <vector>
+
+#include "hgs_internal.cuh"
+
+using namespace hgs;
+
+namespace {
+
+thread_local std::string g_err;
+
+template <class F>
+int guarded(F&& f) {
+    try {
+        f();
+        return HGS_OK;
+    } catch (const Failure& e) {
+        g_err = e.what();
+        return e.code;
+    } catch (const std::bad_alloc&) {
+        g_err = "hgs: host allocation failed";
+        return HGS_ECUDA;
+    } catch (const std::exception& e) {
+        g_err = e.what();
+        return HGS_ECUDA;
+    }
+}
+
+void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
+    if (bytes) HGS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
+}
+
+void upload_csr(DevCsr& d, int32_t n, const std::vector<int32_t>& rp, const std::vector<int32_t>& ci,
+                cudaStream_t st) {
+    d.n = n;
+    d.nnz = (int64_t)ci.size();
+    d.rp.reserve(rp.size());
+    d.ci.reserve(std::max<size_t>(ci.size(), 1));
+    upload(d.rp.p, rp.data(), rp.size() * sizeof(int32_t), st);
+    upload(d.ci.p, ci.data(), ci.size() * sizeof(int32_t), st);
+    int32_t md = 0;
+    for (int32_t u = 0; u < n; ++u) md = std::max(md, rp[u + 1] - rp[u]);
+    d.max_deg = md;
+}
+
+// SamplerConfig::validate (sampler.cpp:57-62), verbatim messages.
+void validate_cfg(const hgs_config* cfg) {
+    if (!cfg) fail(HGS_EINVAL, "hgs: null config");
+    if (cfg->depth < 1) fail(HGS_EINVAL, "SamplerConfig: depth must be >= 1");
+    if (cfg->fanout < 1) fail(HGS_EINVAL, "SamplerConfig: fanout must be >= 1");
+    if (cfg->batch_size < 1) fail(HGS_EINVAL, "SamplerConfig: batch_size must be >= 1");
+    if (cfg->bulk_batches < 1) fail(HGS_EINVAL, "SamplerConfig: bulk_batches must be >= 1");
+    if (cfg->rng != HGS_RNG_XOSHIRO && cfg->rng != HGS_RNG_PHILOX) fail(HGS_EINVAL, "hgs: unknown rng kind");
+}
+
+// The walk's squareness checks of the reference: symmetrize_pattern
+// (sparse.cpp:261) or, unsymmetrized, spgemm(q, walk) (sparse.cpp:79-81).
+void check_square(const DevGraph& g, int32_t symmetrize) {
+    if (g.n_rows == g.n_cols) return;
+    if (symmetrize) fail(HGS_EINVAL, "symmetrize_pattern: matrix must be square");
+    fail(HGS_EINVAL, "spgemm: inner dimensions disagree (" + std::to_string(g.n_cols) + " vs " +
+                         std::to_string(g.n_rows) + ")");
+}
+
+}  // namespace
+
+extern "C" {
+
+const char* hgs_last_error(void) { return g_err.c_str(); }
+int hgs_abi_version(void) { return HGS_ABI_VERSION; }
+
+int hgs_device_count(int* count) {
+    return guarded([&] {
+        int c = 0;
+        const cudaError_t e = cudaGetDeviceCount(&c);
+        if (e != cudaSuccess) { cudaGetLastError(); c = 0; }
+        *count = c;
+    });
+}
+
+uint64_t hgs_derive(uint64_t seed, const uint64_t* path, int32_t len) { return derive_seed(seed, path, len); }
+
+void hgs_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
+    uint32_t c[4] = {ctr[0], ctr[1], ctr[2], ctr[3]};
+    philox4x32_10(c, key[0], key[1]);
+    std::memcpy(out, c, sizeof(c));
+}
+
+// ---- graph -------------------------------------------------------------------
+
+int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr,
+                     const int64_t* col_idx, const double* values, hgs_graph** out) {
+    return guarded([&] {
+        if (!out) fail(HGS_EINVAL, "hgs_graph_create: null out");
+        *out = nullptr;
+        if (n_rows < 0 || n_cols < 0) fail(HGS_EINVAL, "hgs_graph_create: negative dimension");
+        if (n_rows >= ((int64_t)1 << 31) - 1 || n_cols >= ((int64_t)1 << 31) - 1)
+            fail(HGS_ERANGE, "hgs_graph_create: more than 2^31-2 vertices");
+        if (!row_ptr) fail(HGS_EINVAL, "hgs_graph_create: null row_ptr");
+        if (row_ptr[0] != 0) fail(HGS_EINVAL, "hgs_graph_create: row_ptr[0] must be 0");
+        const int64_t nnz = row_ptr[n_rows];
+        if (nnz >= ((int64_t)1 << 31) - 1) fail(HGS_ERANGE, "hgs_graph_create: more than 2^31-2 entries");
+        if (nnz > 0 && !col_idx) fail(HGS_EINVAL, "hgs_graph_create: null col_idx");
+        const int32_t n = (int32_t)n_rows;
+        std::vector<int32_t> rp(n + 1), ci, gid, frp, fci;
+        ci.reserve(nnz);
+        bool zeros = false, neg = false;
+        std::vector<uint8_t> negrow;
+        for (int32_t u = 0; u < n; ++u) {
+            if (row_ptr[u + 1] < row_ptr[u]) fail(HGS_EINVAL, "hgs_graph_create: row_ptr not non-decreasing");
+            for (int64_t k = row_ptr[u]; k < row_ptr[u + 1]; ++k) {
+                const int64_t c = col_idx[k];
+                if (c < 0 || c >= n_cols)
+                    fail(HGS_EINVAL, "CsrMatrix: entry (" + std::to_string(u) + ", " + std::to_string(c) +
+                                         ") out of range for " + std::to_string(n_rows) + "x" +
+                                         std::to_string(n_cols));
+                if (values && values[k] == 0.0) {  // dropped by spgemm (sparse.cpp:118-121)
+                    zeros = true;
+                    continue;
+                }
+                if (values && values[k] < 0.0) {
+                    if (negrow.empty()) negrow.assign(n, 0);
+                    negrow[u] = 1;
+                    neg = true;
+                }
+                ci.push_back((int32_t)c);
+                gid.push_back((int32_t)k);
+            }
+            rp[u + 1] = (int32_t)ci.size();
+        }
+        auto* h = new hgs_graph;
+        DevGraph& g = h->g;
+        try {
+            g.device = device;
+            HGS_CUDA(cudaSetDevice(device));
+            HGS_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+            g.n_rows = n_rows;
+            g.n_cols = n_cols;
+            g.nnz = nnz;
+            upload_csr(g.a, n, rp, ci, g.stream);
+            if (zeros) {
+                g.has_gid = true;
+                g.a_gid.reserve(gid.size());
+                upload(g.a_gid.p, gid.data(), gid.size() * sizeof(int32_t), g.stream);
+                frp.resize(n + 1);
+                fci.resize(nnz);
+                for (int32_t u = 0; u <= n; ++u) frp[u] = (int32_t)row_ptr[u];
+                for (int64_t k = 0; k < nnz; ++k) fci[k] = (int32_t)col_idx[k];
+                g.has_full = true;
+                upload_csr(g.a_full, n, frp, fci, g.stream);
+            }
+            if (neg) {
+                g.has_neg = true;
+                g.neg_row.reserve(n);
+                upload(g.neg_row.p, negrow.data(), n, g.stream);
+            }
+            HGS_CUDA(cudaStreamSynchronize(g.stream));
+        } catch (...) {
+            if (g.stream) cudaStreamDestroy(g.stream);
+            delete h;
+            throw;
+        }
+        *out = h;
+    });
+}
+
+int hgs_graph_attach_features(hgs_graph* h, const double* node_feat, int64_t f_v,
+                              const double* edge_feat, int64_t f_e, const uint8_t* labels) {
+    return guarded([&] {
+        if (!h) fail(HGS_EINVAL, "hgs: null graph");
+        DevGraph& g = h->g;
+        if (f_v < 0 || f_e < 0) fail(HGS_EINVAL, "hgs_graph_attach_features: negative width");
+        HGS_CUDA(cudaSetDevice(g.device));
+        g.f_v = (int32_t)f_v;
+        g.f_e = (int32_t)f_e;
+        g.node_feat.reserve((size_t)std::max<int64_t>(1, g.n_rows * f_v));
+        g.edge_feat.reserve((size_t)std::max<int64_t>(1, g.nnz * f_e));
+        g.labels.reserve((size_t)std::max<int64_t>(1, g.nnz));
+        upload(g.node_feat.p, node_feat, sizeof(double) * g.n_rows * f_v, g.stream);
+        upload(g.edge_feat.p, edge_feat, sizeof(double) * g.nnz * f_e, g.stream);
+        upload(g.labels.p, labels, g.nnz, g.stream);
+        HGS_CUDA(cudaStreamSynchronize(g.stream));
+        g.has_features = true;
+    });
+}
+
+int hgs_graph_info(hgs_graph* h, int64_t* info) {
+    return guarded([&] {
+        if (!h) fail(HGS_EINVAL, "hgs: null graph");
+        DevGraph& g = h->g;
+        HGS_CUDA(cudaSetDevice(g.device));
+        if (g.n_rows == g.n_cols) graph_build_walk_sym(g);
+        info[0] = g.n_rows;
+        info[1] = g.n_cols;
+        info[2] = g.nnz;
+        info[3] = g.sym_built ? g.walk_sym.nnz : -1;
+        info[4] = g.sym_built ? g.walk_sym.max_deg : -1;
+        info[5] = g.a.max_deg;
+        info[6] = g.f_v;
+        info[7] = g.f_e;
+    });
+}
+
+int hgs_graph_walk(hgs_graph* h, int32_t symmetrize, int64_t* row_ptr, int64_t* col_idx) {
+    return guarded([&] {
+        if (!h) fail(HGS_EINVAL, "hgs: null graph");
+        DevGraph& g = h->g;
+        HGS_CUDA(cudaSetDevice(g.device));
+        check_square(g, symmetrize);
+        if (symmetrize) graph_build_walk_sym(g);
+        const DevCsr& w = symmetrize ? g.walk_sym : g.a;
+        std::vector<int32_t> rp(w.n + 1), ci(w.nnz);
+        HGS_CUDA(cudaMemcpy(rp.data(), w.rp.p, sizeof(int32_t) * (w.n + 1), cudaMemcpyDeviceToHost));
+        if (w.nnz) HGS_CUDA(cudaMemcpy(ci.data(), w.ci.p, sizeof(int32_t) * w.nnz, cudaMemcpyDeviceToHost));
+        for (int32_t u = 0; u <= w.n; ++u) row_ptr[u] = rp[u];
+        for (int64_t k = 0; k < w.nnz; ++k) col_idx[k] = ci[k];
+    });
+}
+
+int hgs_graph_destroy(hgs_graph* h) {
+    return guarded([&] {
+        if (!h) return;
+        cudaSetDevice(h->g.device);
+        cudaStream_t st = h->g.stream;
+        delete h;
+        if (st) cudaStreamDestroy(st);
+    });
+}
+
+// ---- sampling -------------------------------------------------------------------
+
+int hgs_sample_create(hgs_graph* g, void* stream, hgs_sample** out) {
+    return guarded([&] {
+        if (!g || !out) fail(HGS_EINVAL, "hgs_sample_create: null argument");
+        HGS_CUDA(cudaSetDevice(g->g.device));
+        auto* s = new hgs_sample;
+        s->graph = g;
+        if (stream) s->stream = (cudaStream_t)stream;
+        else {
+            HGS_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));
+            s->own_stream = true;
+        }
+        *out = s;
+    });
+}
+
+int hgs_sample_destroy(hgs_sample* s) {
+    return guarded([&] {
+        if (!s) return;
+        cudaSetDevice(s->graph->g.device);
+        if (s->pending) cudaStreamSynchronize(s->stream);
+        for (auto& e : s->ev) if (e) cudaEventDestroy(e);
+        if (s->h_state) cudaFreeHost(s->h_state);
+        cudaStream_t st = s->own_stream ? s->stream : nullptr;
+        delete s;
+        if (st) cudaStreamDestroy(st);
+    });
+}
+
+int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
+                   const int64_t* batch_off, int64_t n_batches, const uint64_t* seeds,
+                   const uint64_t* rng_state) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        validate_cfg(cfg);
+        DevGraph& g = s->graph->g;
+        if (n_batches < 0 || !batch_off) fail(HGS_EINVAL, "hgs_sample_run: bad batch offsets");
+        if (batch_off[0] != 0) fail(HGS_EINVAL, "hgs_sample_run: batch_off[0] must be 0");
+        for (int64_t b = 0; b < n_batches; ++b)
+            if (batch_off[b + 1] < batch_off[b]) fail(HGS_EINVAL, "hgs_sample_run: batch_off not non-decreasing");
+        const int64_t R = batch_off[n_batches];
+        if (R >= ((int64_t)1 << 31) - 1) fail(HGS_ERANGE, "hgs_sample_run: too many roots");
+        // check_roots per batch (sampler.cpp:12-20), in order, verbatim messages
+        static thread_local std::vector<uint8_t> seen;
+        if ((int64_t)seen.size() < g.n_rows) seen.assign((size_t)g.n_rows, 0);
+        for (int64_t b = 0; b < n_batches; ++b) {
+            int64_t i = batch_off[b];
+            for (; i < batch_off[b + 1]; ++i) {
+                const int64_t r = roots[i];
+                if (r < 0 || r >= g.n_rows) {
+                    for (int64_t j = batch_off[b]; j < i; ++j) seen[roots[j]] = 0;
+                    fail(HGS_EINVAL, "sampler: root " + std::to_string(r) + " out of range");
+                }
+                if (seen[r]) {
+                    for (int64_t j = batch_off[b]; j < i; ++j) seen[roots[j]] = 0;
+                    fail(HGS_EINVAL, "sampler: duplicate root " + std::to_string(r));
+                }
+                seen[r] = 1;
+            }
+            for (int64_t j = batch_off[b]; j < batch_off[b + 1]; ++j) seen[roots[j]] = 0;
+        }
+        check_square(g, cfg->symmetrize);
+        if (R > 0 && !seeds) fail(HGS_EINVAL, "hgs_sample_run: null seeds");
+        HGS_CUDA(cudaSetDevice(g.device));
+        if (s->pending) HGS_CUDA(cudaStreamSynchronize(s->stream));
+        s->pending = false;
+        s->boff64.reserve((size_t)n_batches + 1);
+        s->seeds.reserve((size_t)R + 1);
+        s->roots64.reserve((size_t)R + 1);
+        upload(s->roots64.p, roots, sizeof(int64_t) * R, s->stream);
+        upload(s->boff64.p, batch_off, sizeof(int64_t) * (n_batches + 1), s->stream);
+        upload(s->seeds.p, seeds, sizeof(uint64_t) * R, s->stream);
+        const bool philox = cfg->rng == HGS_RNG_PHILOX;
+        if (rng_state) {
+            const size_t words = philox ? (size_t)R : 4 * (size_t)R;
+            s->rng_state.reserve(words + 1);
+            upload(s->rng_state.p, rng_state, sizeof(uint64_t) * words, s->stream);
+        }
+        CallInputs in;
+        in.roots64 = s->roots64.p;
+        in.batch_off = s->boff64.p;
+        in.seeds = s->seeds.p;
+        in.state = rng_state ? s->rng_state.p : nullptr;
+        in.R = R;
+        in.k = n_batches;
+        sample_enqueue(s, *cfg, in);
+        sample_finish(s, *cfg, in);
+    });
+}
+
+int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d_roots,
+                          const int64_t* d_batch_off, int64_t n_roots, int64_t n_batches,
+                          const uint64_t* d_seeds) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        validate_cfg(cfg);
+        DevGraph& g = s->graph->g;
+        check_square(g, cfg->symmetrize);
+        HGS_CUDA(cudaSetDevice(g.device));
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_run_device: previous run not waited for");
+        CallInputs in;
+        in.roots32 = d_roots;
+        in.batch_off = d_batch_off;
+        in.seeds = d_seeds;
+        in.R = n_roots;
+        in.k = n_batches;
+        sample_enqueue(s, *cfg, in);
+        // remembered for a possible capacity re-run in hgs_sample_wait
+        s->last_in = in;
+        s->last_cfg = *cfg;
+    });
+}
+
+int hgs_sample_wait(hgs_sample* s, int64_t* counts) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        HGS_CUDA(cudaSetDevice(s->graph->g.device));
+        if (s->pending) sample_finish(s, s->last_cfg, s->last_in);
+        if (counts) {
+            counts[0] = s->R;
+            counts[1] = s->k;
+            counts[2] = s->V;
+            counts[3] = s->E;
+        }
+    });
+}
+
+int hgs_sample_copy_to_host(hgs_sample* s, const hgs_host_out* o) {
+    return guarded([&] {
+        if (!s || !o) fail(HGS_EINVAL, "hgs: null argument");
+        HGS_CUDA(cudaSetDevice(s->graph->g.device));
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_copy_to_host: run not waited for");
+        cudaStream_t st = s->stream;
+        const DevGraph& g = s->graph->g;
+        auto cp = [&](void* dst, const void* src, size_t bytes) {
+            if (dst && bytes) HGS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyDeviceToHost, st));
+        };
+        const size_t R = s->R, k = s->k, V = s->V, E = s->E;
+        cp(o->batch_voff, s->batch_voff.p, 4 * (k + 1));
+        cp(o->batch_eoff, s->batch_eoff.p, 4 * (k + 1));
+        cp(o->comp_off, s->comp_off.p, 4 * (R + k));
+        cp(o->l2g, s->l2g.p, 4 * V);
+        cp(o->roots_local, s->roots_local.p, 4 * R);
+        cp(o->e_row, s->e_row.p, 4 * E);
+        cp(o->e_col, s->e_col.p, 4 * E);
+        cp(o->e_gid, s->e_gid.p, 4 * E);
+        if (s->gathered) {
+            cp(o->xv, s->xv.p, 8 * V * g.f_v);
+            cp(o->ye, s->ye.p, 8 * E * g.f_e);
+            cp(o->lab, s->lab.p, E);
+        }
+        if (R) {
+            cp(o->draws, s->draws.p, 4 * R);
+            cp(o->decisions, s->decisions.p, 4 * R);
+        }
+        HGS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
+int hgs_sample_device_views(hgs_sample* s, hgs_device_views* v) {
+    return guarded([&] {
+        if (!s || !v) fail(HGS_EINVAL, "hgs: null argument");
+        v->batch_voff = s->batch_voff.p; v->batch_eoff = s->batch_eoff.p; v->comp_off = s->comp_off.p;
+        v->l2g = s->l2g.p; v->roots_local = s->roots_local.p; v->e_row = s->e_row.p;
+        v->e_col = s->e_col.p; v->e_gid = s->e_gid.p; v->root_voff = s->root_voff.p;
+        v->root_eoff = s->root_eoff.p; v->xv = s->gathered ? s->xv.p : nullptr;
+        v->ye = s->gathered ? s->ye.p : nullptr; v->lab = s->gathered ? s->lab.p : nullptr;
+        v->draws = s->draws.p; v->decisions = s->decisions.p; v->touched = s->touched.p;
+        v->touched_count = s->tcount.p; v->touched_stride = s->touched_stride;
+        v->level_counts = s->level_counts.p;
+    });
+}
+
+int hgs_sample_kernel_times(hgs_sample* s, float* ms) {
+    return guarded([&] {
+        if (!s || !s->profiled) fail(HGS_EINVAL, "hgs_sample_kernel_times: last run was not profiled");
+        HGS_CUDA(cudaSetDevice(s->graph->g.device));
+        HGS_CUDA(cudaEventSynchronize(s->ev[3]));
+        HGS_CUDA(cudaEventElapsedTime(&ms[0], s->ev[0], s->ev[1]));
+        HGS_CUDA(cudaEventElapsedTime(&ms[1], s->ev[1], s->ev[2]));
+        HGS_CUDA(cudaEventElapsedTime(&ms[2], s->ev[2], s->ev[3]));
+        HGS_CUDA(cudaEventElapsedTime(&ms[3], s->ev[0], s->ev[3]));
+    });
+}
+
+int hgs_sample_launches(hgs_sample* s, int64_t* n) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        *n = s->launches;
+    });
+}
+
+}  // extern "C"

@@ -1,0 +1,333 @@
+// graph.cu — device graph store and K0 (walk CSR build).
+//
+// K0 restates symmetrize_pattern (sparse.cpp:260-272: pattern of A ∪ Aᵀ,
+// canonical = rows ascending, columns strictly ascending) as
+//   (1) a stable LSD radix sort of A's entries by column with the row as
+//       payload — the transpose, whose in-lists come out row-ascending
+//       because the input is row-major;
+//   (2) a per-row merge of the (sorted) out-list with the (sorted) in-list,
+//       dropping duplicates: a count pass, a scan, a write pass.
+// It runs once per graph (ingest), not per sampling call.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cstring>
+
+#include "hgs_internal.cuh"
+
+namespace hgs {
+
+void fail_cuda(cudaError_t e, const char* what) {
+    fail(HGS_ECUDA, std::string("CUDA error ") + cudaGetErrorName(e) + ": " +
+                        cudaGetErrorString(e) + " (" + what + ")");
+}
+
+// ---------------------------------------------------------------------------
+// exclusive scan (int32), out[n] = total
+
+namespace {
+
+constexpr int kScanThreads = 512;
+constexpr int kScanItems = 4;
+constexpr int kScanTile = kScanThreads * kScanItems;
+
+__device__ __forceinline__ int32_t block_excl_scan(int32_t v, int32_t* warp_tot, int32_t& total) {
+    const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
+    const int32_t inc = warp_incl_scan(v);
+    if (lane == 31) warp_tot[warp] = inc;
+    __syncthreads();
+    if (warp == 0) {
+        const int nw = blockDim.x >> 5;
+        int32_t t = lane < nw ? warp_tot[lane] : 0;
+        const int32_t ti = warp_incl_scan(t);
+        if (lane < nw) warp_tot[lane] = ti - t;
+        if (lane == nw - 1) warp_tot[32] = ti;
+    }
+    __syncthreads();
+    total = warp_tot[32];
+    const int32_t r = warp_tot[warp] + inc - v;
+    __syncthreads();
+    return r;
+}
+
+__global__ void k_scan_tiles(const int32_t* __restrict__ in, int32_t* __restrict__ out,
+                             int64_t n, int32_t* __restrict__ tile_sums) {
+    __shared__ int32_t wt[33];
+    const int64_t base = (int64_t)blockIdx.x * kScanTile + (int64_t)threadIdx.x * kScanItems;
+    int32_t x[kScanItems];
+    int32_t s = 0;
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        x[i] = (base + i < n) ? in[base + i] : 0;
+        s += x[i];
+    }
+    int32_t total;
+    int32_t run = block_excl_scan(s, wt, total);
+#pragma unroll
+    for (int i = 0; i < kScanItems; ++i) {
+        if (base + i < n) out[base + i] = run;
+        run += x[i];
+    }
+    if (threadIdx.x == 0) tile_sums[blockIdx.x] = total;
+}
+
+__global__ void k_scan_add(int32_t* __restrict__ out, int64_t n,
+                           const int32_t* __restrict__ tile_off) {
+    const int64_t base = (int64_t)blockIdx.x * kScanTile;
+    const int32_t add = tile_off[blockIdx.x];
+    for (int i = threadIdx.x; i < kScanTile; i += blockDim.x)
+        if (base + i < n) out[base + i] += add;
+}
+
+__global__ void k_set_total(int32_t* out, int64_t n, const int32_t* tile_off, int64_t tiles) {
+    out[n] = tile_off[tiles];
+}
+
+}  // namespace
+
+void scan_exclusive_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t st) {
+    if (n <= 0) {
+        HGS_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), st));
+        return;
+    }
+    const int64_t tiles = (n + kScanTile - 1) / kScanTile;
+    if (tiles == 1) {  // one tile: its sum is the total
+        k_scan_tiles<<<1, kScanThreads, 0, st>>>(in, out, n, out + n);
+        HGS_CUDA(cudaGetLastError());
+        return;
+    }
+    int32_t* sums = nullptr;
+    HGS_CUDA(cudaMallocAsync(&sums, sizeof(int32_t) * (2 * tiles + 2), st));
+    int32_t* offs = sums + tiles + 1;
+    k_scan_tiles<<<(unsigned)tiles, kScanThreads, 0, st>>>(in, out, n, sums);
+    HGS_CUDA(cudaGetLastError());
+    scan_exclusive_i32(sums, offs, tiles, st);  // offs[tiles] = total
+    k_scan_add<<<(unsigned)tiles, kScanThreads, 0, st>>>(out, n, offs);
+    k_set_total<<<1, 1, 0, st>>>(out, n, offs, tiles);
+    HGS_CUDA(cudaGetLastError());
+    HGS_CUDA(cudaFreeAsync(sums, st));
+}
+
+// ---------------------------------------------------------------------------
+// stable LSD radix sort of (uint32 key, int32 value) pairs, 8-bit digits.
+// Each 256-thread block owns a tile of 2048 keys; every warp a contiguous
+// 256-key sub-tile it walks in order, so ranks are stable: peers with the
+// same digit are ranked with __match_any_sync + lane order, warps in warp
+// order, tiles in tile order (digit-major histogram scan).
+
+namespace {
+
+constexpr int kRadix = 256;
+constexpr int kSortThreads = 256;
+constexpr int kWarpKeys = 256;
+constexpr int kSortTile = (kSortThreads / 32) * kWarpKeys;
+
+__global__ void k_radix_hist(const uint32_t* __restrict__ keys, int64_t n, int shift,
+                             int32_t* __restrict__ hist, int64_t tiles) {
+    __shared__ int32_t cnt[kRadix];
+    for (int i = threadIdx.x; i < kRadix; i += blockDim.x) cnt[i] = 0;
+    __syncthreads();
+    const int64_t base = (int64_t)blockIdx.x * kSortTile;
+    for (int i = threadIdx.x; i < kSortTile; i += blockDim.x)
+        if (base + i < n) atomicAdd(&cnt[(keys[base + i] >> shift) & 0xff], 1);
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += blockDim.x) hist[(int64_t)d * tiles + blockIdx.x] = cnt[d];
+}
+
+__global__ void k_radix_scatter(const uint32_t* __restrict__ keys, const int32_t* __restrict__ vals,
+                                int64_t n, int shift, const int32_t* __restrict__ offs,
+                                int64_t tiles, uint32_t* __restrict__ okeys,
+                                int32_t* __restrict__ ovals) {
+    __shared__ int32_t wc[kSortThreads / 32][kRadix];
+    const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+    for (int i = threadIdx.x; i < (kSortThreads / 32) * kRadix; i += blockDim.x) (&wc[0][0])[i] = 0;
+    __syncthreads();
+    const int64_t wbase = (int64_t)blockIdx.x * kSortTile + (int64_t)warp * kWarpKeys;
+    for (int step = 0; step < kWarpKeys / 32; ++step) {
+        const int64_t idx = wbase + step * 32 + lane;
+        const bool ok = idx < n;
+        const unsigned act = __ballot_sync(kFull, ok);
+        if (ok) {
+            const uint32_t d = (keys[idx] >> shift) & 0xff;
+            const unsigned peers = __match_any_sync(act, d);
+            if ((__ffs(peers) - 1) == lane) wc[warp][d] += __popc(peers);
+        }
+        __syncwarp();
+    }
+    __syncthreads();
+    for (int d = threadIdx.x; d < kRadix; d += blockDim.x) {
+        int32_t run = offs[(int64_t)d * tiles + blockIdx.x];
+        for (int w = 0; w < kSortThreads / 32; ++w) {
+            const int32_t t = wc[w][d];
+            wc[w][d] = run;
+            run += t;
+        }
+    }
+    __syncthreads();
+    for (int step = 0; step < kWarpKeys / 32; ++step) {
+        const int64_t idx = wbase + step * 32 + lane;
+        const bool ok = idx < n;
+        const unsigned act = __ballot_sync(kFull, ok);
+        uint32_t key = 0, d = 0;
+        unsigned peers = 0;
+        int32_t pos = 0;
+        if (ok) {
+            key = keys[idx];
+            d = (key >> shift) & 0xff;
+            peers = __match_any_sync(act, d);
+            pos = wc[warp][d] + __popc(peers & ((1u << lane) - 1u));
+            okeys[pos] = key;
+            ovals[pos] = vals[idx];
+        }
+        __syncwarp();
+        if (ok && (__ffs(peers) - 1) == lane) wc[warp][d] += __popc(peers);
+        __syncwarp();
+    }
+}
+
+}  // namespace
+
+// Sorts (keys, vals) in place using the given temporaries; key_bits = number
+// of low bits that can be nonzero.
+static void radix_sort_pairs(uint32_t* keys, int32_t* vals, uint32_t* tkeys, int32_t* tvals,
+                             int64_t n, int key_bits, cudaStream_t st) {
+    if (n <= 1) return;
+    const int64_t tiles = (n + kSortTile - 1) / kSortTile;
+    int32_t* hist = nullptr;
+    HGS_CUDA(cudaMallocAsync(&hist, sizeof(int32_t) * (kRadix * tiles * 2 + 1), st));
+    int32_t* offs = hist + kRadix * tiles;
+    uint32_t *ka = keys, *kb = tkeys;
+    int32_t *va = vals, *vb = tvals;
+    int passes = 0;
+    for (int shift = 0; shift < key_bits; shift += 8, ++passes) {
+        k_radix_hist<<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, n, shift, hist, tiles);
+        scan_exclusive_i32(hist, offs, kRadix * tiles, st);
+        k_radix_scatter<<<(unsigned)tiles, kSortThreads, 0, st>>>(ka, va, n, shift, offs, tiles, kb, vb);
+        HGS_CUDA(cudaGetLastError());
+        std::swap(ka, kb);
+        std::swap(va, vb);
+    }
+    if (passes & 1) {
+        HGS_CUDA(cudaMemcpyAsync(keys, ka, sizeof(uint32_t) * n, cudaMemcpyDeviceToDevice, st));
+        HGS_CUDA(cudaMemcpyAsync(vals, va, sizeof(int32_t) * n, cudaMemcpyDeviceToDevice, st));
+    }
+    HGS_CUDA(cudaFreeAsync(hist, st));
+}
+
+// ---------------------------------------------------------------------------
+// K0 kernels
+
+namespace {
+
+__global__ void k_row_ids(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ rows) {
+    for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x)
+        for (int32_t k = rp[u]; k < rp[u + 1]; ++k) rows[k] = u;
+}
+
+// t_rp[v] = first position of key >= v in the sorted column keys.
+__global__ void k_lower_bound(const uint32_t* __restrict__ sorted, int64_t nnz, int32_t n,
+                              int32_t* __restrict__ t_rp) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v <= n; v += gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = nnz;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if (sorted[mid] < (uint32_t)v) lo = mid + 1; else hi = mid;
+        }
+        t_rp[v] = (int32_t)lo;
+    }
+}
+
+// Merge out-list and in-list of row u (both ascending), unique. WRITE=false
+// counts into cnt[u]; WRITE=true writes at w_ci[w_rp[u]...].
+template <bool WRITE>
+__global__ void k_merge_rows(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                             const int32_t* __restrict__ t_rp, const int32_t* __restrict__ t_ci,
+                             int32_t n, int32_t* __restrict__ cnt, const int32_t* __restrict__ w_rp,
+                             int32_t* __restrict__ w_ci, int32_t* __restrict__ max_deg) {
+    for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        int32_t i = rp[u];
+        const int32_t ie = rp[u + 1];
+        int32_t j = t_rp[u];
+        const int32_t je = t_rp[u + 1];
+        int32_t w = WRITE ? w_rp[u] : 0;
+        int32_t c = 0;
+        int64_t last = -1;
+        while (i < ie || j < je) {
+            int32_t v;
+            if (j >= je || (i < ie && ci[i] <= t_ci[j])) v = ci[i++];
+            else v = t_ci[j++];
+            if (v == last) continue;
+            last = v;
+            if (WRITE) w_ci[w++] = v;
+            ++c;
+        }
+        if (!WRITE) {
+            cnt[u] = c;
+            atomicMax(max_deg, c);
+        }
+    }
+}
+
+__global__ void k_recip(uint64_t* r, int32_t n) {
+    for (int32_t m = blockIdx.x * blockDim.x + threadIdx.x; m < n; m += gridDim.x * blockDim.x)
+        r[m] = m ? (~0ULL / (uint64_t)m) : 0ULL;
+}
+
+}  // namespace
+
+void graph_build_walk_sym(DevGraph& g) {
+    if (g.sym_built) return;
+    const DevCsr& a = g.full_pattern();
+    const int32_t n = a.n;
+    const int64_t nnz = a.nnz;
+    cudaStream_t st = g.stream;
+    DevCsr& w = g.walk_sym;
+    w.n = n;
+    w.rp.reserve((size_t)n + 1);
+    DevBuf<uint32_t> keys, tkeys;
+    DevBuf<int32_t> vals, tvals, t_rp, cnt, maxd;
+    keys.reserve(nnz); tkeys.reserve(nnz); vals.reserve(nnz); tvals.reserve(nnz);
+    t_rp.reserve((size_t)n + 1); cnt.reserve((size_t)n + 1); maxd.reserve(1);
+    const int threads = 256;
+    const unsigned rows_grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + threads - 1) / threads, 1 << 16));
+    if (nnz > 0) {
+        HGS_CUDA(cudaMemcpyAsync(keys.p, a.ci.p, sizeof(int32_t) * nnz, cudaMemcpyDeviceToDevice, st));
+        k_row_ids<<<rows_grid, threads, 0, st>>>(a.rp.p, n, vals.p);
+        int bits = 1;
+        while (bits < 32 && ((int64_t)1 << bits) < (int64_t)n) ++bits;
+        radix_sort_pairs(keys.p, vals.p, tkeys.p, tvals.p, nnz, bits, st);
+    }
+    k_lower_bound<<<(unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 1 + threads - 1) / threads, 1 << 16)), threads, 0, st>>>(
+        keys.p, nnz, n, t_rp.p);
+    HGS_CUDA(cudaMemsetAsync(maxd.p, 0, sizeof(int32_t), st));
+    k_merge_rows<false><<<rows_grid, threads, 0, st>>>(a.rp.p, a.ci.p, t_rp.p, vals.p, n, cnt.p,
+                                                       nullptr, nullptr, maxd.p);
+    HGS_CUDA(cudaGetLastError());
+    scan_exclusive_i32(cnt.p, w.rp.p, n, st);
+    int32_t h[2];
+    HGS_CUDA(cudaMemcpyAsync(&h[0], w.rp.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaMemcpyAsync(&h[1], maxd.p, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaStreamSynchronize(st));
+    w.nnz = h[0];
+    w.max_deg = h[1];
+    w.ci.reserve((size_t)w.nnz);
+    k_merge_rows<true><<<rows_grid, threads, 0, st>>>(a.rp.p, a.ci.p, t_rp.p, vals.p, n, nullptr,
+                                                      w.rp.p, w.ci.p, nullptr);
+    HGS_CUDA(cudaGetLastError());
+    HGS_CUDA(cudaStreamSynchronize(st));
+    g.sym_built = true;
+    graph_ensure_recip(g, w.max_deg);
+}
+
+void graph_ensure_recip(DevGraph& g, int32_t max_m) {
+    const int32_t need = max_m + 1;
+    if (need <= g.recip_n) return;
+    g.recip.release();
+    g.recip.reserve((size_t)need);
+    k_recip<<<(unsigned)std::max(1, std::min((need + 255) / 256, 1 << 16)), 256, 0, g.stream>>>(g.recip.p, need);
+    HGS_CUDA(cudaGetLastError());
+    HGS_CUDA(cudaStreamSynchronize(g.stream));
+    g.recip_n = need;
+}
+
+}  // namespace hgs

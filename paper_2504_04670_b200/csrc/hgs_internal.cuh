@@ -1,0 +1,210 @@
+// hgs_internal.cuh — device graph store, workspaces and shared device helpers.
+#pragma once
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <stdexcept>
+#include <string>
+#include <vector>
+
+#include "hgs.h"
+#include "hgs_rng.cuh"
+
+namespace hgs {
+
+// Failure carried up to the C ABI: code = HGS_E*, message = reference text.
+struct Failure : std::runtime_error {
+    int code;
+    Failure(int c, const std::string& m) : std::runtime_error(m), code(c) {}
+};
+[[noreturn]] inline void fail(int code, const std::string& msg) { throw Failure(code, msg); }
+[[noreturn]] void fail_cuda(cudaError_t e, const char* what);
+
+#define HGS_CUDA(expr)                                          \
+    do {                                                        \
+        cudaError_t hgs_e_ = (expr);                            \
+        if (hgs_e_ != cudaSuccess) ::hgs::fail_cuda(hgs_e_, #expr); \
+    } while (0)
+
+// Grow-only device buffer.
+template <class T>
+struct DevBuf {
+    T* p = nullptr;
+    size_t cap = 0;
+    void reserve(size_t n) {
+        if (n <= cap) return;
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+        HGS_CUDA(cudaMalloc(&p, (n ? n : 1) * sizeof(T)));
+        cap = n;
+    }
+    void release() {
+        if (p) cudaFree(p);
+        p = nullptr;
+        cap = 0;
+    }
+    ~DevBuf() { release(); }
+    DevBuf() = default;
+    DevBuf(const DevBuf&) = delete;
+    DevBuf& operator=(const DevBuf&) = delete;
+};
+
+// One CSR pattern on the device (int32 positions; n, nnz < 2^31).
+struct DevCsr {
+    DevBuf<int32_t> rp, ci;
+    int32_t n = 0;
+    int64_t nnz = 0;
+    int32_t max_deg = 0;
+};
+
+// Device-resident event: the extraction matrix A (directed, edge ids), the
+// walk matrices the expansion samples from, the bounded() reciprocal table
+// and optional features. Built once per event.
+struct DevGraph {
+    int device = 0;
+    int64_t n_rows = 0, n_cols = 0, nnz = 0;  // as given by the caller
+    DevCsr a;                // extraction matrix: A minus explicit zeros
+    DevBuf<int32_t> a_gid;   // a position -> input CSR position (only if zeros dropped)
+    bool has_gid = false;
+    DevCsr a_full;           // full pattern of A (only if zeros dropped; else == a)
+    bool has_full = false;
+    DevCsr walk_sym;         // pattern(A ∪ Aᵀ), built lazily by K0
+    bool sym_built = false;
+    DevBuf<uint8_t> neg_row; // rows of A holding a negative value (only if any)
+    bool has_neg = false;
+    DevBuf<uint64_t> recip;  // recip[m] = floor((2^64-1)/m), m in [1, recip_n)
+    int32_t recip_n = 0;
+    // features (gather_features)
+    DevBuf<double> node_feat, edge_feat;
+    DevBuf<uint8_t> labels;
+    int32_t f_v = 0, f_e = 0;
+    bool has_features = false;
+    cudaStream_t stream = nullptr;  // ingest stream
+
+    const DevCsr& full_pattern() const { return has_full ? a_full : a; }
+};
+
+void graph_build_walk_sym(DevGraph& g);  // K0 (graph.cu)
+
+// Inputs of one sampling call (device pointers).
+struct CallInputs {
+    const int32_t* roots32 = nullptr;  // one of roots32 / roots64
+    const int64_t* roots64 = nullptr;
+    const int64_t* batch_off = nullptr;
+    const uint64_t* seeds = nullptr;
+    const uint64_t* state = nullptr;
+    int64_t R = 0, k = 0;
+};
+void graph_ensure_recip(DevGraph& g, int32_t max_m);
+
+// Device exclusive scan: out[0..n] with out[n] = total (int32, total < 2^31).
+void scan_exclusive_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t st);
+
+// ---- warp helpers -----------------------------------------------------------
+#if defined(__CUDACC__)
+constexpr unsigned kFull = 0xffffffffu;
+
+__device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+template <class T>
+__device__ __forceinline__ T warp_incl_scan(T v) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        T u = __shfl_up_sync(kFull, v, o);
+        if (lane >= o) v += u;
+    }
+    return v;
+}
+
+template <class T>
+__device__ __forceinline__ T warp_sum(T v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+}
+
+// Bitonic sort of 32*E keys held lane-major (lane l owns keys l*E .. l*E+E-1),
+// ascending. Intra-lane stages are register compare-exchanges; inter-lane
+// stages exchange through shuffles.
+template <int E>
+__device__ __forceinline__ void warp_bitonic_sort(uint32_t (&k)[E]) {
+    const int lane = lane_id();
+#pragma unroll
+    for (int size = 2; size <= 32 * E; size <<= 1) {
+#pragma unroll
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            if (stride >= E) {
+                const int lm = stride / E;
+                const bool lower = (lane & lm) == 0;
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    const bool up = (((lane * E + e) & size) == 0);
+                    const uint32_t other = __shfl_xor_sync(kFull, k[e], lm);
+                    const bool keep_min = (lower == up);
+                    k[e] = keep_min ? min(k[e], other) : max(k[e], other);
+                }
+            } else {
+#pragma unroll
+                for (int e = 0; e < E; ++e) {
+                    if ((e & stride) == 0) {
+                        const int e2 = e | stride;
+                        const bool up = (((lane * E + e) & size) == 0);
+                        const uint32_t x = k[e], y = k[e2];
+                        const bool sw = up ? (x > y) : (x < y);
+                        k[e] = sw ? y : x;
+                        k[e2] = sw ? x : y;
+                    }
+                }
+            }
+        }
+    }
+}
+#endif
+
+}  // namespace hgs
+
+// Opaque handle types of the C ABI.
+struct hgs_graph {
+    hgs::DevGraph g;
+};
+
+struct hgs_sample {
+    hgs_graph* graph = nullptr;
+    cudaStream_t stream = nullptr;
+    bool own_stream = false;
+    // inputs (device copies of host inputs)
+    hgs::DevBuf<int64_t> roots64, boff64;
+    hgs::DevBuf<uint64_t> seeds, rng_state;
+    hgs::CallInputs last_in;
+    hgs_config last_cfg{};
+    // expand scratch
+    hgs::DevBuf<int32_t> touched, tcount, level_counts;
+    hgs::DevBuf<uint32_t> draws, decisions;
+    int64_t touched_stride = 0;
+    // look-back state
+    hgs::DevBuf<unsigned long long> status, bbase;
+    hgs::DevBuf<int32_t> ticket;  // [0]=ticket [1]=error code [2..3]=error detail
+    // outputs
+    hgs::DevBuf<int32_t> l2g, roots_local, comp_off, batch_voff, batch_eoff;
+    hgs::DevBuf<int32_t> e_row, e_col, e_gid, root_voff, root_eoff;
+    hgs::DevBuf<double> xv, ye;
+    hgs::DevBuf<uint8_t> lab;
+    size_t v_cap = 0, e_cap = 0;
+    // pinned host mirror of small per-call state
+    int32_t* h_state = nullptr;  // [0..3] error flags, [4]=V, [5]=E
+    // last call
+    int64_t R = 0, k = 0, V = 0, E = 0;
+    int64_t depth = 0, fanout = 0;
+    int32_t gathered = 0, symmetrize = 1, rng = 0;
+    bool pending = false;
+    bool profiled = false;
+    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    int64_t launches = 0;
+};
+
+namespace hgs {
+void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in);
+void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in);
+}  // namespace hgs

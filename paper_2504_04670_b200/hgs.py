@@ -1,0 +1,291 @@
+"""Python bindings (ctypes) of the C ABI in include/hgs.h.
+
+Mirrors the reference's sampler API shape for use from Python harnesses
+(tests, bench): a device-resident :class:`Graph` (one per event, the
+reference's ``make_edge_id_matrix`` + features) and a reusable
+:class:`Sampler` workspace whose :meth:`Sampler.bulk_shadow` is
+``hitgnn::bulk_shadow`` (+ ``gather_features`` when ``gather=True``).
+
+There is no CPU fallback: if ``lib/libhgs.so`` is missing or no CUDA device
+is visible, every sampling call raises.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_PKG, "lib", "libhgs.so")
+
+HGS_OK, HGS_EINVAL, HGS_ECUDA, HGS_ERANGE = 0, 1, 2, 3
+RNG_XOSHIRO, RNG_PHILOX = 0, 1
+
+# Exported symbols declared in include/hgs.h (checked by tests/test_abi.py).
+EXPORTS = [
+    "hgs_last_error", "hgs_abi_version", "hgs_device_count", "hgs_graph_create",
+    "hgs_graph_attach_features", "hgs_graph_info", "hgs_graph_walk", "hgs_graph_destroy",
+    "hgs_sample_create", "hgs_sample_destroy", "hgs_sample_run", "hgs_sample_run_device",
+    "hgs_sample_wait", "hgs_sample_copy_to_host", "hgs_sample_device_views",
+    "hgs_sample_kernel_times", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
+]
+
+
+class SamplerError(ValueError):
+    """std::invalid_argument of the reference (HGS_EINVAL)."""
+
+
+class HgsRuntimeError(RuntimeError):
+    """CUDA / runtime failure or implementation limit (HGS_ECUDA, HGS_ERANGE)."""
+
+
+class Config(C.Structure):
+    _fields_ = [("depth", C.c_int64), ("fanout", C.c_int64), ("batch_size", C.c_int64),
+                ("bulk_batches", C.c_int64), ("symmetrize", C.c_int32), ("rng", C.c_int32),
+                ("gather", C.c_int32), ("profile", C.c_int32)]
+
+
+class HostOut(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("batch_voff", "batch_eoff", "comp_off", "l2g",
+                                            "roots_local", "e_row", "e_col", "e_gid", "xv", "ye",
+                                            "lab", "draws", "decisions")]
+
+
+class DeviceViews(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("batch_voff", "batch_eoff", "comp_off", "l2g",
+                                            "roots_local", "e_row", "e_col", "e_gid",
+                                            "root_voff", "root_eoff", "xv", "ye", "lab", "draws",
+                                            "decisions", "touched", "touched_count",
+                                            "level_counts")] + [("touched_stride", C.c_int64)]
+
+
+_lib_cache: C.CDLL | None = None
+
+
+def lib() -> C.CDLL:
+    global _lib_cache
+    if _lib_cache is None:
+        if not os.path.exists(LIB_PATH):
+            raise HgsRuntimeError(
+                f"{LIB_PATH} is missing: build it with `python -m paper_2504_04670_b200.build` "
+                "(no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        vp, i64, i32 = C.c_void_p, C.c_int64, C.c_int32
+        L.hgs_last_error.restype = C.c_char_p
+        L.hgs_derive.restype = C.c_uint64
+        L.hgs_derive.argtypes = [C.c_uint64, vp, i32]
+        L.hgs_philox4x32_10.argtypes = [vp, vp, vp]
+        L.hgs_device_count.argtypes = [C.POINTER(C.c_int)]
+        L.hgs_graph_create.argtypes = [C.c_int, i64, i64, vp, vp, vp, C.POINTER(vp)]
+        L.hgs_graph_attach_features.argtypes = [vp, vp, i64, vp, i64, vp]
+        L.hgs_graph_info.argtypes = [vp, vp]
+        L.hgs_graph_walk.argtypes = [vp, i32, vp, vp]
+        L.hgs_graph_destroy.argtypes = [vp]
+        L.hgs_sample_create.argtypes = [vp, vp, C.POINTER(vp)]
+        L.hgs_sample_destroy.argtypes = [vp]
+        L.hgs_sample_run.argtypes = [vp, C.POINTER(Config), vp, vp, i64, vp, vp]
+        L.hgs_sample_run_device.argtypes = [vp, C.POINTER(Config), vp, vp, i64, i64, vp]
+        L.hgs_sample_wait.argtypes = [vp, vp]
+        L.hgs_sample_copy_to_host.argtypes = [vp, C.POINTER(HostOut)]
+        L.hgs_sample_device_views.argtypes = [vp, C.POINTER(DeviceViews)]
+        L.hgs_sample_kernel_times.argtypes = [vp, vp]
+        L.hgs_sample_launches.argtypes = [vp, vp]
+        _lib_cache = L
+    return _lib_cache
+
+
+def _check(rc: int) -> None:
+    if rc == HGS_OK:
+        return
+    msg = lib().hgs_last_error().decode()
+    if rc == HGS_EINVAL:
+        raise SamplerError(msg)
+    raise HgsRuntimeError(msg)
+
+
+def _p(a):
+    return None if a is None else C.c_void_p(a.ctypes.data)
+
+
+def device_count() -> int:
+    c = C.c_int(0)
+    _check(lib().hgs_device_count(C.byref(c)))
+    return c.value
+
+
+def derive(seed: int, path) -> int:
+    p = np.ascontiguousarray(path, dtype=np.uint64)
+    return int(lib().hgs_derive(C.c_uint64(seed), _p(p), len(p)))
+
+
+def derive_many(seed: int, prefix, n_batches: int, batch_size: int) -> np.ndarray:
+    """Per-root seeds derive(seed, prefix + [bi, pos]) for the bench protocol
+    (cli.cpp:401-408) and trainer streams (trainer.cpp:200-206)."""
+    out = np.empty(n_batches * batch_size, np.uint64)
+    pre = list(prefix)
+    w = 0
+    for bi in range(n_batches):
+        for pos in range(batch_size):
+            out[w] = derive(seed, pre + [bi, pos])
+            w += 1
+    return out
+
+
+def philox4x32_10(ctr, key) -> np.ndarray:
+    c = np.ascontiguousarray(ctr, np.uint32)
+    k = np.ascontiguousarray(key, np.uint32)
+    o = np.zeros(4, np.uint32)
+    lib().hgs_philox4x32_10(_p(c), _p(k), _p(o))
+    return o
+
+
+class Graph:
+    """Device-resident event graph (CSR A with edge ids; optional features)."""
+
+    def __init__(self, row_ptr, col_idx, values=None, n_cols=None, device=0):
+        rp = np.ascontiguousarray(row_ptr, np.int64)
+        ci = np.ascontiguousarray(col_idx, np.int64)
+        va = None if values is None else np.ascontiguousarray(values, np.float64)
+        self.n = len(rp) - 1
+        self.n_cols = self.n if n_cols is None else int(n_cols)
+        self.nnz = int(rp[-1])
+        self._h = C.c_void_p()
+        _check(lib().hgs_graph_create(device, self.n, self.n_cols, _p(rp), _p(ci), _p(va),
+                                      C.byref(self._h)))
+        self.f_v = self.f_e = 0
+
+    def attach_features(self, node_feat, edge_feat, labels):
+        nf = np.ascontiguousarray(node_feat, np.float64)
+        ef = np.ascontiguousarray(edge_feat, np.float64)
+        lb = np.ascontiguousarray(labels, np.uint8)
+        self.f_v = nf.shape[1] if nf.ndim == 2 else (nf.size // max(self.n, 1))
+        self.f_e = ef.shape[1] if ef.ndim == 2 else (ef.size // max(self.nnz, 1))
+        _check(lib().hgs_graph_attach_features(self._h, _p(nf), self.f_v, _p(ef), self.f_e,
+                                               _p(lb)))
+        return self
+
+    def info(self) -> dict:
+        a = np.zeros(8, np.int64)
+        _check(lib().hgs_graph_info(self._h, _p(a)))
+        keys = ["n_rows", "n_cols", "nnz", "walk_nnz", "max_walk_deg", "max_out_deg", "f_v", "f_e"]
+        return dict(zip(keys, (int(x) for x in a)))
+
+    def walk(self, symmetrize=True):
+        info = self.info()
+        nnz = info["walk_nnz"] if symmetrize else self.nnz
+        rp = np.zeros(self.n + 1, np.int64)
+        ci = np.zeros(max(nnz, 1), np.int64)
+        _check(lib().hgs_graph_walk(self._h, int(symmetrize), _p(rp), _p(ci)))
+        return rp, ci[:int(rp[-1])]
+
+    def close(self):
+        if self._h:
+            lib().hgs_graph_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+
+@dataclass
+class SampleCounts:
+    R: int
+    k: int
+    V: int
+    E: int
+
+
+class Sampler:
+    """A reusable device workspace bound to one Graph and one CUDA stream."""
+
+    def __init__(self, graph: Graph, stream: int | None = None):
+        self.graph = graph
+        self._h = C.c_void_p()
+        _check(lib().hgs_sample_create(graph._h, C.c_void_p(stream) if stream else None,
+                                       C.byref(self._h)))
+        self.counts = SampleCounts(0, 0, 0, 0)
+        self.gathered = False
+
+    @staticmethod
+    def config(depth=3, fanout=6, symmetrize=True, rng=RNG_XOSHIRO, gather=False, profile=False,
+               batch_size=1, bulk_batches=1) -> Config:
+        return Config(depth, fanout, batch_size, bulk_batches, int(symmetrize), int(rng),
+                      int(gather), int(profile))
+
+    def bulk_shadow(self, roots, batch_off, seeds, *, state=None, **cfg) -> SampleCounts:
+        """hitgnn::bulk_shadow (+ gather_features) from host arrays; blocks."""
+        r = np.ascontiguousarray(roots, np.int64)
+        b = np.ascontiguousarray(batch_off, np.int64)
+        s = np.ascontiguousarray(seeds, np.uint64)
+        st = None if state is None else np.ascontiguousarray(state, np.uint64)
+        c = self.config(**cfg)
+        _check(lib().hgs_sample_run(self._h, C.byref(c), _p(r), _p(b), len(b) - 1, _p(s), _p(st)))
+        self.gathered = bool(c.gather)
+        return self.wait()
+
+    def run_device(self, d_roots: int, d_batch_off: int, n_roots: int, n_batches: int,
+                   d_seeds: int, **cfg) -> None:
+        """Enqueue with device pointers (int32 roots, int64 batch_off, u64 seeds)."""
+        c = self.config(**cfg)
+        self.gathered = bool(c.gather)
+        _check(lib().hgs_sample_run_device(self._h, C.byref(c), C.c_void_p(d_roots),
+                                           C.c_void_p(d_batch_off), n_roots, n_batches,
+                                           C.c_void_p(d_seeds)))
+
+    def wait(self) -> SampleCounts:
+        a = np.zeros(4, np.int64)
+        _check(lib().hgs_sample_wait(self._h, _p(a)))
+        self.counts = SampleCounts(*(int(x) for x in a))
+        return self.counts
+
+    def alloc_host(self, pinned_alloc=None) -> dict:
+        c = self.counts
+        g = self.graph
+        mk = pinned_alloc or (lambda n, dt: np.empty(n, dt))
+        out = dict(batch_voff=mk(c.k + 1, np.int32), batch_eoff=mk(c.k + 1, np.int32),
+                   comp_off=mk(c.R + c.k, np.int32), l2g=mk(c.V, np.int32),
+                   roots_local=mk(c.R, np.int32), e_row=mk(c.E, np.int32),
+                   e_col=mk(c.E, np.int32), e_gid=mk(c.E, np.int32),
+                   draws=mk(c.R, np.uint32), decisions=mk(c.R, np.uint32))
+        if self.gathered:
+            out.update(xv=mk(c.V * g.f_v, np.float64), ye=mk(c.E * g.f_e, np.float64),
+                       lab=mk(c.E, np.uint8))
+        return out
+
+    def to_host(self, out: dict | None = None) -> dict:
+        out = out if out is not None else self.alloc_host()
+        ho = HostOut(**{k: (v.ctypes.data if v is not None and v.size else None)
+                        for k, v in out.items()})
+        _check(lib().hgs_sample_copy_to_host(self._h, C.byref(ho)))
+        return out
+
+    def device_views(self) -> DeviceViews:
+        v = DeviceViews()
+        _check(lib().hgs_sample_device_views(self._h, C.byref(v)))
+        return v
+
+    def kernel_times(self) -> np.ndarray:
+        ms = np.zeros(4, np.float32)
+        _check(lib().hgs_sample_kernel_times(self._h, _p(ms)))
+        return ms
+
+    def launches(self) -> int:
+        n = np.zeros(1, np.int64)
+        _check(lib().hgs_sample_launches(self._h, _p(n)))
+        return int(n[0])
+
+    def close(self):
+        if self._h:
+            lib().hgs_sample_destroy(self._h)
+            self._h = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
