@@ -1,0 +1,382 @@
+#!/usr/bin/env python
+"""bench.py — bulk ShaDow sampling throughput on B200 (BASELINE.json metric).
+
+One step = one bulk_shadow + gather_features call (the trainer's `sample_s`
+region, reference trainer.cpp:456-459) over k=64 minibatches x 1024 roots of
+the synthetic TrackML-shaped event C2 (n=120,373 hits, m=1,509,282 edges),
+depth 3, fanout 6, symmetrized walk, per-root xoshiro streams
+(PerRootChoiceSource) — BASELINE.json configs[1]. Roots and seeds follow the
+reference's `bench-sampling` protocol (cli.cpp:381-408) with rep = step index.
+
+  value  device-resident throughput: inputs already in HBM, CUDA events on the
+         launching stream around each step, L2 flushed (512 MiB memset)
+         before every timed step; minibatches/s over all ranks (max rank time).
+  e2e    the same metric through the C ABI with host buffers: pinned H2D of
+         roots/offsets/seeds, the call, and D2H of every output array the
+         reference API returns (vertex maps, edges, edge ids, gathered node/edge
+         features, labels), wall-clocked.
+  roofline  of the dominant kernel (k_extract): algorithmic bytes per launch
+         (SURVEY.md §8(d) model) / its CUDA-event duration.
+  cpu_baseline  the reference CPU sampler (oracle/_ref: the unmodified
+         reference sources built by oracle/Makefile) on a bounded sample, all
+         host threads, batch-sharded.
+
+Multi-GPU (torchrun): weak scaling — every rank samples its own 64 batches
+(rep offset by rank); no collective on the data path; timing = max over ranks.
+`--impl reference` times the reference CPU sampler instead (rank 0 only).
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import subprocess
+import sys
+import tempfile
+import time
+
+import numpy as np
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "sampled minibatches/sec (and edges/sec) at 1/2/4/8 B200; % of HBM roofline"
+UNIT = "minibatches/s"
+K_BATCHES, BATCH, DEPTH, FANOUT = 64, 1024, 3, 6
+WORKLOAD = "C2"
+
+
+def log(*a):
+    print(*a, file=sys.stderr, flush=True)
+
+
+def peaks():
+    p = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(p):
+        with open(p) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured"
+    return 6650.0, "fallback"
+
+
+def config_dict(n_gpus, ev):
+    return {"workload": "C2: synthetic TrackML-shaped event, n=%d hits / m=%d edges, %d minibatches"
+            " x %d seeds per GPU, %d-hop, fanout %d, symmetrized walk, per-root xoshiro streams,"
+            " bulk_shadow+gather_features" % (ev.n, ev.m, K_BATCHES, BATCH, DEPTH, FANOUT),
+            "minibatches_per_step_per_gpu": K_BATCHES, "roots_per_minibatch": BATCH,
+            "depth": DEPTH, "fanout": FANOUT, "parallelism": f"shard{n_gpus} (replicated graph)",
+            "l2": "flushed (512 MiB memset) before every timed step"}
+
+
+# ----------------------------------------------------------------------------
+# clocks
+
+
+class Clocks:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index):
+        self.index = index
+        self.path = tempfile.mktemp(suffix=".csv")
+        self.p = None
+
+    def __enter__(self):
+        try:
+            self.f = open(self.path, "w")
+            self.p = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "100"],
+                                      stdout=self.f, stderr=subprocess.DEVNULL)
+        except Exception:
+            self.p = None
+        return self
+
+    def __exit__(self, *a):
+        if self.p:
+            self.p.terminate()
+            try:
+                self.p.wait(timeout=5)
+            except Exception:
+                self.p.kill()
+            self.f.close()
+
+    def summary(self):
+        rows = []
+        try:
+            with open(self.path) as f:
+                for line in f:
+                    parts = [x.strip() for x in line.split(",")]
+                    if len(parts) >= 9:
+                        rows.append(parts)
+        except Exception:
+            pass
+        if not rows:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["unsampled"], "samples": 0}
+        sm = [float(r[1]) for r in rows if r[1].replace(".", "").isdigit()]
+        mx = [float(r[2]) for r in rows if r[2].replace(".", "").isdigit()]
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        reasons = sorted({names[i] for r in rows for i in range(4) if r[5 + i].lower() == "active"})
+        return {"sm_mhz": float(np.median(sm)) if sm else None,
+                "sm_max_mhz": max(mx) if mx else None, "reasons": reasons, "samples": len(rows)}
+
+
+# ----------------------------------------------------------------------------
+# reference / CPU baseline
+
+
+def cpu_sample_time(ev, n_batches, threads, rep0=1000):
+    """Reference bulk_shadow + gather_features (oracle/_ref) on n_batches of the
+    workload, batch-sharded over `threads`. Falls back to the C restatement
+    ("port") if the reference build is absent."""
+    from oracle import oracle as O
+    from paper_2504_04670_b200 import workload as W
+    roots, boff, seeds = W.bench_roots(ev.n, BATCH, n_batches, seed=1, rep=rep0)
+    g = O.Graph(n=ev.n, rp=ev.rp, ci=ev.ci, node_feat=ev.node_feat, edge_feat=ev.edge_feat,
+                labels=ev.labels)
+    if O.ref_available():
+        t, V, E = O.ref_time_sample(g, roots, boff, seeds, depth=DEPTH, fanout=FANOUT,
+                                    threads=threads)
+        return t, V, E, "reference"
+    t, V, E = O.port_time_sample(g, roots, boff, seeds, depth=DEPTH, fanout=FANOUT,
+                                 threads=threads)
+    return t, V, E, "port"
+
+
+def run_reference(args, world, rank):
+    if rank != 0:
+        return
+    from paper_2504_04670_b200 import workload as W
+    ev = W.preset_event(WORKLOAD)
+    threads = os.cpu_count() or 1
+    nb = max(threads, 8)
+    times = []
+    kind = None
+    for i in range(args.warmup + args.steps):
+        t, V, E, kind = cpu_sample_time(ev, nb, threads, rep0=2000 + i)
+        if i >= args.warmup:
+            times.append(t)
+    total = sum(times)
+    value = nb * len(times) / total
+    line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "impl": "reference", "config": config_dict(world, ev),
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
+                             "sample": f"{nb} minibatches x {BATCH} roots of C2 per step, "
+                                       f"bulk_shadow+gather_features, batch-sharded over "
+                                       f"{threads} threads"},
+            "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------
+# the GPU arm
+
+
+def byte_model(st, f_v, f_e, gather=True):
+    """Algorithmic bytes of one call (split per stage; see
+    DESIGN.md): expand = roots + seeds + offsets + walk row_ptr pairs of the
+    expanded rows + chosen walk col_idx; extract = A row_ptr pairs of the set
+    vertices + scanned A col_idx; pack = the outputs (vtx, comp_off,
+    roots_local, 3 x E edge arrays, batch offsets) + the feature/label gather
+    (read + write). Scratch traffic (touched lists, edge slots) earns nothing."""
+    R, k, V, E, S = st["R"], st["k"], st["V"], st["E"], st["S"]
+    expand = 12 * R + 4 * (k + 1) + 8 * st["F_expand"] + 4 * st["F_children"]
+    extract = 8 * V + 4 * S
+    pack = 4 * V + 4 * (R + k) + 4 * R + 12 * E + 8 * (k + 1)
+    if gather:
+        pack += 16 * f_v * V + (16 * f_e + 2) * E
+    return expand, extract, pack
+
+
+def run_gpu(args, world, rank, local_rank):
+    import torch
+    import torch.distributed as dist
+    from paper_2504_04670_b200 import hgs, workload as W
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    t0 = time.time()
+    ev = W.preset_event(WORKLOAD)
+    log(f"[rank {rank}] event n={ev.n} m={ev.m} generated in {time.time() - t0:.1f}s")
+    G = hgs.Graph(ev.rp, ev.ci, device=local_rank).attach_features(ev.node_feat, ev.edge_feat,
+                                                                    ev.labels)
+    stream = torch.cuda.Stream(dev)  # a real (non-default) stream shared with the C ABI
+    S = hgs.Sampler(G, stream=stream.cuda_stream)
+    cfg = dict(depth=DEPTH, fanout=FANOUT, symmetrize=True, rng=hgs.RNG_XOSHIRO, gather=True,
+               batch_size=BATCH, bulk_batches=K_BATCHES)
+    nsteps = args.warmup + args.steps
+    host_in, dev_in = [], []
+    for i in range(nsteps):
+        rep = rank * nsteps + i
+        roots, boff, seeds = W.bench_roots(ev.n, BATCH, K_BATCHES, seed=1, rep=rep)
+        host_in.append((roots, boff, seeds))
+        dev_in.append((torch.from_numpy(roots.astype(np.int32)).to(dev),
+                       torch.from_numpy(boff).to(dev),
+                       torch.from_numpy(seeds.view(np.int64)).to(dev)))
+    with torch.cuda.stream(stream):
+        flush = torch.empty(512 << 20, dtype=torch.uint8, device=dev)
+
+    def step_device(i, profile):
+        r, b, s = dev_in[i]
+        S.run_device(r.data_ptr(), b.data_ptr(), r.numel(), b.numel() - 1, s.data_ptr(),
+                     profile=profile, **cfg)
+
+    for i in range(args.warmup):
+        step_device(i, True)
+        S.wait()
+
+    if world > 1:
+        dist.barrier()
+    torch.cuda.synchronize()
+    ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
+    step_ms, kern, stats, launches = [], [], [], 0
+    with Clocks(local_rank) as clk:
+        for j in range(args.steps):
+            i = args.warmup + j
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            ev0[j].record(stream)
+            step_device(i, True)
+            ev1[j].record(stream)
+            S.wait()
+            step_ms.append(ev0[j].elapsed_time(ev1[j]))
+            kern.append(S.kernel_times())
+            launches += S.launches()
+            stats.append(S.stats())
+        torch.cuda.synchronize()
+        if world > 1:
+            dist.barrier()
+        # ---- e2e through the C ABI with host buffers (pinned)
+        cap_v = int(max(s["V"] for s in stats) * 1.25) + 1024
+        cap_e = int(max(s["E"] for s in stats) * 1.25) + 1024
+        R = K_BATCHES * BATCH
+
+        def pin(n, dt):
+            return torch.empty(max(n, 1), dtype=dt, pin_memory=True).numpy()
+
+        hout = dict(batch_voff=pin(K_BATCHES + 1, torch.int32), batch_eoff=pin(K_BATCHES + 1, torch.int32),
+                    comp_off=pin(R + K_BATCHES, torch.int32), l2g=pin(cap_v, torch.int32),
+                    roots_local=pin(R, torch.int32), e_row=pin(cap_e, torch.int32),
+                    e_col=pin(cap_e, torch.int32), e_gid=pin(cap_e, torch.int32),
+                    draws=pin(R, torch.int32).view(np.uint32),
+                    decisions=pin(R, torch.int32).view(np.uint32),
+                    xv=pin(cap_v * G.f_v, torch.float64), ye=pin(cap_e * G.f_e, torch.float64),
+                    lab=pin(cap_e, torch.uint8))
+        hin = []
+        for (roots, boff, seeds) in host_in:
+            pr, pb, ps = pin(len(roots), torch.int64), pin(len(boff), torch.int64), pin(len(seeds), torch.int64)
+            pr[:] = roots
+            pb[:] = boff
+            ps[:] = seeds.view(np.int64)
+            hin.append((pr, pb, ps.view(np.uint64)))
+        e2e_s, h2d, d2h = [], 0, 0
+        for i in range(nsteps):
+            pr, pb, ps = hin[i]
+            torch.cuda.synchronize()
+            t1 = time.perf_counter()
+            c = S.bulk_shadow(pr, pb, ps, **cfg)
+            S.to_host(hout)
+            t2 = time.perf_counter()
+            if i >= args.warmup:
+                e2e_s.append(t2 - t1)
+                h2d = pr.nbytes + pb.nbytes + ps.nbytes
+                d2h = (4 * 2 * (c.k + 1) + 4 * (c.R + c.k) + 4 * c.V + 4 * c.R + 12 * c.E
+                       + 8 * c.V * G.f_v + 8 * c.E * G.f_e + c.E + 8 * c.R)
+    total_ms = float(sum(step_ms))
+    e2e_total = float(sum(e2e_s))
+    if world > 1:
+        t = torch.tensor([total_ms, e2e_total], device=dev, dtype=torch.float64)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        total_ms, e2e_total = float(t[0]), float(t[1])
+    if rank != 0:
+        return
+    mb = world * K_BATCHES * args.steps
+    value = mb / (total_ms / 1e3)
+    edges = sum(s["E"] for s in stats)
+    kern = np.array(kern)
+    kt_mean = kern.mean(axis=0)  # expand, extract, scan, pack, finalize, total
+    bm = np.mean([byte_model(s, G.f_v, G.f_e, True) for s in stats], axis=0)
+    b_exp, b_ext, b_pack = (float(x) for x in bm)
+    bt = b_exp + b_ext + b_pack
+    peak, peak_kind = peaks()
+    stage_ms = {"expand": float(kt_mean[0]), "extract": float(kt_mean[1]), "scan": float(kt_mean[2]),
+                "pack": float(kt_mean[3]), "finalize": float(kt_mean[4])}
+    stage_bytes = {"expand": b_exp, "extract": b_ext, "pack": b_pack}
+    top = max(("expand", "extract", "pack"), key=lambda n: stage_ms[n])
+    ext_ms = stage_ms[top]
+    bx = stage_bytes[top]
+    achieved = bx / (ext_ms / 1e3) / 1e9
+    call_gbs = bt / (float(np.mean(step_ms)) / 1e3) / 1e9
+    prof = os.path.join(ROOT, "profiles", "extract_dram_bytes.json")
+    traffic = None
+    if os.path.exists(prof):
+        with open(prof) as f:
+            traffic = json.load(f).get("dram_bytes_per_launch")
+    line = {
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
+        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "config": config_dict(world, ev),
+        "edges_per_s": world * edges / (total_ms / 1e3),
+        "roofline": {"bound": "hbm", "kernel": {"expand": "k_expand", "extract": "k_extract",
+                                                "pack": "k_pack"}[top], "achieved": achieved, "peak": peak,
+                     "peak_kind": peak_kind, "unit": "GB/s", "frac": achieved / peak,
+                     "traffic": traffic, "alg_bytes_per_launch": bx,
+                     "kernel_ms": ext_ms,
+                     "kernel_share_of_step": ext_ms / float(np.mean(step_ms)),
+                     "call_alg_bytes": bt, "call_frac": call_gbs / peak,
+                     "stage_ms": stage_ms, "stage_alg_bytes": stage_bytes,
+                     "stage_frac": {n: stage_bytes[n] / (stage_ms[n] / 1e3) / 1e9 / peak
+                                    for n in stage_bytes}},
+        "gpu_launches": int(launches),
+        "clocks": clk.summary(),
+        "e2e": {"value": mb / e2e_total if e2e_total > 0 else None, "unit": UNIT,
+                "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
+                "path": "hgs_sample_run (host int64 inputs, pinned) + hgs_sample_copy_to_host "
+                        "(all outputs, pinned), wall clock"},
+        "counts_per_step": {k: int(np.mean([s[k] for s in stats])) for k in ("V", "E", "S")},
+    }
+    if world == 1 and not args.no_cpu_baseline:
+        threads = os.cpu_count() or 1
+        nb = 2 * threads
+        t, V, E, kind = cpu_sample_time(ev, nb, threads)
+        line["cpu_baseline"] = {"value": nb / t, "unit": UNIT, "cores": threads, "kind": kind,
+                                "sample": f"{nb} minibatches x {BATCH} roots of C2, "
+                                          f"bulk_shadow+gather_features, batch-sharded over "
+                                          f"{threads} host threads ({t:.1f}s wall)"}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    args = ap.parse_args()
+    args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    if args.impl == "reference":
+        run_reference(args, world, rank)
+        return
+    if world > 1:
+        import torch
+        import torch.distributed as dist
+        torch.cuda.set_device(local_rank)
+        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+    try:
+        run_gpu(args, world, rank, local_rank)
+    finally:
+        if world > 1:
+            import torch.distributed as dist
+            dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -124,6 +124,11 @@ int hgs_graph_info(hgs_graph* g, int64_t* info);
  * row_ptr[n+1], col_idx[walk nnz]. */
 int hgs_graph_walk(hgs_graph* g, int32_t symmetrize, int64_t* row_ptr, int64_t* col_idx);
 int hgs_graph_destroy(hgs_graph* g);
+/* gather_features for an arbitrary batch (sampler.cpp:211-243): node rows of
+ * l2g[V] and edge rows / labels of edge ids eid[E] (input CSR positions) into
+ * host xv[V*f_v], ye[E*f_e], lab[E]. Ids are range-checked (HGS_EINVAL). */
+int hgs_graph_gather(hgs_graph* g, const int64_t* l2g, int64_t V, const int64_t* eid, int64_t E,
+                     double* xv, double* ye, uint8_t* lab);
 
 /* ---- sampling ------------------------------------------------------------- */
 /* stream: a cudaStream_t (NULL = a stream owned by the handle). */
@@ -150,9 +155,16 @@ int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d
 int hgs_sample_wait(hgs_sample* s, int64_t* counts);
 int hgs_sample_copy_to_host(hgs_sample* s, const hgs_host_out* out);
 int hgs_sample_device_views(hgs_sample* s, hgs_device_views* out);
-/* Per-kernel times (ms) of the last profiled run: [0]=expand [1]=extract
- * [2]=finalize [3]=total; returns HGS_EINVAL if the run was not profiled. */
-int hgs_sample_kernel_times(hgs_sample* s, float* ms4);
+/* Per-stage times (ms) of the last profiled run, from CUDA events on the
+ * handle's stream: [0]=expand (K1) [1]=extract (K2) [2]=offset scan
+ * [3]=pack+gather (K3) [4]=finalize [5]=total; HGS_EINVAL if not profiled. */
+int hgs_sample_kernel_times(hgs_sample* s, float* ms6);
+/* Work counters of the last run, reduced on the device (outside any timed
+ * region): [0]=R [1]=k [2]=V [3]=E [4]=S (A entries scanned = sum of
+ * out-degrees over all sampled vertices) [5]=sum of expanded frontier rows
+ * (levels 0..d-1) [6]=sum of chosen children (levels 1..d) [7]=decisions
+ * [8]=draws [9..9+d] = frontier rows per level 0..d. n >= 10 + depth. */
+int hgs_sample_stats(hgs_sample* s, int64_t* stats, int32_t n);
 /* Number of kernels the last run launched (for gpu_launches accounting). */
 int hgs_sample_launches(hgs_sample* s, int64_t* n);
 

@@ -1,0 +1,42 @@
+/*
+ * hgs_tools.h — C entry points of libhitgnn_gpu.so used by the Python
+ * harnesses (bench, tests). Not part of the sampler boundary (hgs.h).
+ *
+ * hgs_generate_event: the synthetic TrackML-shaped event generator
+ * (hitgnn::generate_event; reference data.cpp:124-268) returning the
+ * make_edge_id_matrix CSR (sampler.cpp:203-209) and features.
+ */
+#ifndef HGS_TOOLS_H
+#define HGS_TOOLS_H
+#include <stdint.h>
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef struct hgs_event hgs_event;
+
+/* Returns 0 on success; message via hgs_tools_last_error(). */
+int hgs_generate_event(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
+                       int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,
+                       uint64_t seed, uint64_t event_id, hgs_event** out);
+/* sizes: [0]=n [1]=m [2]=f_v [3]=f_e */
+void hgs_event_sizes(const hgs_event* ev, int64_t* sizes);
+/* row_ptr[n+1], col_idx[m] (make_edge_id_matrix CSR), node_feat[n*f_v],
+ * edge_feat[m*f_e], labels[m]; any pointer may be NULL. */
+void hgs_event_copy(const hgs_event* ev, int64_t* row_ptr, int64_t* col_idx, double* node_feat,
+                    double* edge_feat, uint8_t* labels);
+void hgs_event_free(hgs_event* ev);
+const char* hgs_tools_last_error(void);
+
+/* epoch_root_batches (sampler.cpp:245-263) with Rng(rng_seed): writes the
+ * shuffled permutation of [0, n) to perm; returns the number of batches. */
+int64_t hgs_epoch_root_batches(int64_t n, int64_t batch_size, uint64_t rng_seed, int64_t* perm);
+/* seeds[bi*b + pos] = Rng::derive(seed, prefix ++ {bi, pos}) for bi < k, pos < b
+ * (bench protocol cli.cpp:401-408, trainer root_stream_seed trainer.cpp:200-206). */
+void hgs_derive_grid(uint64_t seed, const uint64_t* prefix, int32_t prefix_len, int64_t k,
+                     int64_t b, uint64_t* seeds);
+
+#ifdef __cplusplus
+}
+#endif
+#endif

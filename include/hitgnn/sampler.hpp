@@ -1,0 +1,3 @@
+// Forwarding header: the drop-in declares the whole reference API in core.hpp.
+#pragma once
+#include "hitgnn/core.hpp"

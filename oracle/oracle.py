@@ -342,3 +342,31 @@ def ref_time_sample(g: Graph, roots, batch_off, seeds, *, rng=RNG_XOSHIRO, depth
                             ef.shape[1], _ptr(lab), _ptr(roots), _ptr(batch_off),
                             len(batch_off) - 1, _ptr(seeds), rng, depth, fanout, threads, ve)
     return t, int(ve[0]), int(ve[1])
+
+
+def port_time_sample(g: Graph, roots, batch_off, seeds, *, rng=RNG_XOSHIRO, depth=3, fanout=6,
+                     threads=1):
+    """Wall seconds of the C restatement (bulk_shadow + gather) batch-sharded
+    over `threads` Python threads (ctypes releases the GIL). (seconds, V, E)"""
+    import time
+    from concurrent.futures import ThreadPoolExecutor
+
+    roots = np.asarray(roots, np.int64)
+    batch_off = np.asarray(batch_off, np.int64)
+    seeds = np.asarray(seeds, np.uint64)
+    k = len(batch_off) - 1
+    threads = max(1, min(threads, k))
+
+    def work(t):
+        b0, b1 = k * t // threads, k * (t + 1) // threads
+        if b1 <= b0:
+            return 0, 0
+        r0, r1 = batch_off[b0], batch_off[b1]
+        s = bulk_shadow(g, roots[r0:r1], batch_off[b0:b1 + 1] - r0, seeds[r0:r1], rng=rng,
+                        depth=depth, fanout=fanout, gather=True)
+        return s.V, s.E
+
+    t0 = time.perf_counter()
+    with ThreadPoolExecutor(threads) as ex:
+        res = list(ex.map(work, range(threads)))
+    return time.perf_counter() - t0, sum(r[0] for r in res), sum(r[1] for r in res)

@@ -236,6 +236,36 @@ int hgs_graph_destroy(hgs_graph* h) {
     });
 }
 
+int hgs_graph_gather(hgs_graph* h, const int64_t* l2g, int64_t V, const int64_t* eid, int64_t E,
+                     double* xv, double* ye, uint8_t* lab) {
+    return guarded([&] {
+        if (!h) fail(HGS_EINVAL, "hgs: null graph");
+        DevGraph& g = h->g;
+        if (!g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
+        for (int64_t i = 0; i < V; ++i)
+            if (l2g[i] < 0 || l2g[i] >= g.n_rows)
+                fail(HGS_EINVAL, "gather_features: batch vertex out of range for event");
+        for (int64_t i = 0; i < E; ++i)
+            if (eid[i] < 0 || eid[i] >= g.nnz)
+                fail(HGS_EINVAL, "gather_features: adjacency values do not carry edge ids; "
+                                 "sample from make_edge_id_matrix(event)");
+        HGS_CUDA(cudaSetDevice(g.device));
+        cudaStream_t st = g.stream;
+        DevBuf<int64_t> dl, de;
+        DevBuf<double> dx, dy;
+        DevBuf<uint8_t> db;
+        dl.reserve((size_t)V + 1); de.reserve((size_t)E + 1);
+        dx.reserve((size_t)(V * g.f_v) + 1); dy.reserve((size_t)(E * g.f_e) + 1); db.reserve((size_t)E + 1);
+        upload(dl.p, l2g, sizeof(int64_t) * V, st);
+        upload(de.p, eid, sizeof(int64_t) * E, st);
+        gather_rows(g, dl.p, V, de.p, E, dx.p, dy.p, db.p, st);
+        if (V * g.f_v) HGS_CUDA(cudaMemcpyAsync(xv, dx.p, sizeof(double) * V * g.f_v, cudaMemcpyDeviceToHost, st));
+        if (E * g.f_e) HGS_CUDA(cudaMemcpyAsync(ye, dy.p, sizeof(double) * E * g.f_e, cudaMemcpyDeviceToHost, st));
+        if (E) HGS_CUDA(cudaMemcpyAsync(lab, db.p, E, cudaMemcpyDeviceToHost, st));
+        HGS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 // ---- sampling -------------------------------------------------------------------
 
 int hgs_sample_create(hgs_graph* g, void* stream, hgs_sample** out) {
@@ -410,15 +440,23 @@ int hgs_sample_device_views(hgs_sample* s, hgs_device_views* v) {
     });
 }
 
-int hgs_sample_kernel_times(hgs_sample* s, float* ms) {
+int hgs_sample_kernel_times(hgs_sample* s, float* ms) {  // 6 entries
     return guarded([&] {
         if (!s || !s->profiled) fail(HGS_EINVAL, "hgs_sample_kernel_times: last run was not profiled");
         HGS_CUDA(cudaSetDevice(s->graph->g.device));
-        HGS_CUDA(cudaEventSynchronize(s->ev[3]));
-        HGS_CUDA(cudaEventElapsedTime(&ms[0], s->ev[0], s->ev[1]));
-        HGS_CUDA(cudaEventElapsedTime(&ms[1], s->ev[1], s->ev[2]));
-        HGS_CUDA(cudaEventElapsedTime(&ms[2], s->ev[2], s->ev[3]));
-        HGS_CUDA(cudaEventElapsedTime(&ms[3], s->ev[0], s->ev[3]));
+        HGS_CUDA(cudaEventSynchronize(s->ev[5]));
+        for (int i = 0; i < 5; ++i) HGS_CUDA(cudaEventElapsedTime(&ms[i], s->ev[i], s->ev[i + 1]));
+        HGS_CUDA(cudaEventElapsedTime(&ms[5], s->ev[0], s->ev[5]));
+    });
+}
+
+int hgs_sample_stats(hgs_sample* s, int64_t* stats, int32_t n) {
+    return guarded([&] {
+        if (!s || !stats) fail(HGS_EINVAL, "hgs: null argument");
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_stats: run not waited for");
+        if (n < 10 + s->depth) fail(HGS_EINVAL, "hgs_sample_stats: stats array too short");
+        HGS_CUDA(cudaSetDevice(s->graph->g.device));
+        sample_stats(s, stats, n);
     });
 }
 

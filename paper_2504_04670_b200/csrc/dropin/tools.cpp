@@ -1,0 +1,86 @@
+// tools.cpp — extern "C" wrappers (include/hgs_tools.h) for Python harnesses.
+#include <algorithm>
+#include <string>
+
+#include "hgs_tools.h"
+#include "hitgnn/core.hpp"
+#include "../hgs_rng.cuh"
+
+struct hgs_event {
+    hitgnn::EventGraph ev;
+    hitgnn::CsrMatrix a;
+};
+
+namespace {
+thread_local std::string g_tools_err;
+}
+
+extern "C" {
+
+const char* hgs_tools_last_error(void) { return g_tools_err.c_str(); }
+
+int hgs_generate_event(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
+                       int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,
+                       uint64_t seed, uint64_t event_id, hgs_event** out) {
+    try {
+        hitgnn::GenConfig cfg;
+        cfg.n_tracks = n_tracks;
+        cfg.hits_min = hits_min;
+        cfg.hits_max = hits_max;
+        cfg.detector_layers = layers;
+        cfg.noise_hits = noise_hits;
+        cfg.false_edge_factor = false_edge_factor;
+        cfg.f_v = f_v;
+        cfg.f_e = f_e;
+        cfg.seed = seed;
+        auto* e = new hgs_event;
+        e->ev = hitgnn::generate_event(cfg, event_id);
+        e->a = hitgnn::make_edge_id_matrix(e->ev);
+        *out = e;
+        return 0;
+    } catch (const std::exception& ex) {
+        g_tools_err = ex.what();
+        return 1;
+    }
+}
+
+void hgs_event_sizes(const hgs_event* e, int64_t* s) {
+    s[0] = e->ev.n;
+    s[1] = e->ev.m();
+    s[2] = e->ev.node_features.cols;
+    s[3] = e->ev.edge_features.cols;
+}
+
+void hgs_event_copy(const hgs_event* e, int64_t* rp, int64_t* ci, double* nf, double* ef, uint8_t* lab) {
+    if (rp) std::copy(e->a.row_ptr.begin(), e->a.row_ptr.end(), rp);
+    if (ci) std::copy(e->a.col_idx.begin(), e->a.col_idx.end(), ci);
+    if (nf) std::copy(e->ev.node_features.data.begin(), e->ev.node_features.data.end(), nf);
+    if (ef) std::copy(e->ev.edge_features.data.begin(), e->ev.edge_features.data.end(), ef);
+    if (lab) std::copy(e->ev.labels.begin(), e->ev.labels.end(), lab);
+}
+
+void hgs_event_free(hgs_event* e) { delete e; }
+
+int64_t hgs_epoch_root_batches(int64_t n, int64_t b, uint64_t rng_seed, int64_t* perm) {
+    hitgnn::Rng rng(rng_seed);
+    const auto batches = hitgnn::epoch_root_batches(n, b, rng);
+    int64_t w = 0;
+    for (const auto& bb : batches)
+        for (auto v : bb) perm[w++] = v;
+    return static_cast<int64_t>(batches.size());
+}
+
+void hgs_derive_grid(uint64_t seed, const uint64_t* prefix, int32_t plen, int64_t k, int64_t b,
+                     uint64_t* seeds) {
+    std::vector<uint64_t> path(prefix, prefix + plen);
+    path.push_back(0);
+    path.push_back(0);
+    for (int64_t bi = 0; bi < k; ++bi)
+        for (int64_t pos = 0; pos < b; ++pos) {
+            path[plen] = static_cast<uint64_t>(bi);
+            path[plen + 1] = static_cast<uint64_t>(pos);
+            seeds[bi * b + pos] = hgs::derive_seed(seed, path.data(), plen + 2);
+        }
+}
+
+}  // extern "C"

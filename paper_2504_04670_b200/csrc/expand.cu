@@ -1,0 +1,262 @@
+// expand.cu — K1: stacked-Q frontier expansion, one lane per root.
+//
+// Restates sample_rows + the expansion loop of bulk_shadow
+// (sampler.cpp:64-86, 160-184) per root: level by level, every frontier row v
+// with deg_walk(v) > 0 makes one choose(deg, min(s, deg)) decision on the
+// root's own stream (PerRootChoiceSource resumes the stream across levels,
+// rng.hpp:67-82; the Philox source numbers decisions per root), positions come
+// back sorted and map to the walk row's ascending columns, children are
+// appended in (parent row, position) order. Rows with no support make no
+// decision (sampler.cpp:75). The frontier is a multiset: duplicates are
+// expanded again (no dedup until the touched set).
+//
+// Output: per root a touched list (root, then levels 1..d in BFS order) in a
+// fixed-stride scratch slot, its length, per-level row counts and the
+// draws/decisions consumed. The (row start, degree) pairs of the rows still to
+// expand are cached per lane in shared memory, so the next level issues no
+// dependent row_ptr loads.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace hgs {
+
+
+
+
+// A random stream for one root, in either mode; draw(i, m) returns the
+// accepted bounded(m) result of Fisher-Yates step i (Rng::bounded
+// semantics, rng.cpp:43-50).
+template <bool PHILOX>
+struct RootStream;
+
+template <>
+struct RootStream<false> {
+    Xoshiro256 x;
+    uint32_t draws = 0;
+    __device__ void init(uint64_t seed, const uint64_t* st) {
+        if (st) { x.a = st[0]; x.b = st[1]; x.c = st[2]; x.d = st[3]; }
+        else x.seed(seed);
+    }
+    __device__ __forceinline__ void begin_decision(uint32_t) {}
+    __device__ __forceinline__ uint32_t draw(uint32_t, uint64_t m, uint64_t rc) {
+        uint64_t v;
+        do {
+            v = x.next();
+            ++draws;
+        } while (rejected(v, m, rc));
+        return (uint32_t)mod_by_recip(v, m, rc);
+    }
+};
+
+template <>
+struct RootStream<true> {
+    uint64_t seed = 0;
+    uint32_t dec = 0, draws = 0;
+    __device__ void init(uint64_t s, const uint64_t*) { seed = s; }
+    __device__ __forceinline__ void begin_decision(uint32_t d) { dec = d; }
+    __device__ __forceinline__ uint32_t draw(uint32_t step, uint64_t m, uint64_t rc) {
+        uint64_t v;
+        uint32_t att = 0;
+        do {
+            v = philox_draw(seed, dec, step, att++);
+            ++draws;
+        } while (rejected(v, m, rc));
+        return (uint32_t)mod_by_recip(v, m, rc);
+    }
+};
+
+// choose(n, k) of RandomChoiceSource (rng.cpp:105-119) over a virtual
+// identity array, for k <= KCAP: slots < k live in registers; slots >= k that
+// a swap displaced live in a short (pos, val) list. Output sorted ascending.
+template <int KCAP, bool PHILOX>
+__device__ __forceinline__ void choose_regs(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
+                                            const uint64_t* __restrict__ recip,
+                                            uint32_t (&val)[KCAP]) {
+    uint32_t dpos[KCAP], dval[KCAP];
+#pragma unroll
+    for (int q = 0; q < KCAP; ++q) { val[q] = q; dpos[q] = 0xffffffffu; dval[q] = 0; }
+    int nd = 0;
+#pragma unroll
+    for (int i = 0; i < KCAP; ++i) {
+        if (i < (int)k) {
+            const uint64_t m = n - (uint32_t)i;
+            const uint32_t j = (uint32_t)i + rs.draw((uint32_t)i, m, __ldg(recip + m));
+            const uint32_t vi = val[i];
+            uint32_t vj = j;
+            if (j < k) {
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q) if ((uint32_t)q == j) vj = val[q];
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q) if ((uint32_t)q == j) val[q] = vi;
+            } else {
+                bool found = false;
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q)
+                    if (dpos[q] == j) { vj = dval[q]; dval[q] = vi; found = true; }
+                if (!found) {
+#pragma unroll
+                    for (int q = 0; q < KCAP; ++q)
+                        if (q == nd) { dpos[q] = j; dval[q] = vi; }
+                    ++nd;
+                }
+            }
+            val[i] = vj;
+        }
+    }
+#pragma unroll
+    for (int q = 0; q < KCAP; ++q) if (q >= (int)k) val[q] = 0xffffffffu;
+    // odd-even transposition network
+#pragma unroll
+    for (int round = 0; round < KCAP; ++round) {
+#pragma unroll
+        for (int q = round & 1; q + 1 < KCAP; q += 2) {
+            const uint32_t a = val[q], b = val[q + 1];
+            val[q] = min(a, b);
+            val[q + 1] = max(a, b);
+        }
+    }
+}
+
+// Generic variant for large fanouts (local-memory arrays, k <= 256).
+template <bool PHILOX>
+__device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
+                             const uint64_t* __restrict__ recip, uint32_t* val) {
+    uint32_t dpos[256], dval[256];
+    int nd = 0;
+    for (uint32_t q = 0; q < k; ++q) val[q] = q;
+    for (uint32_t i = 0; i < k; ++i) {
+        const uint64_t m = n - i;
+        const uint32_t j = i + rs.draw(i, m, __ldg(recip + m));
+        const uint32_t vi = val[i];
+        uint32_t vj = j;
+        if (j < k) {
+            vj = val[j];
+            val[j] = vi;
+        } else {
+            int f = -1;
+            for (int q = 0; q < nd; ++q) if (dpos[q] == j) f = q;
+            if (f >= 0) { vj = dval[f]; dval[f] = vi; }
+            else { dpos[nd] = j; dval[nd] = vi; ++nd; }
+        }
+        val[i] = vj;
+    }
+    for (uint32_t a = 1; a < k; ++a) {  // insertion sort
+        const uint32_t x = val[a];
+        uint32_t b = a;
+        while (b > 0 && val[b - 1] > x) { val[b] = val[b - 1]; --b; }
+        val[b] = x;
+    }
+}
+
+template <int KCAP, bool PHILOX, bool LOCAL>
+__global__ void __launch_bounds__(128) k_expand(ExpandParams p) {
+    extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree)
+    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    if (r >= p.R) return;
+    const int bd = blockDim.x, ti = threadIdx.x;
+
+    const int32_t root = p.roots32 ? p.roots32[r] : (int32_t)p.roots64[r];
+    if (root < 0 || root >= p.n) {
+        report(p.ticket, kErrRootRange, r, root);
+        p.tcount[r] = 0;
+        return;
+    }
+    RootStream<PHILOX> rs;
+    rs.init(p.seeds[r], (!PHILOX && p.state) ? p.state + 4 * (size_t)r : nullptr);
+    uint32_t ndec = (PHILOX && p.state) ? (uint32_t)p.state[r] : 0u;
+    const uint32_t dec0 = ndec;
+
+    int32_t* out = p.touched + (size_t)r * p.stride;
+    int32_t* lc = p.level_counts + (size_t)r * (p.depth + 1);
+    out[0] = root;
+    lc[0] = 1;
+    const bool cached = p.cache_entries > 0;
+    {
+        const int32_t b = p.w_rp[root];
+        if (cached) cache[ti] = make_int2(b, p.w_rp[root + 1] - b);
+    }
+    int T = 1, lvl_begin = 0, lvl_end = 1;
+    for (int level = 0; level < p.depth; ++level) {
+        const bool expand_next = level + 1 < p.depth;
+        const int next_begin = T;
+        for (int idx = lvl_begin; idx < lvl_end; ++idx) {
+            int2 row;
+            if (cached) row = cache[(size_t)idx * bd + ti];
+            else {
+                const int32_t v = out[idx];
+                row.x = p.w_rp[v];
+                row.y = p.w_rp[v + 1] - row.x;
+            }
+            if (row.y == 0) continue;  // empty rows make no choose call (sampler.cpp:75)
+            if (p.neg_row && p.neg_row[out[idx]]) {
+                report(p.ticket, kErrNegative, r, level);
+                p.tcount[r] = T;
+                return;
+            }
+            const uint32_t deg = (uint32_t)row.y;
+            const uint32_t k = min((uint32_t)p.fanout, deg);
+            rs.begin_decision(ndec);
+            ++ndec;
+            if (!LOCAL) {
+                uint32_t pos[KCAP];
+                choose_regs<KCAP, PHILOX>(rs, deg, k, p.recip, pos);
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q) {
+                    if (q < (int)k) {
+                        const int32_t c = __ldg(p.w_ci + row.x + pos[q]);
+                        out[T] = c;
+                        if (expand_next && cached) {
+                            const int32_t cb = __ldg(p.w_rp + c);
+                            cache[(size_t)T * bd + ti] = make_int2(cb, __ldg(p.w_rp + c + 1) - cb);
+                        }
+                        ++T;
+                    }
+                }
+            } else {
+                uint32_t pos[256];
+                choose_local<PHILOX>(rs, deg, k, p.recip, pos);
+                for (uint32_t q = 0; q < k; ++q) {
+                    const int32_t c = __ldg(p.w_ci + row.x + pos[q]);
+                    out[T] = c;
+                    if (expand_next && cached) {
+                        const int32_t cb = __ldg(p.w_rp + c);
+                        cache[(size_t)T * bd + ti] = make_int2(cb, __ldg(p.w_rp + c + 1) - cb);
+                    }
+                    ++T;
+                }
+            }
+        }
+        lc[level + 1] = T - next_begin;
+        lvl_begin = next_begin;
+        lvl_end = T;
+    }
+    p.tcount[r] = T;
+    p.draws[r] = rs.draws;
+    p.decisions[r] = ndec - dec0;
+}
+
+template <int KCAP, bool PH, bool LOCAL>
+static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cudaStream_t st) {
+    auto kern = k_expand<KCAP, PH, LOCAL>;
+    if (smem > 48 * 1024)
+        HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const unsigned grid = (unsigned)((ep.R + threads - 1) / threads);
+    kern<<<grid, threads, smem, st>>>(ep);
+    HGS_CUDA(cudaGetLastError());
+}
+
+void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
+                   cudaStream_t st) {
+    const bool local = kmax > 8;  // register fast path covers fanouts up to 8
+    if (philox) {
+        if (local) launch_expand_t<8, true, true>(threads, smem, ep, st);
+        else launch_expand_t<8, true, false>(threads, smem, ep, st);
+    } else {
+        if (local) launch_expand_t<8, false, true>(threads, smem, ep, st);
+        else launch_expand_t<8, false, false>(threads, smem, ep, st);
+    }
+}
+
+
+}  // namespace hgs

@@ -1,0 +1,524 @@
+// extract.cu — K2 (dedup + induced-subgraph extraction), the per-call offset
+// scan, K3 (block-diagonal packing + feature/label gather) and small helpers.
+//
+// K2 k_extract, one warp per root:
+//   sorted_vertex_set (sampler.cpp:48-53): the touched list is inserted into a
+//   shared-memory hash set (4-slot buckets probed with one 16-byte LDS), the
+//   unique vertices are bitonic-sorted in registers and written back over the
+//   touched slot; ranks (local ids) go into the table.
+//   induced_subgraph = S·A·Sᵀ (sparse.cpp:177-191) on the directed edge-id
+//   matrix A: the A rows of the set, in local order, are flattened into one
+//   index space and scanned in 32-wide coalesced windows (row owner of every
+//   lane from a __reduce_or_sync bitmask of row starts), each column probed in
+//   the hash set; hits come out row-major with ascending columns, i.e. in the
+//   reference's CSR order, and are appended to the root's edge slot.
+// Offsets: exclusive scan of (V_r, E_r) over roots (block_diag offsets,
+//   sparse.cpp:245-258) — three small launches.
+// K3 k_pack, one warp per root: rebases into batch-local ids, writes
+//   local_to_global / roots_local / component offsets / COO edges / edge ids,
+//   and gathers node rows, edge rows and labels (gather_features,
+//   sampler.cpp:211-243) with 16-byte vector stores.
+#include <cuda_runtime.h>
+
+#include "kernels.cuh"
+
+namespace hgs {
+
+namespace {
+
+constexpr uint32_t kEmpty = 0xffffffffu;
+
+struct HashSet {
+    uint32_t* key;  // 4 * nb slots, bucket-major
+    uint16_t* rank;
+    uint32_t bmask;
+    int bits;
+
+    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
+
+    // true if v was not present before
+    __device__ __forceinline__ bool insert(uint32_t v) const {
+        uint32_t b = bucket(v);
+        for (;;) {
+            uint32_t* bk = key + 4 * b;
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint32_t prev = atomicCAS(bk + s, kEmpty, v);
+                if (prev == kEmpty) return true;
+                if (prev == v) return false;
+            }
+            b = (b + 1) & bmask;
+        }
+    }
+    // slot index of v, or -1
+    __device__ __forceinline__ int find_slot(uint32_t v) const {
+        uint32_t b = bucket(v);
+        for (;;) {
+            const uint4 q = *reinterpret_cast<const uint4*>(key + 4 * b);
+            if (q.x == v) return 4 * b;
+            if (q.y == v) return 4 * b + 1;
+            if (q.z == v) return 4 * b + 2;
+            if (q.w == v) return 4 * b + 3;
+            if (q.w == kEmpty) return -1;  // slots fill in order: bucket not full
+            b = (b + 1) & bmask;
+        }
+    }
+    __device__ __forceinline__ int find_rank(uint32_t v) const {
+        const int s = find_slot(v);
+        return s < 0 ? -1 : (int)rank[s];
+    }
+};
+
+template <int E>
+__device__ __forceinline__ void sort_regs(int32_t* set, int U) {
+    const int lane = lane_id();
+    uint32_t kk[E];
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        kk[e] = i < U ? (uint32_t)set[i] : 0xffffffffu;
+    }
+    warp_bitonic_sort<E>(kk);
+    __syncwarp();
+#pragma unroll
+    for (int e = 0; e < E; ++e) {
+        const int i = lane * E + e;
+        if (i < U) set[i] = (int32_t)kk[e];
+    }
+    __syncwarp();
+}
+
+__device__ void sort_smem(int32_t* set, int U, int N) {
+    const int lane = lane_id();
+    for (int i = U + lane; i < N; i += 32) set[i] = 0x7fffffff;
+    __syncwarp();
+    for (int size = 2; size <= N; size <<= 1) {
+        for (int stride = size >> 1; stride > 0; stride >>= 1) {
+            for (int t = lane; t < N / 2; t += 32) {
+                const int i = 2 * t - (t & (stride - 1));
+                const int j = i + stride;
+                const bool up = (i & size) == 0;
+                const int32_t a = set[i], b = set[j];
+                if ((a > b) == up) { set[i] = b; set[j] = a; }
+            }
+            __syncwarp();
+        }
+    }
+}
+
+}  // namespace
+
+// ===========================================================================
+// K2
+// ===========================================================================
+
+__global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
+    extern __shared__ __align__(16) unsigned char smem_raw[];
+    const int lane = lane_id();
+    const int warp = threadIdx.x >> 5;
+    unsigned char* q = smem_raw + (size_t)warp * p.warp_bytes;
+    const int nslots = 4 << p.nb_bits;
+    HashSet hs;
+    hs.key = (uint32_t*)q; q += 4 * nslots;
+    int32_t* set = (int32_t*)q; q += 4 * p.set_cap;
+    int32_t* rstart = (int32_t*)q; q += 4 * (p.row_cap + 4);
+    int32_t* rbase = (int32_t*)q; q += 4 * p.row_cap;
+    hs.rank = (uint16_t*)q; q += 2 * nslots;
+    uint16_t* rrank = (uint16_t*)q;
+    hs.bits = p.nb_bits;
+    hs.bmask = (1u << p.nb_bits) - 1u;
+    const unsigned lt = (1u << lane) - 1u;
+    const unsigned le = (2u << lane) - 1u;
+
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < p.R; r += nwarps) {
+        int32_t* tl = p.touched + (size_t)r * p.stride;
+        const int T = p.tcount[r];
+        const int32_t root = tl[0];  // before the slot is overwritten by the set
+
+        // ---- dedup: hash-insert the touched list, compact the new keys
+        for (int i = lane; i < nslots; i += 32) hs.key[i] = kEmpty;
+        __syncwarp();
+        int U = 0;
+        for (int b0 = 0; b0 < T; b0 += 32) {
+            const int idx = b0 + lane;
+            bool fresh = false;
+            int32_t v = 0;
+            if (idx < T) {
+                v = tl[idx];
+                fresh = hs.insert((uint32_t)v);
+            }
+            const unsigned fb = __ballot_sync(kFull, fresh);
+            if (fresh) set[U + __popc(fb & lt)] = v;
+            U += __popc(fb);
+        }
+        __syncwarp();
+        if (U <= 32) sort_regs<1>(set, U);
+        else if (U <= 64) sort_regs<2>(set, U);
+        else if (U <= 128) sort_regs<4>(set, U);
+        else if (U <= 256) sort_regs<8>(set, U);
+        else if (U <= 512) sort_regs<16>(set, U);
+        else {
+            int N = 1024;
+            while (N < U) N <<= 1;
+            sort_smem(set, U, N);
+        }
+
+        // ---- ranks, the sorted set back to global, nonempty A rows
+        int NR = 0, S = 0;
+        for (int b0 = 0; b0 < U; b0 += 32) {
+            const int i = b0 + lane;
+            int32_t rb = 0, deg = 0;
+            if (i < U) {
+                const int32_t u = set[i];
+                hs.rank[hs.find_slot((uint32_t)u)] = (uint16_t)i;
+                tl[i] = u;
+                rb = __ldg(p.a_rp + u);
+                deg = __ldg(p.a_rp + u + 1) - rb;
+            }
+            const bool ne = deg > 0;
+            const unsigned nb = __ballot_sync(kFull, ne);
+            const int incl = warp_incl_scan(deg);
+            if (ne) {
+                const int qi = NR + __popc(nb & lt);
+                rstart[qi] = S + incl - deg;
+                rbase[qi] = rb;
+                rrank[qi] = (uint16_t)i;
+            }
+            NR += __popc(nb);
+            S += __shfl_sync(kFull, incl, 31);
+        }
+        if (lane == 0) rstart[NR] = S;
+        __syncwarp();
+
+        // ---- induced subgraph: 4 windows of 32 entries per iteration
+        int2* ed = p.escratch + (size_t)r * p.e_stride;
+        int cursor = 0, count = 0;
+        for (int w = 0; w < S; w += 128) {
+            int own[4], kk[4];
+            int32_t v[4];
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int ww = w + 32 * u;
+                const int rr = cursor + 1 + lane;
+                const int rs = rr <= NR ? rstart[rr] : 0x7fffffff;
+                const int off = rs - ww;
+                const unsigned bit = (off > 0 && off < 32) ? (1u << off) : 0u;
+                const unsigned M = __reduce_or_sync(kFull, bit);
+                own[u] = min(cursor + __popc(M & le), NR - 1);
+                const int own31 = __shfl_sync(kFull, own[u], 31);
+                cursor = (own31 + 1 <= NR && rstart[own31 + 1] == ww + 32) ? own31 + 1 : own31;
+                const int pos = ww + lane;
+                kk[u] = pos < S ? rbase[own[u]] + (pos - rstart[own[u]]) : -1;
+            }
+#pragma unroll
+            for (int u = 0; u < 4; ++u) v[u] = kk[u] >= 0 ? __ldg(p.a_ci + kk[u]) : -1;
+#pragma unroll
+            for (int u = 0; u < 4; ++u) {
+                const int j = v[u] >= 0 ? hs.find_rank((uint32_t)v[u]) : -1;
+                const bool hit = j >= 0;
+                const unsigned hb = __ballot_sync(kFull, hit);
+                if (hit) {
+                    const int t = count + __popc(hb & lt);
+                    if (t < p.e_stride) {
+                        const int32_t gid = p.a_gid ? __ldg(p.a_gid + kk[u]) : kk[u];
+                        ed[t] = make_int2(((int32_t)rrank[own[u]] << 16) | j, gid);
+                    }
+                }
+                count += __popc(hb);
+            }
+        }
+        if (lane == 0) {
+            p.root_nv[r] = U;
+            p.root_ne[r] = count;
+            p.root_rloc[r] = hs.find_rank((uint32_t)root);
+            p.root_scan[r] = S;
+            if (count > p.e_stride) {
+                atomicMax(&p.ticket[4], count);
+                report(p.ticket, kErrCapacity, r, count);
+            }
+        }
+        __syncwarp();
+    }
+}
+
+// ===========================================================================
+// offsets: exclusive scan of (V_r, E_r)
+// ===========================================================================
+
+constexpr int kPairTile = 1024;  // roots per tile, 256 threads x 4
+
+__device__ __forceinline__ void block_scan_pair(int64_t& a, int64_t& b, int64_t* sh, int64_t& ta, int64_t& tb) {
+    // exclusive block scan of two int64 values; sh holds 2*33 entries
+    const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5, nw = blockDim.x >> 5;
+    int64_t ia = a, ib = b;
+#pragma unroll
+    for (int o = 1; o < 32; o <<= 1) {
+        const int64_t xa = __shfl_up_sync(kFull, ia, o), xb = __shfl_up_sync(kFull, ib, o);
+        if (lane >= o) { ia += xa; ib += xb; }
+    }
+    if (lane == 31) { sh[wid] = ia; sh[33 + wid] = ib; }
+    __syncthreads();
+    if (wid == 0) {
+        int64_t wa = lane < nw ? sh[lane] : 0, wb = lane < nw ? sh[33 + lane] : 0;
+        int64_t sa = wa, sb = wb;
+#pragma unroll
+        for (int o = 1; o < 32; o <<= 1) {
+            const int64_t xa = __shfl_up_sync(kFull, sa, o), xb = __shfl_up_sync(kFull, sb, o);
+            if (lane >= o) { sa += xa; sb += xb; }
+        }
+        if (lane < nw) { sh[lane] = sa - wa; sh[33 + lane] = sb - wb; }
+        if (lane == nw - 1) { sh[32] = sa; sh[65] = sb; }
+    }
+    __syncthreads();
+    ta = sh[32];
+    tb = sh[65];
+    a = sh[wid] + ia - a;
+    b = sh[33 + wid] + ib - b;
+    __syncthreads();
+}
+
+__global__ void k_scan_reduce(const int32_t* __restrict__ nv, const int32_t* __restrict__ ne, int32_t R,
+                              int64_t* __restrict__ tile_sums) {
+    __shared__ int64_t sh[66];
+    int64_t a = 0, b = 0;
+    const int base = blockIdx.x * kPairTile + threadIdx.x * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i)
+        if (base + i < R) { a += nv[base + i]; b += ne[base + i]; }
+    int64_t ta, tb;
+    block_scan_pair(a, b, sh, ta, tb);
+    if (threadIdx.x == 0) { tile_sums[2 * blockIdx.x] = ta; tile_sums[2 * blockIdx.x + 1] = tb; }
+}
+
+__global__ void k_scan_tiles(int64_t* __restrict__ tile_sums, int32_t tiles, int32_t* __restrict__ ticket) {
+    __shared__ int64_t sh[66];
+    __shared__ int64_t carry[2];
+    if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
+    __syncthreads();
+    for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
+        const int t = t0 + threadIdx.x;
+        int64_t a = t < tiles ? tile_sums[2 * t] : 0, b = t < tiles ? tile_sums[2 * t + 1] : 0;
+        int64_t ta, tb;
+        block_scan_pair(a, b, sh, ta, tb);
+        if (t < tiles) { tile_sums[2 * t] = carry[0] + a; tile_sums[2 * t + 1] = carry[1] + b; }
+        __syncthreads();
+        if (threadIdx.x == 0) { carry[0] += ta; carry[1] += tb; }
+        __syncthreads();
+    }
+    if (threadIdx.x == 0) {
+        tile_sums[2 * tiles] = carry[0];
+        tile_sums[2 * tiles + 1] = carry[1];
+        if (carry[0] > 0x7fffffff || carry[1] > 0x7fffffff) report(ticket, kErrOverflow, 0, 0);
+    }
+}
+
+__global__ void k_scan_apply(const int32_t* __restrict__ nv, const int32_t* __restrict__ ne, int32_t R,
+                             const int64_t* __restrict__ tile_offs, int32_t tiles,
+                             int32_t* __restrict__ voff, int32_t* __restrict__ eoff) {
+    __shared__ int64_t sh[66];
+    int64_t x[4], y[4], a = 0, b = 0;
+    const int base = blockIdx.x * kPairTile + threadIdx.x * 4;
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        x[i] = base + i < R ? nv[base + i] : 0;
+        y[i] = base + i < R ? ne[base + i] : 0;
+        a += x[i];
+        b += y[i];
+    }
+    int64_t ta, tb;
+    block_scan_pair(a, b, sh, ta, tb);
+    a += tile_offs[2 * blockIdx.x];
+    b += tile_offs[2 * blockIdx.x + 1];
+#pragma unroll
+    for (int i = 0; i < 4; ++i) {
+        if (base + i < R) { voff[base + i] = (int32_t)a; eoff[base + i] = (int32_t)b; }
+        a += x[i];
+        b += y[i];
+    }
+    if (blockIdx.x == 0 && threadIdx.x == 0) {
+        voff[R] = (int32_t)tile_offs[2 * tiles];
+        eoff[R] = (int32_t)tile_offs[2 * tiles + 1];
+    }
+}
+
+void launch_scan(const int32_t* nv, const int32_t* ne, int32_t R, int64_t* tmp, int32_t* voff,
+                 int32_t* eoff, int32_t* ticket, cudaStream_t st) {
+    const int tiles = (R + kPairTile - 1) / kPairTile;
+    k_scan_reduce<<<tiles, 256, 0, st>>>(nv, ne, R, tmp);
+    k_scan_tiles<<<1, 1024, 0, st>>>(tmp, tiles, ticket);
+    k_scan_apply<<<tiles, 256, 0, st>>>(nv, ne, R, tmp, tiles, voff, eoff);
+    HGS_CUDA(cudaGetLastError());
+}
+
+int64_t scan_tmp_words(int64_t R) { return 2 * ((R + kPairTile - 1) / kPairTile) + 4; }
+
+// ===========================================================================
+// K3
+// ===========================================================================
+
+__global__ void __launch_bounds__(256) k_pack(PackParams p) {
+    const int lane = lane_id();
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
+        int b;
+        {
+            int lo = 0, hi = p.k;  // largest b with batch_off[b] <= r
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.batch_off[mid] <= r) lo = mid; else hi = mid - 1;
+            }
+            b = lo;
+        }
+        const int f = (int)p.batch_off[b];
+        const int64_t vb = p.root_voff[r], eb = p.root_eoff[r];
+        const int Vr = p.root_voff[r + 1] - (int32_t)vb;
+        const int Er = p.root_eoff[r + 1] - (int32_t)eb;
+        if (vb + Vr > p.v_cap || eb + Er > p.e_cap) {
+            if (lane == 0) report(p.ticket, kErrCapacity, r, -1);
+            continue;
+        }
+        const int32_t loc = (int32_t)vb - p.root_voff[f];
+        const int32_t* set = p.touched + (size_t)r * p.stride;
+        for (int i = lane; i < Vr; i += 32) __stcs(p.l2g + vb + i, set[i]);
+        if (lane == 0) {
+            p.roots_local[r] = loc + p.root_rloc[r];
+            p.comp_off[r + b] = loc;
+            if (r == p.batch_off[b + 1] - 1) p.comp_off[r + 1 + b] = loc + Vr;
+        }
+        const int2* ed = p.escratch + (size_t)r * p.e_stride;
+        for (int t = lane; t < Er; t += 32) {
+            const int2 e = ed[t];
+            __stcs(p.e_row + eb + t, loc + (e.x >> 16));
+            __stcs(p.e_col + eb + t, loc + (e.x & 0xffff));
+            __stcs(p.e_gid + eb + t, e.y);
+            if (p.gather) {
+                p.lab[eb + t] = __ldg(p.labels + e.y);
+                if (p.f_e == 2) {
+                    const double2 x = __ldg(reinterpret_cast<const double2*>(p.edge_feat) + e.y);
+                    __stcs(reinterpret_cast<double2*>(p.ye) + eb + t, x);
+                } else {
+                    for (int c = 0; c < p.f_e; ++c)
+                        __stcs(p.ye + (eb + t) * p.f_e + c, __ldg(p.edge_feat + (int64_t)e.y * p.f_e + c));
+                }
+            }
+        }
+        if (p.gather) {
+            if ((p.f_v & 1) == 0) {  // rows as f_v/2 16-byte pieces
+                const int q2 = p.f_v >> 1;
+                const double2* src = reinterpret_cast<const double2*>(p.node_feat);
+                double2* dst = reinterpret_cast<double2*>(p.xv) + vb * q2;
+                for (int e = lane; e < Vr * q2; e += 32) {
+                    const int i = (int)__umulhi((unsigned)e, p.fv_magic);
+                    __stcs(dst + e, __ldg(src + (int64_t)set[i] * q2 + (e - i * q2)));
+                }
+            } else {
+                double* dst = p.xv + vb * p.f_v;
+                for (int e = lane; e < Vr * p.f_v; e += 32) {
+                    const int i = e / p.f_v;
+                    __stcs(dst + e, __ldg(p.node_feat + (int64_t)set[i] * p.f_v + (e - i * p.f_v)));
+                }
+            }
+        }
+    }
+}
+
+__global__ void k_finalize(const int64_t* __restrict__ batch_off, int32_t k, int32_t R,
+                           const int32_t* __restrict__ root_voff, const int32_t* __restrict__ root_eoff,
+                           int32_t* __restrict__ batch_voff, int32_t* __restrict__ batch_eoff,
+                           int32_t* __restrict__ comp_off) {
+    for (int b = blockIdx.x * blockDim.x + threadIdx.x; b <= k; b += gridDim.x * blockDim.x) {
+        const int64_t f = batch_off[b];
+        batch_voff[b] = root_voff[f];
+        batch_eoff[b] = root_eoff[f];
+        if (b < k && batch_off[b + 1] == f) comp_off[f + b] = 0;  // empty batch
+    }
+}
+
+// ===========================================================================
+// standalone gather + stats
+// ===========================================================================
+
+__global__ void k_gather(const double* __restrict__ node_feat, int32_t f_v,
+                         const double* __restrict__ edge_feat, int32_t f_e,
+                         const uint8_t* __restrict__ labels, const int64_t* __restrict__ l2g,
+                         int64_t V, const int64_t* __restrict__ eid, int64_t E,
+                         double* __restrict__ xv, double* __restrict__ ye, uint8_t* __restrict__ lab) {
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    const int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+    for (int64_t e = t0; e < V * f_v; e += stride) {
+        const int64_t i = e / f_v;
+        xv[e] = node_feat[l2g[i] * f_v + (e - i * f_v)];
+    }
+    for (int64_t e = t0; e < E * f_e; e += stride) {
+        const int64_t i = e / f_e;
+        ye[e] = edge_feat[eid[i] * f_e + (e - i * f_e)];
+    }
+    for (int64_t i = t0; i < E; i += stride) lab[i] = labels[eid[i]];
+}
+
+__global__ void k_stats(const int32_t* __restrict__ level_counts, int32_t depth,
+                        const int32_t* __restrict__ root_scan, const uint32_t* __restrict__ decisions,
+                        const uint32_t* __restrict__ draws, int32_t R,
+                        unsigned long long* __restrict__ out) {
+    unsigned long long acc[3 + 16] = {};
+    for (int r = blockIdx.x * blockDim.x + threadIdx.x; r < R; r += gridDim.x * blockDim.x) {
+        acc[0] += (unsigned)root_scan[r];
+        acc[1] += decisions[r];
+        acc[2] += draws[r];
+        for (int l = 0; l <= depth && l < 16; ++l) acc[3 + l] += (unsigned)level_counts[(size_t)r * (depth + 1) + l];
+    }
+    for (int i = 0; i < 3 + 16; ++i) {
+        unsigned long long v = acc[i];
+        for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+        if ((threadIdx.x & 31) == 0 && v) atomicAdd(out + i, v);
+    }
+}
+
+// ---- launchers -----------------------------------------------------------------
+
+void launch_extract(int grid, size_t smem, const ExtractParams& xp, cudaStream_t st) {
+    HGS_CUDA(cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_extract<<<grid, 128, smem, st>>>(xp);
+    HGS_CUDA(cudaGetLastError());
+}
+
+int extract_blocks_per_sm(size_t smem) {
+    HGS_CUDA(cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    int per_sm = 0;
+    HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract, 128, smem));
+    return per_sm > 0 ? per_sm : 1;
+}
+
+void launch_pack(int grid, const PackParams& pp, cudaStream_t st) {
+    k_pack<<<grid, 256, 0, st>>>(pp);
+    HGS_CUDA(cudaGetLastError());
+}
+
+void launch_finalize(const int64_t* batch_off, int32_t k, int32_t R, const int32_t* voff,
+                     const int32_t* eoff, int32_t* bvoff, int32_t* beoff, int32_t* comp_off,
+                     cudaStream_t st) {
+    k_finalize<<<(unsigned)((k + 1 + 255) / 256), 256, 0, st>>>(batch_off, k, R, voff, eoff, bvoff, beoff,
+                                                               comp_off);
+    HGS_CUDA(cudaGetLastError());
+}
+
+void launch_gather(const DevGraph& g, const int64_t* d_l2g, int64_t V, const int64_t* d_eid, int64_t E,
+                   double* d_xv, double* d_ye, uint8_t* d_lab, cudaStream_t st) {
+    const int64_t work = std::max<int64_t>(std::max<int64_t>(V * g.f_v, E * g.f_e), std::max<int64_t>(E, 1));
+    const unsigned grid = (unsigned)std::min<int64_t>((work + 255) / 256, 148 * 16);
+    k_gather<<<grid, 256, 0, st>>>(g.node_feat.p, g.f_v, g.edge_feat.p, g.f_e, g.labels.p, d_l2g, V, d_eid,
+                                   E, d_xv, d_ye, d_lab);
+    HGS_CUDA(cudaGetLastError());
+}
+
+void launch_stats(const int32_t* level_counts, int32_t depth, const int32_t* root_scan,
+                  const uint32_t* decisions, const uint32_t* draws, int32_t R,
+                  unsigned long long* out, cudaStream_t st) {
+    if (R <= 0) return;
+    k_stats<<<(unsigned)std::min<int64_t>((R + 255) / 256, 1024), 256, 0, st>>>(
+        level_counts, depth, root_scan, decisions, draws, R, out);
+    HGS_CUDA(cudaGetLastError());
+}
+
+}  // namespace hgs

@@ -183,28 +183,35 @@ struct hgs_sample {
     hgs::DevBuf<int32_t> touched, tcount, level_counts;
     hgs::DevBuf<uint32_t> draws, decisions;
     int64_t touched_stride = 0;
-    // look-back state
-    hgs::DevBuf<unsigned long long> status, bbase;
-    hgs::DevBuf<int32_t> ticket;  // [0]=ticket [1]=error code [2..3]=error detail
+    // extract scratch + offsets
+    hgs::DevBuf<int32_t> root_nv, root_ne, root_rloc;
+    hgs::DevBuf<int2> escratch;
+    int32_t e_stride = 512;
+    hgs::DevBuf<int64_t> scan_tmp;
+    hgs::DevBuf<unsigned long long> stats_tmp;
+    hgs::DevBuf<int32_t> ticket;  // [1]=error code [2..3]=error detail [4]=max E_r seen
     // outputs
     hgs::DevBuf<int32_t> l2g, roots_local, comp_off, batch_voff, batch_eoff;
-    hgs::DevBuf<int32_t> e_row, e_col, e_gid, root_voff, root_eoff;
+    hgs::DevBuf<int32_t> e_row, e_col, e_gid, root_voff, root_eoff, root_scan;
     hgs::DevBuf<double> xv, ye;
     hgs::DevBuf<uint8_t> lab;
     size_t v_cap = 0, e_cap = 0;
     // pinned host mirror of small per-call state
-    int32_t* h_state = nullptr;  // [0..3] error flags, [4]=V, [5]=E
+    int32_t* h_state = nullptr;  // [0..4] error words, [8]=V, [9]=E
     // last call
     int64_t R = 0, k = 0, V = 0, E = 0;
     int64_t depth = 0, fanout = 0;
     int32_t gathered = 0, symmetrize = 1, rng = 0;
     bool pending = false;
     bool profiled = false;
-    cudaEvent_t ev[4] = {nullptr, nullptr, nullptr, nullptr};
+    cudaEvent_t ev[6] = {};
     int64_t launches = 0;
 };
 
 namespace hgs {
 void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in);
 void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in);
+void sample_stats(hgs_sample* s, int64_t* out, int n);
+void gather_rows(DevGraph& g, const int64_t* d_l2g, int64_t V, const int64_t* d_eid, int64_t E,
+                 double* d_xv, double* d_ye, uint8_t* d_lab, cudaStream_t st);
 }  // namespace hgs

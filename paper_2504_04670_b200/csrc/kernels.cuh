@@ -1,0 +1,104 @@
+// kernels.cuh — parameter blocks and launchers shared by the sampling kernels.
+#pragma once
+#include <algorithm>
+
+#include "hgs_internal.cuh"
+
+namespace hgs {
+
+enum : int32_t { kErrNone = 0, kErrRootRange = 1, kErrNegative = 2, kErrOverflow = 3, kErrCapacity = 4 };
+
+__device__ __forceinline__ void report(int32_t* t, int32_t code, int32_t a, int32_t b) {
+    if (atomicCAS(&t[1], 0, code) == 0) {
+        t[2] = a;
+        t[3] = b;
+    }
+}
+
+struct ExpandParams {
+    const int32_t* __restrict__ w_rp;
+    const int32_t* __restrict__ w_ci;
+    const uint64_t* __restrict__ recip;
+    const uint8_t* __restrict__ neg_row;  // nullable
+    const int32_t* __restrict__ roots32;  // one of roots32 / roots64
+    const int64_t* __restrict__ roots64;
+    const uint64_t* __restrict__ seeds;
+    const uint64_t* __restrict__ state;   // nullable: resume states
+    int32_t R, depth, fanout, n;
+    int64_t stride;
+    int32_t cache_entries;                // (b,deg) entries cached per lane in smem
+    int32_t* __restrict__ touched;
+    int32_t* __restrict__ tcount;
+    int32_t* __restrict__ level_counts;
+    uint32_t* __restrict__ draws;
+    uint32_t* __restrict__ decisions;
+    int32_t* __restrict__ ticket;         // [0] ticket, [1] error code, [2] root, [3] aux
+};
+
+void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
+                   cudaStream_t st);
+
+// K2: dedup + induced-subgraph extraction into per-root scratch.
+struct ExtractParams {
+    const int32_t* __restrict__ a_rp;
+    const int32_t* __restrict__ a_ci;
+    const int32_t* __restrict__ a_gid;  // nullable
+    int32_t* __restrict__ touched;      // in: touched lists; out: sorted sets
+    const int32_t* __restrict__ tcount;
+    int64_t stride;
+    int32_t R;
+    int32_t* __restrict__ root_nv;
+    int32_t* __restrict__ root_ne;
+    int32_t* __restrict__ root_rloc;
+    int32_t* __restrict__ root_scan;
+    int2* __restrict__ escratch;        // per root: e_stride x (local i<<16 | j, edge id)
+    int32_t e_stride;
+    int32_t* __restrict__ ticket;
+    int32_t nb_bits, set_cap, row_cap, warp_bytes;
+};
+
+// K3: packing + gather.
+struct PackParams {
+    const int32_t* __restrict__ touched;
+    int64_t stride;
+    const int32_t* __restrict__ root_voff;
+    const int32_t* __restrict__ root_eoff;
+    const int32_t* __restrict__ root_rloc;
+    const int2* __restrict__ escratch;
+    int32_t e_stride;
+    const int64_t* __restrict__ batch_off;
+    int32_t k, R;
+    int32_t* __restrict__ l2g;
+    int32_t* __restrict__ roots_local;
+    int32_t* __restrict__ comp_off;
+    int32_t* __restrict__ e_row;
+    int32_t* __restrict__ e_col;
+    int32_t* __restrict__ e_gid;
+    double* __restrict__ xv;
+    double* __restrict__ ye;
+    uint8_t* __restrict__ lab;
+    const double* __restrict__ node_feat;
+    const double* __restrict__ edge_feat;
+    const uint8_t* __restrict__ labels;
+    int32_t f_v, f_e, gather;
+    uint32_t fv_magic;  // ceil(2^32 / (f_v/2)) for even f_v
+    int64_t v_cap, e_cap;
+    int32_t* __restrict__ ticket;
+};
+
+void launch_extract(int grid, size_t smem, const ExtractParams& xp, cudaStream_t st);
+int extract_blocks_per_sm(size_t smem);
+void launch_scan(const int32_t* nv, const int32_t* ne, int32_t R, int64_t* tmp, int32_t* voff,
+                 int32_t* eoff, int32_t* ticket, cudaStream_t st);
+int64_t scan_tmp_words(int64_t R);
+void launch_pack(int grid, const PackParams& pp, cudaStream_t st);
+void launch_finalize(const int64_t* batch_off, int32_t k, int32_t R, const int32_t* voff,
+                     const int32_t* eoff, int32_t* bvoff, int32_t* beoff, int32_t* comp_off,
+                     cudaStream_t st);
+void launch_gather(const DevGraph& g, const int64_t* d_l2g, int64_t V, const int64_t* d_eid, int64_t E,
+                   double* d_xv, double* d_ye, uint8_t* d_lab, cudaStream_t st);
+void launch_stats(const int32_t* level_counts, int32_t depth, const int32_t* root_scan,
+                  const uint32_t* decisions, const uint32_t* draws, int32_t R,
+                  unsigned long long* out, cudaStream_t st);
+
+}  // namespace hgs

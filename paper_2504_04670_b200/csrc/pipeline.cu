@@ -1,0 +1,267 @@
+// pipeline.cu — host orchestration of one bulk_shadow call on the device:
+// K1 expand → K2 extract → offset scan → K3 pack/gather → batch offsets, all
+// on the sample handle's stream with no host synchronisation in between.
+// Capacity guesses (edge slots per root, output edge capacity) are checked
+// on the device; on overflow the call is re-run once with exact sizes.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <string>
+#include <vector>
+
+#include "kernels.cuh"
+
+namespace hgs {
+
+namespace {
+
+int64_t tree_bound(int64_t kmax, int64_t upto) {
+    // 1 + kmax + ... + kmax^upto, saturating at 2^40
+    int64_t total = 0, term = 1;
+    const int64_t cap = (int64_t)1 << 40;
+    for (int64_t l = 0; l <= upto; ++l) {
+        total = std::min(cap, total + term);
+        term = std::min(cap, term * std::max<int64_t>(kmax, 1));
+    }
+    return total;
+}
+
+struct CallPlan {
+    int64_t kmax, max_t, cache_entries;
+    int expand_threads;
+    size_t expand_smem;
+    int32_t nb_bits, set_cap, row_cap, warp_bytes;
+};
+
+CallPlan plan_call(const DevCsr& walk, int64_t depth, int64_t fanout) {
+    CallPlan c{};
+    c.kmax = std::min<int64_t>(fanout, walk.max_deg);
+    if (c.kmax > 256) fail(HGS_ERANGE, "hgs: min(fanout, max degree) > 256 is not supported by this build");
+    c.max_t = tree_bound(c.kmax, depth);
+    if (c.max_t > 32767)
+        fail(HGS_ERANGE, "hgs: per-root tree bound " + std::to_string(c.max_t) +
+                             " exceeds this build's limit (32767); reduce depth/fanout");
+    c.cache_entries = tree_bound(c.kmax, depth - 1);
+    c.expand_threads = 128;
+    c.expand_smem = (size_t)c.cache_entries * 128 * sizeof(int2);
+    if (c.expand_smem > 96 * 1024) {
+        c.expand_threads = 64;
+        c.expand_smem = (size_t)c.cache_entries * 64 * sizeof(int2);
+        if (c.expand_smem > 96 * 1024) {
+            c.cache_entries = 0;
+            c.expand_smem = 0;
+            c.expand_threads = 128;
+        }
+    }
+    // hash set: 4-slot buckets, >= 4 slots per possible key
+    int bits = 2;
+    while ((4 << bits) < 4 * c.max_t) ++bits;
+    c.nb_bits = bits;
+    c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);
+    if (c.max_t > 512) {
+        int n = 1024;
+        while (n < c.max_t) n <<= 1;
+        c.set_cap = n;
+    }
+    c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
+    const size_t slots = (size_t)4 << c.nb_bits;
+    size_t bytes = 4 * slots + 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 4) + 4 * (size_t)c.row_cap +
+                   2 * slots + 2 * (size_t)c.row_cap;
+    bytes = (bytes + 15) / 16 * 16;
+    c.warp_bytes = (int32_t)bytes;
+    if (4 * bytes > 200 * 1024) fail(HGS_ERANGE, "hgs: per-root working set too large for shared memory");
+    return c;
+}
+
+int sm_count(int device) {
+    int n = 0;
+    HGS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
+    return n;
+}
+
+}  // namespace
+
+void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) {
+    DevGraph& g = s->graph->g;
+    HGS_CUDA(cudaSetDevice(g.device));
+    if (cfg.symmetrize) graph_build_walk_sym(g);
+    const DevCsr& walk = cfg.symmetrize ? g.walk_sym : g.a;
+    graph_ensure_recip(g, walk.max_deg);
+    if (cfg.gather && !g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
+    const CallPlan c = plan_call(walk, cfg.depth, cfg.fanout);
+    const int64_t R = in.R, k = in.k;
+    if (R * c.max_t >= ((int64_t)1 << 40)) fail(HGS_ERANGE, "hgs: too many roots for one call");
+    cudaStream_t st = s->stream;
+
+    s->R = R; s->k = k; s->depth = cfg.depth; s->fanout = cfg.fanout;
+    s->gathered = cfg.gather; s->symmetrize = cfg.symmetrize; s->rng = cfg.rng;
+    s->launches = 0;
+    s->touched_stride = c.max_t;
+    const size_t R1 = (size_t)R + 1;
+    s->touched.reserve((size_t)std::max<int64_t>(R, 1) * c.max_t);
+    s->tcount.reserve(R1);
+    s->level_counts.reserve(R1 * (cfg.depth + 1));
+    s->draws.reserve(R1);
+    s->decisions.reserve(R1);
+    s->root_nv.reserve(R1);
+    s->root_ne.reserve(R1);
+    s->root_rloc.reserve(R1);
+    s->root_scan.reserve(R1);
+    s->escratch.reserve(R1 * s->e_stride);
+    s->scan_tmp.reserve(scan_tmp_words(R));
+    s->ticket.reserve(8);
+    s->root_voff.reserve(R1);
+    s->root_eoff.reserve(R1);
+    s->roots_local.reserve(R1);
+    s->comp_off.reserve((size_t)(R + k) + 1);
+    s->batch_voff.reserve((size_t)k + 1);
+    s->batch_eoff.reserve((size_t)k + 1);
+    const size_t vneed = (size_t)std::max<int64_t>(1, R * c.max_t);
+    if (s->v_cap < vneed) s->v_cap = vneed;
+    if (s->e_cap < s->v_cap * 2) s->e_cap = s->v_cap * 2;
+    s->l2g.reserve(s->v_cap);
+    s->e_row.reserve(s->e_cap);
+    s->e_col.reserve(s->e_cap);
+    s->e_gid.reserve(s->e_cap);
+    if (cfg.gather) {
+        s->xv.reserve(s->v_cap * (size_t)std::max(1, g.f_v));
+        s->ye.reserve(s->e_cap * (size_t)std::max(1, g.f_e));
+        s->lab.reserve(s->e_cap);
+    }
+    HGS_CUDA(cudaMemsetAsync(s->ticket.p, 0, 8 * sizeof(int32_t), st));
+    if (R == 0) {
+        HGS_CUDA(cudaMemsetAsync(s->root_voff.p, 0, sizeof(int32_t), st));
+        HGS_CUDA(cudaMemsetAsync(s->root_eoff.p, 0, sizeof(int32_t), st));
+    }
+    if (!s->ev[0]) for (auto& e : s->ev) HGS_CUDA(cudaEventCreate(&e));
+    s->profiled = cfg.profile != 0;
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[0], st));
+
+    if (R > 0) {
+        ExpandParams ep{};
+        ep.w_rp = walk.rp.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
+        ep.neg_row = (!cfg.symmetrize && g.has_neg) ? g.neg_row.p : nullptr;
+        ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
+        ep.R = (int32_t)R; ep.depth = (int32_t)cfg.depth;
+        ep.fanout = (int32_t)std::min<int64_t>(cfg.fanout, 1 << 30);
+        ep.n = (int32_t)g.n_rows; ep.stride = c.max_t; ep.cache_entries = (int32_t)c.cache_entries;
+        ep.touched = s->touched.p; ep.tcount = s->tcount.p; ep.level_counts = s->level_counts.p;
+        ep.draws = s->draws.p; ep.decisions = s->decisions.p; ep.ticket = s->ticket.p;
+        launch_expand(c.expand_threads, c.expand_smem, c.kmax, ep, cfg.rng == HGS_RNG_PHILOX, st);
+        ++s->launches;
+    }
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[1], st));
+    if (R > 0) {
+        ExtractParams xp{};
+        xp.a_rp = g.a.rp.p; xp.a_ci = g.a.ci.p; xp.a_gid = g.has_gid ? g.a_gid.p : nullptr;
+        xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t; xp.R = (int32_t)R;
+        xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
+        xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
+        xp.ticket = s->ticket.p; xp.nb_bits = c.nb_bits; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
+        xp.warp_bytes = c.warp_bytes;
+        const size_t smem = (size_t)4 * c.warp_bytes;
+        const int per_sm = extract_blocks_per_sm(smem);
+        const int64_t grid = std::min<int64_t>((int64_t)per_sm * sm_count(g.device), (R + 3) / 4);
+        launch_extract((int)std::max<int64_t>(grid, 1), smem, xp, st);
+        ++s->launches;
+    }
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
+    if (R > 0) {
+        launch_scan(s->root_nv.p, s->root_ne.p, (int32_t)R, s->scan_tmp.p, s->root_voff.p, s->root_eoff.p,
+                    s->ticket.p, st);
+        s->launches += 3;
+    }
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[3], st));
+    if (R > 0) {
+        PackParams pp{};
+        pp.touched = s->touched.p; pp.stride = c.max_t; pp.root_voff = s->root_voff.p;
+        pp.root_eoff = s->root_eoff.p; pp.root_rloc = s->root_rloc.p; pp.escratch = s->escratch.p;
+        pp.e_stride = s->e_stride; pp.batch_off = in.batch_off; pp.k = (int32_t)k; pp.R = (int32_t)R;
+        pp.l2g = s->l2g.p; pp.roots_local = s->roots_local.p; pp.comp_off = s->comp_off.p;
+        pp.e_row = s->e_row.p; pp.e_col = s->e_col.p; pp.e_gid = s->e_gid.p;
+        pp.xv = s->xv.p; pp.ye = s->ye.p; pp.lab = s->lab.p;
+        pp.node_feat = g.node_feat.p; pp.edge_feat = g.edge_feat.p; pp.labels = g.labels.p;
+        pp.f_v = g.f_v; pp.f_e = g.f_e; pp.gather = cfg.gather;
+        const uint32_t q2 = (uint32_t)std::max(1, g.f_v / 2);
+        pp.fv_magic = (uint32_t)((((uint64_t)1 << 32) + q2 - 1) / q2);
+        pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
+        const int64_t grid = std::min<int64_t>((int64_t)sm_count(g.device) * 8, (R + 7) / 8);
+        launch_pack((int)std::max<int64_t>(grid, 1), pp, st);
+        ++s->launches;
+    }
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
+    launch_finalize(in.batch_off, (int32_t)k, (int32_t)R, s->root_voff.p, s->root_eoff.p, s->batch_voff.p,
+                    s->batch_eoff.p, s->comp_off.p, st);
+    ++s->launches;
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[5], st));
+    if (!s->h_state) HGS_CUDA(cudaMallocHost(&s->h_state, 16 * sizeof(int32_t)));
+    HGS_CUDA(cudaMemcpyAsync(s->h_state, s->ticket.p, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaMemcpyAsync(s->h_state + 8, s->batch_voff.p + k, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaMemcpyAsync(s->h_state + 9, s->batch_eoff.p + k, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    s->pending = true;
+}
+
+void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) {
+    if (!s->pending) return;
+    HGS_CUDA(cudaStreamSynchronize(s->stream));
+    s->pending = false;
+    const int32_t code = s->h_state[1];
+    if (code == kErrRootRange)
+        fail(HGS_EINVAL, "sampler: root " + std::to_string(s->h_state[3]) + " out of range");
+    if (code == kErrNegative)
+        fail(HGS_EINVAL, "row_normalize: negative value in a visited walk row (root ordinal " +
+                             std::to_string(s->h_state[2]) + ", level " + std::to_string(s->h_state[3]) + ")");
+    if (code == kErrOverflow)
+        fail(HGS_ERANGE, "hgs: more than 2^31-1 sampled vertices/edges in one call; split the call");
+    s->V = s->h_state[8];
+    s->E = s->h_state[9];
+    if (code == kErrCapacity) {
+        // An edge slot or the output capacity was too small: grow to the
+        // observed need and run the call again (inputs are still resident).
+        const int32_t need = s->h_state[4];
+        if (need > s->e_stride) {
+            int32_t es = s->e_stride;
+            while (es < need) es *= 2;
+            s->e_stride = es;
+            s->escratch.release();
+        }
+        if ((size_t)s->E > s->e_cap) {
+            s->e_cap = (size_t)s->E + (size_t)s->E / 8 + 1024;
+            s->e_row.release(); s->e_col.release(); s->e_gid.release(); s->ye.release(); s->lab.release();
+        }
+        if ((size_t)s->V > s->v_cap) {
+            s->v_cap = (size_t)s->V;
+            s->l2g.release(); s->xv.release();
+        }
+        sample_enqueue(s, cfg, in);
+        sample_finish(s, cfg, in);
+    }
+}
+
+void sample_stats(hgs_sample* s, int64_t* out, int n) {
+    if (s->depth > 15) fail(HGS_ERANGE, "hgs_sample_stats: depth > 15");
+    s->stats_tmp.reserve(19);
+    HGS_CUDA(cudaMemsetAsync(s->stats_tmp.p, 0, sizeof(unsigned long long) * 19, s->stream));
+    launch_stats(s->level_counts.p, (int32_t)s->depth, s->root_scan.p, s->decisions.p, s->draws.p,
+                 (int32_t)s->R, s->stats_tmp.p, s->stream);
+    unsigned long long h[19];
+    HGS_CUDA(cudaMemcpyAsync(h, s->stats_tmp.p, sizeof(h), cudaMemcpyDeviceToHost, s->stream));
+    HGS_CUDA(cudaStreamSynchronize(s->stream));
+    std::vector<int64_t> st(10 + 16, 0);
+    st[0] = s->R; st[1] = s->k; st[2] = s->V; st[3] = s->E; st[4] = (int64_t)h[0];
+    for (int l = 0; l <= s->depth; ++l) {
+        if (l < s->depth) st[5] += (int64_t)h[3 + l];
+        if (l >= 1) st[6] += (int64_t)h[3 + l];
+        st[9 + l] = (int64_t)h[3 + l];
+    }
+    st[7] = (int64_t)h[1];
+    st[8] = (int64_t)h[2];
+    for (int i = 0; i < n && i < (int)st.size(); ++i) out[i] = st[i];
+}
+
+void gather_rows(DevGraph& g, const int64_t* d_l2g, int64_t V, const int64_t* d_eid, int64_t E,
+                 double* d_xv, double* d_ye, uint8_t* d_lab, cudaStream_t st) {
+    launch_gather(g, d_l2g, V, d_eid, E, d_xv, d_ye, d_lab, st);
+}
+
+}  // namespace hgs

@@ -27,9 +27,10 @@ RNG_XOSHIRO, RNG_PHILOX = 0, 1
 EXPORTS = [
     "hgs_last_error", "hgs_abi_version", "hgs_device_count", "hgs_graph_create",
     "hgs_graph_attach_features", "hgs_graph_info", "hgs_graph_walk", "hgs_graph_destroy",
+    "hgs_graph_gather",
     "hgs_sample_create", "hgs_sample_destroy", "hgs_sample_run", "hgs_sample_run_device",
     "hgs_sample_wait", "hgs_sample_copy_to_host", "hgs_sample_device_views",
-    "hgs_sample_kernel_times", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
+    "hgs_sample_kernel_times", "hgs_sample_stats", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
 ]
 
 
@@ -92,6 +93,7 @@ def lib() -> C.CDLL:
         L.hgs_sample_device_views.argtypes = [vp, C.POINTER(DeviceViews)]
         L.hgs_sample_kernel_times.argtypes = [vp, vp]
         L.hgs_sample_launches.argtypes = [vp, vp]
+        L.hgs_sample_stats.argtypes = [vp, vp, i32]
         _lib_cache = L
     return _lib_cache
 
@@ -270,9 +272,17 @@ class Sampler:
         return v
 
     def kernel_times(self) -> np.ndarray:
-        ms = np.zeros(4, np.float32)
+        ms = np.zeros(6, np.float32)
         _check(lib().hgs_sample_kernel_times(self._h, _p(ms)))
         return ms
+
+    def stats(self) -> dict:
+        a = np.zeros(32, np.int64)
+        _check(lib().hgs_sample_stats(self._h, _p(a), 32))
+        keys = ["R", "k", "V", "E", "S", "F_expand", "F_children", "decisions", "draws"]
+        d = dict(zip(keys, (int(x) for x in a[:9])))
+        d["F_levels"] = [int(x) for x in a[9:]]
+        return d
 
     def launches(self) -> int:
         n = np.zeros(1, np.int64)

@@ -1,0 +1,118 @@
+"""Synthetic TrackML-shaped workloads (BASELINE.json configs) for the bench
+and the parity tests: the event generator (C++, libhitgnn_gpu.so), the
+reference's bench-sampling root/seed protocol (cli.cpp:378-408) and the
+trainer's seed streams (trainer.cpp:195-206)."""
+from __future__ import annotations
+
+import ctypes as C
+import os
+from dataclasses import dataclass
+
+import numpy as np
+
+from . import hgs
+
+_PKG = os.path.dirname(os.path.abspath(__file__))
+TOOLS_PATH = os.path.join(_PKG, "lib", "libhitgnn_gpu.so")
+
+# GenConfig presets of SURVEY.md §8(d).
+GEN = {
+    "C1": dict(n_tracks=1100, hits_min=7, hits_max=10, layers=12, noise=650, false_factor=11.0,
+               f_v=6, f_e=2, seed=1),
+    "C2": dict(n_tracks=13000, hits_min=7, hits_max=10, layers=12, noise=10000,
+               false_factor=14.5, f_v=6, f_e=2, seed=1),
+}
+# sampler shapes: (batches k, roots per batch b, depth d, fanout s)
+SHAPE = {"C1": (16, 256, 2, 6), "C2": (64, 1024, 3, 6), "C3": (512, 1024, 3, 6)}
+
+_tools: C.CDLL | None = None
+
+
+def tools() -> C.CDLL:
+    global _tools
+    if _tools is None:
+        if not os.path.exists(TOOLS_PATH):
+            raise hgs.HgsRuntimeError(f"{TOOLS_PATH} missing; run python -m paper_2504_04670_b200.build")
+        hgs.lib()  # load libhgs first (libhitgnn_gpu depends on it)
+        L = C.CDLL(TOOLS_PATH)
+        vp = C.c_void_p
+        L.hgs_generate_event.argtypes = [C.c_int64] * 5 + [C.c_double, C.c_int64, C.c_int64,
+                                                           C.c_uint64, C.c_uint64, C.POINTER(vp)]
+        L.hgs_event_sizes.argtypes = [vp, vp]
+        L.hgs_event_copy.argtypes = [vp] * 6
+        L.hgs_event_free.argtypes = [vp]
+        L.hgs_tools_last_error.restype = C.c_char_p
+        L.hgs_epoch_root_batches.restype = C.c_int64
+        L.hgs_epoch_root_batches.argtypes = [C.c_int64, C.c_int64, C.c_uint64, vp]
+        L.hgs_derive_grid.argtypes = [C.c_uint64, vp, C.c_int32, C.c_int64, C.c_int64, vp]
+        _tools = L
+    return _tools
+
+
+@dataclass
+class Event:
+    n: int
+    rp: np.ndarray  # int64 [n+1] (make_edge_id_matrix CSR)
+    ci: np.ndarray  # int64 [m]
+    node_feat: np.ndarray  # (n, f_v) f64
+    edge_feat: np.ndarray  # (m, f_e) f64
+    labels: np.ndarray  # (m,) u8
+
+    @property
+    def m(self) -> int:
+        return int(self.rp[-1])
+
+
+def generate_event(n_tracks=1100, hits_min=7, hits_max=10, layers=12, noise=650,
+                   false_factor=11.0, f_v=6, f_e=2, seed=1, event_id=0) -> Event:
+    L = tools()
+    h = C.c_void_p()
+    if L.hgs_generate_event(n_tracks, hits_min, hits_max, layers, noise, false_factor, f_v, f_e,
+                            seed, event_id, C.byref(h)) != 0:
+        raise ValueError(L.hgs_tools_last_error().decode())
+    sz = np.zeros(4, np.int64)
+    L.hgs_event_sizes(h, sz.ctypes.data)
+    n, m, fv, fe = (int(x) for x in sz)
+    ev = Event(n=n, rp=np.zeros(n + 1, np.int64), ci=np.zeros(m, np.int64),
+               node_feat=np.zeros((n, fv)), edge_feat=np.zeros((m, fe)),
+               labels=np.zeros(m, np.uint8))
+    L.hgs_event_copy(h, ev.rp.ctypes.data, ev.ci.ctypes.data, ev.node_feat.ctypes.data,
+                     ev.edge_feat.ctypes.data, ev.labels.ctypes.data)
+    L.hgs_event_free(h)
+    return ev
+
+
+def preset_event(name: str, event_id: int = 0) -> Event:
+    return generate_event(**GEN[name], event_id=event_id)
+
+
+def epoch_root_batches(n: int, b: int, rng_seed: int) -> list[np.ndarray]:
+    """sampler.cpp:245-263 (host utility): Fisher-Yates with Rng(rng_seed)."""
+    perm = np.zeros(n, np.int64)
+    nb = int(tools().hgs_epoch_root_batches(n, b, rng_seed, perm.ctypes.data))
+    size = n if n < b else b
+    return [perm[i * size:(i + 1) * size] for i in range(nb)]
+
+
+def derive_grid(seed: int, prefix, k: int, b: int) -> np.ndarray:
+    pre = np.ascontiguousarray(prefix, np.uint64)
+    out = np.zeros(k * b, np.uint64)
+    tools().hgs_derive_grid(seed, pre.ctypes.data, len(pre), k, b, out.ctypes.data)
+    return out
+
+
+def bench_roots(n: int, b: int, k: int, seed: int = 1, rep: int = 0):
+    """Roots, batch offsets and per-root seeds of `hitgnn bench-sampling`
+    (cli.cpp:381-408): roots = epoch_root_batches(n, b,
+    Rng(derive(seed,{'bench',k,rep}))) truncated to k; seeds
+    derive(seed,{'strm',k,rep,bi,pos})."""
+    if k * b > n:
+        b = max(1, n // k)
+    batches = epoch_root_batches(n, b, hgs.derive(seed, [0x62656E6368, k, rep]))
+    if len(batches) < k:
+        raise ValueError(f"event too small for k={k} batches of {b}")
+    batches = batches[:k]
+    roots = np.concatenate(batches).astype(np.int64)
+    boff = np.arange(k + 1, dtype=np.int64) * b
+    seeds = derive_grid(seed, [0x7374726D, k, rep], k, b)
+    return roots, boff, seeds
