@@ -66,56 +66,45 @@ struct RootStream<true> {
     }
 };
 
-// choose(n, k) of RandomChoiceSource (rng.cpp:105-119) over a virtual
-// identity array, for k <= KCAP: slots < k live in registers; slots >= k that
-// a swap displaced live in a short (pos, val) list. Output sorted ascending.
+// choose(n, k) of RandomChoiceSource (rng.cpp:105-119) for k <= KCAP without
+// materialising the array: step i swaps slots i and j_i = i + bounded(n - i)
+// (j_i >= i), so slot i ends holding the value that sat at j_i just before
+// step i — the pre-step value of the latest earlier step a with j_a == j_i,
+// or j_i itself — and later steps never touch slot i again. The pre-step
+// value of slot i is likewise the pre-step value of the latest a with
+// j_a == i, or i. O(k^2) register compares, then a 19-comparator network.
 template <int KCAP, bool PHILOX>
-__device__ __forceinline__ void choose_regs(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
-                                            const uint64_t* __restrict__ recip,
-                                            uint32_t (&val)[KCAP]) {
-    uint32_t dpos[KCAP], dval[KCAP];
-#pragma unroll
-    for (int q = 0; q < KCAP; ++q) { val[q] = q; dpos[q] = 0xffffffffu; dval[q] = 0; }
-    int nd = 0;
+__device__ __forceinline__ void choose_small(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
+                                             const uint64_t* recip, uint32_t (&out)[KCAP]) {
+    static_assert(KCAP == 8, "sorting network below is for 8 keys");
+    uint32_t jj[KCAP], pre[KCAP];
 #pragma unroll
     for (int i = 0; i < KCAP; ++i) {
+        out[i] = 0xffffffffu;
         if (i < (int)k) {
             const uint64_t m = n - (uint32_t)i;
-            const uint32_t j = (uint32_t)i + rs.draw((uint32_t)i, m, __ldg(recip + m));
-            const uint32_t vi = val[i];
-            uint32_t vj = j;
-            if (j < k) {
+            const uint32_t ji = (uint32_t)i + rs.draw((uint32_t)i, m, recip[m]);
+            uint32_t pi = (uint32_t)i, vi = ji;
 #pragma unroll
-                for (int q = 0; q < KCAP; ++q) if ((uint32_t)q == j) vj = val[q];
-#pragma unroll
-                for (int q = 0; q < KCAP; ++q) if ((uint32_t)q == j) val[q] = vi;
-            } else {
-                bool found = false;
-#pragma unroll
-                for (int q = 0; q < KCAP; ++q)
-                    if (dpos[q] == j) { vj = dval[q]; dval[q] = vi; found = true; }
-                if (!found) {
-#pragma unroll
-                    for (int q = 0; q < KCAP; ++q)
-                        if (q == nd) { dpos[q] = j; dval[q] = vi; }
-                    ++nd;
-                }
+            for (int a = 0; a < i; ++a) {  // ascending: the latest match wins
+                pi = (jj[a] == (uint32_t)i) ? pre[a] : pi;
+                vi = (jj[a] == ji) ? pre[a] : vi;
             }
-            val[i] = vj;
+            jj[i] = ji;
+            pre[i] = pi;
+            out[i] = vi;
         }
     }
-#pragma unroll
-    for (int q = 0; q < KCAP; ++q) if (q >= (int)k) val[q] = 0xffffffffu;
-    // odd-even transposition network
-#pragma unroll
-    for (int round = 0; round < KCAP; ++round) {
-#pragma unroll
-        for (int q = round & 1; q + 1 < KCAP; q += 2) {
-            const uint32_t a = val[q], b = val[q + 1];
-            val[q] = min(a, b);
-            val[q + 1] = max(a, b);
-        }
+#define HGS_CX(x, y)                                                   \
+    {                                                                  \
+        const uint32_t lo = min(out[x], out[y]), hi = max(out[x], out[y]); \
+        out[x] = lo;                                                   \
+        out[y] = hi;                                                   \
     }
+    HGS_CX(0, 1) HGS_CX(2, 3) HGS_CX(4, 5) HGS_CX(6, 7) HGS_CX(0, 2) HGS_CX(1, 3) HGS_CX(4, 6)
+    HGS_CX(5, 7) HGS_CX(1, 2) HGS_CX(5, 6) HGS_CX(0, 4) HGS_CX(3, 7) HGS_CX(1, 5) HGS_CX(2, 6)
+    HGS_CX(1, 4) HGS_CX(3, 6) HGS_CX(2, 4) HGS_CX(3, 5) HGS_CX(3, 4)
+#undef HGS_CX
 }
 
 // Generic variant for large fanouts (local-memory arrays, k <= 256).
@@ -127,7 +116,7 @@ __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
     for (uint32_t q = 0; q < k; ++q) val[q] = q;
     for (uint32_t i = 0; i < k; ++i) {
         const uint64_t m = n - i;
-        const uint32_t j = i + rs.draw(i, m, __ldg(recip + m));
+        const uint32_t j = i + rs.draw(i, m, recip[m]);
         const uint32_t vi = val[i];
         uint32_t vj = j;
         if (j < k) {
@@ -151,8 +140,16 @@ __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
 
 template <int KCAP, bool PHILOX, bool LOCAL>
 __global__ void __launch_bounds__(128) k_expand(ExpandParams p) {
-    extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree)
+    extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree), then the recip table
     const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    // bounded() reciprocals in shared memory when the table is small
+    uint64_t* srecip = reinterpret_cast<uint64_t*>(cache + (size_t)p.cache_entries * blockDim.x);
+    const uint64_t* recip = p.recip;
+    if (p.recip_smem > 0) {
+        for (int i = threadIdx.x; i < p.recip_smem; i += blockDim.x) srecip[i] = p.recip[i];
+        __syncthreads();
+        recip = srecip;
+    }
     if (r >= p.R) return;
     const int bd = blockDim.x, ti = threadIdx.x;
 
@@ -200,22 +197,27 @@ __global__ void __launch_bounds__(128) k_expand(ExpandParams p) {
             ++ndec;
             if (!LOCAL) {
                 uint32_t pos[KCAP];
-                choose_regs<KCAP, PHILOX>(rs, deg, k, p.recip, pos);
+                choose_small<KCAP, PHILOX>(rs, deg, k, recip, pos);
+                int32_t c[KCAP];
 #pragma unroll
-                for (int q = 0; q < KCAP; ++q) {
-                    if (q < (int)k) {
-                        const int32_t c = __ldg(p.w_ci + row.x + pos[q]);
-                        out[T] = c;
-                        if (expand_next && cached) {
-                            const int32_t cb = __ldg(p.w_rp + c);
-                            cache[(size_t)T * bd + ti] = make_int2(cb, __ldg(p.w_rp + c + 1) - cb);
-                        }
-                        ++T;
+                for (int q = 0; q < KCAP; ++q) c[q] = q < (int)k ? __ldg(p.w_ci + row.x + pos[q]) : 0;
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q) if (q < (int)k) out[T + q] = c[q];
+                if (expand_next && cached) {
+                    int32_t b0[KCAP], b1[KCAP];
+#pragma unroll
+                    for (int q = 0; q < KCAP; ++q) {
+                        b0[q] = q < (int)k ? __ldg(p.w_rp + c[q]) : 0;
+                        b1[q] = q < (int)k ? __ldg(p.w_rp + c[q] + 1) : 0;
                     }
+#pragma unroll
+                    for (int q = 0; q < KCAP; ++q)
+                        if (q < (int)k) cache[(size_t)(T + q) * bd + ti] = make_int2(b0[q], b1[q] - b0[q]);
                 }
+                T += (int)k;
             } else {
                 uint32_t pos[256];
-                choose_local<PHILOX>(rs, deg, k, p.recip, pos);
+                choose_local<PHILOX>(rs, deg, k, recip, pos);
                 for (uint32_t q = 0; q < k; ++q) {
                     const int32_t c = __ldg(p.w_ci + row.x + pos[q]);
                     out[T] = c;

@@ -28,44 +28,117 @@ namespace {
 
 constexpr uint32_t kEmpty = 0xffffffffu;
 
-struct HashSet {
-    uint32_t* key;  // 4 * nb slots, bucket-major
-    uint16_t* rank;
-    uint32_t bmask;
-    int bits;
+// Shared-memory hash set of the root's vertex set mapping vertex -> local id
+// (rank in the sorted set). 4-slot buckets, one 16-byte LDS per probed
+// bucket; slots of a bucket fill in order, so a bucket with a free slot ends
+// a miss. PACKED: entry = vertex << rank_bits | rank (32 bit) and a bucket is
+// 4 entries; otherwise entry = (vertex, rank) and a bucket spans 2 x 16 B.
+template <bool PACKED>
+struct HashSet;
 
+template <>
+struct HashSet<true> {
+    uint32_t* slot;
+    uint32_t bmask, rmask;
+    int bits, rb;
+    static constexpr int kBytesPerSlot = 4;
     __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
+    __device__ __forceinline__ void clear(int nslots) const {
+        for (int i = lane_id(); i < nslots / 4; i += 32)
+            reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
+    }
+    __device__ __forceinline__ bool insert(uint32_t v) const {
+        const uint32_t e = (v << rb) | rmask, hi = v << rb;
+        uint32_t b = bucket(v);
+        for (;;) {
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const uint32_t prev = atomicCAS(slot + 4 * b + s, kEmpty, e);
+                if (prev == kEmpty) return true;
+                if ((prev ^ hi) <= rmask) return false;
+            }
+            b = (b + 1) & bmask;
+        }
+    }
+    __device__ __forceinline__ int find_slot(uint32_t v) const {
+        const uint32_t hi = v << rb;
+        uint32_t b = bucket(v);
+        for (;;) {
+            const uint4 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
+            if ((q.x ^ hi) <= rmask) return 4 * b;
+            if ((q.y ^ hi) <= rmask) return 4 * b + 1;
+            if ((q.z ^ hi) <= rmask) return 4 * b + 2;
+            if ((q.w ^ hi) <= rmask) return 4 * b + 3;
+            if (q.w == kEmpty) return -1;
+            b = (b + 1) & bmask;
+        }
+    }
+    __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)] = (v << rb) | r; }
+    __device__ __forceinline__ int find_rank(uint32_t v) const {
+        const uint32_t hi = v << rb;
+        uint32_t b = bucket(v);
+        for (;;) {
+            const uint4 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
+            int r = -1;
+            r = ((q.w ^ hi) <= rmask) ? (int)(q.w & rmask) : r;
+            r = ((q.z ^ hi) <= rmask) ? (int)(q.z & rmask) : r;
+            r = ((q.y ^ hi) <= rmask) ? (int)(q.y & rmask) : r;
+            r = ((q.x ^ hi) <= rmask) ? (int)(q.x & rmask) : r;
+            if (r >= 0 || q.w == kEmpty) return r;
+            b = (b + 1) & bmask;
+        }
+    }
+};
 
-    // true if v was not present before
+template <>
+struct HashSet<false> {
+    uint2* slot;  // (vertex, rank)
+    uint32_t bmask, rmask;
+    int bits, rb;
+    static constexpr int kBytesPerSlot = 8;
+    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
+    __device__ __forceinline__ void clear(int nslots) const {
+        for (int i = lane_id(); i < nslots; i += 32) slot[i] = make_uint2(kEmpty, 0);
+    }
     __device__ __forceinline__ bool insert(uint32_t v) const {
         uint32_t b = bucket(v);
         for (;;) {
-            uint32_t* bk = key + 4 * b;
 #pragma unroll
             for (int s = 0; s < 4; ++s) {
-                const uint32_t prev = atomicCAS(bk + s, kEmpty, v);
+                const uint32_t prev = atomicCAS(&slot[4 * b + s].x, kEmpty, v);
                 if (prev == kEmpty) return true;
                 if (prev == v) return false;
             }
             b = (b + 1) & bmask;
         }
     }
-    // slot index of v, or -1
     __device__ __forceinline__ int find_slot(uint32_t v) const {
         uint32_t b = bucket(v);
         for (;;) {
-            const uint4 q = *reinterpret_cast<const uint4*>(key + 4 * b);
-            if (q.x == v) return 4 * b;
-            if (q.y == v) return 4 * b + 1;
-            if (q.z == v) return 4 * b + 2;
-            if (q.w == v) return 4 * b + 3;
-            if (q.w == kEmpty) return -1;  // slots fill in order: bucket not full
+            const uint4 q0 = *reinterpret_cast<const uint4*>(slot + 4 * b);
+            const uint4 q1 = *reinterpret_cast<const uint4*>(slot + 4 * b + 2);
+            if (q0.x == v) return 4 * b;
+            if (q0.z == v) return 4 * b + 1;
+            if (q1.x == v) return 4 * b + 2;
+            if (q1.z == v) return 4 * b + 3;
+            if (q1.z == kEmpty) return -1;
             b = (b + 1) & bmask;
         }
     }
+    __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)].y = r; }
     __device__ __forceinline__ int find_rank(uint32_t v) const {
-        const int s = find_slot(v);
-        return s < 0 ? -1 : (int)rank[s];
+        uint32_t b = bucket(v);
+        for (;;) {
+            const uint4 q0 = *reinterpret_cast<const uint4*>(slot + 4 * b);
+            const uint4 q1 = *reinterpret_cast<const uint4*>(slot + 4 * b + 2);
+            int r = -1;
+            r = (q1.z == v) ? (int)q1.w : r;
+            r = (q1.x == v) ? (int)q1.y : r;
+            r = (q0.z == v) ? (int)q0.w : r;
+            r = (q0.x == v) ? (int)q0.y : r;
+            if (r >= 0 || q1.z == kEmpty) return r;
+            b = (b + 1) & bmask;
+        }
     }
 };
 
@@ -112,21 +185,25 @@ __device__ void sort_smem(int32_t* set, int U, int N) {
 // K2
 // ===========================================================================
 
-__global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
+template <bool PACKED>
+__global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     unsigned char* q = smem_raw + (size_t)warp * p.warp_bytes;
     const int nslots = 4 << p.nb_bits;
-    HashSet hs;
-    hs.key = (uint32_t*)q; q += 4 * nslots;
+    HashSet<PACKED> hs;
+    hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
+    q += HashSet<PACKED>::kBytesPerSlot * nslots;
     int32_t* set = (int32_t*)q; q += 4 * p.set_cap;
-    int32_t* rstart = (int32_t*)q; q += 4 * (p.row_cap + 4);
-    int32_t* rbase = (int32_t*)q; q += 4 * p.row_cap;
-    hs.rank = (uint16_t*)q; q += 2 * nslots;
+    uint16_t* wcur = reinterpret_cast<uint16_t*>(set);  // window -> row of its first entry (after set dies)
+    int32_t* rstart = (int32_t*)q; q += 4 * (p.row_cap + 36);
+    int32_t* rdelta = (int32_t*)q; q += 4 * p.row_cap;  // A position of a row entry = flat index + rdelta
     uint16_t* rrank = (uint16_t*)q;
     hs.bits = p.nb_bits;
     hs.bmask = (1u << p.nb_bits) - 1u;
+    hs.rb = p.rank_bits;
+    hs.rmask = (1u << p.rank_bits) - 1u;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned le = (2u << lane) - 1u;
 
@@ -137,7 +214,7 @@ __global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
         const int32_t root = tl[0];  // before the slot is overwritten by the set
 
         // ---- dedup: hash-insert the touched list, compact the new keys
-        for (int i = lane; i < nslots; i += 32) hs.key[i] = kEmpty;
+        hs.clear(nslots);
         __syncwarp();
         int U = 0;
         for (int b0 = 0; b0 < T; b0 += 32) {
@@ -157,9 +234,8 @@ __global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
         else if (U <= 64) sort_regs<2>(set, U);
         else if (U <= 128) sort_regs<4>(set, U);
         else if (U <= 256) sort_regs<8>(set, U);
-        else if (U <= 512) sort_regs<16>(set, U);
         else {
-            int N = 1024;
+            int N = 512;
             while (N < U) N <<= 1;
             sort_smem(set, U, N);
         }
@@ -171,7 +247,7 @@ __global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
             int32_t rb = 0, deg = 0;
             if (i < U) {
                 const int32_t u = set[i];
-                hs.rank[hs.find_slot((uint32_t)u)] = (uint16_t)i;
+                hs.set_rank((uint32_t)u, (uint32_t)i);
                 tl[i] = u;
                 rb = __ldg(p.a_rp + u);
                 deg = __ldg(p.a_rp + u + 1) - rb;
@@ -181,8 +257,9 @@ __global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
             const int incl = warp_incl_scan(deg);
             if (ne) {
                 const int qi = NR + __popc(nb & lt);
-                rstart[qi] = S + incl - deg;
-                rbase[qi] = rb;
+                const int st = S + incl - deg;
+                rstart[qi] = st;
+                rdelta[qi] = rb - st;
                 rrank[qi] = (uint16_t)i;
             }
             NR += __popc(nb);
@@ -191,42 +268,71 @@ __global__ void __launch_bounds__(128) k_extract(ExtractParams p) {
         if (lane == 0) rstart[NR] = S;
         __syncwarp();
 
-        // ---- induced subgraph: 4 windows of 32 entries per iteration
+        // ---- window cursors: row holding the first entry of each 32-window
+        for (int i = NR + 1 + lane; i <= NR + 32; i += 32) rstart[i] = 0x7fffffff;  // sentinels
+        const int nwin = (S + 31) >> 5;
+        const bool direct = nwin <= p.win_cap;
+        if (direct) {
+            for (int qi = lane; qi < NR; qi += 32) {
+                const int s0 = rstart[qi], s1 = rstart[qi + 1];
+                for (int w = (s0 + 31) >> 5; (w << 5) < s1; ++w) wcur[w] = (uint16_t)qi;
+            }
+        }
+        __syncwarp();
+
+        // ---- induced subgraph: scan the flattened rows in 32-entry windows
         int2* ed = p.escratch + (size_t)r * p.e_stride;
-        int cursor = 0, count = 0;
-        for (int w = 0; w < S; w += 128) {
-            int own[4], kk[4];
-            int32_t v[4];
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int ww = w + 32 * u;
-                const int rr = cursor + 1 + lane;
-                const int rs = rr <= NR ? rstart[rr] : 0x7fffffff;
-                const int off = rs - ww;
-                const unsigned bit = (off > 0 && off < 32) ? (1u << off) : 0u;
-                const unsigned M = __reduce_or_sync(kFull, bit);
-                own[u] = min(cursor + __popc(M & le), NR - 1);
-                const int own31 = __shfl_sync(kFull, own[u], 31);
-                cursor = (own31 + 1 <= NR && rstart[own31 + 1] == ww + 32) ? own31 + 1 : own31;
-                const int pos = ww + lane;
-                kk[u] = pos < S ? rbase[own[u]] + (pos - rstart[own[u]]) : -1;
-            }
-#pragma unroll
-            for (int u = 0; u < 4; ++u) v[u] = kk[u] >= 0 ? __ldg(p.a_ci + kk[u]) : -1;
-#pragma unroll
-            for (int u = 0; u < 4; ++u) {
-                const int j = v[u] >= 0 ? hs.find_rank((uint32_t)v[u]) : -1;
-                const bool hit = j >= 0;
-                const unsigned hb = __ballot_sync(kFull, hit);
-                if (hit) {
-                    const int t = count + __popc(hb & lt);
-                    if (t < p.e_stride) {
-                        const int32_t gid = p.a_gid ? __ldg(p.a_gid + kk[u]) : kk[u];
-                        ed[t] = make_int2(((int32_t)rrank[own[u]] << 16) | j, gid);
-                    }
+        int count = 0;
+        // Row owning lane's entry of window w, given the row c holding the
+        // window's first entry: c + #row starts in (base, base + lane].
+        auto owner = [&](int c, int base) -> int {
+            const int off = rstart[c + 1 + lane] - base;
+            const unsigned bit = ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u;
+            return c + __popc(__reduce_or_sync(kFull, bit) & le);
+        };
+        auto emit = [&](int j, int own, int kk) {
+            const bool hit = j >= 0;
+            const unsigned hb = __ballot_sync(kFull, hit);
+            if (hit) {
+                const int t = count + __popc(hb & lt);
+                if (t < p.e_stride) {
+                    const int32_t gid = p.a_gid ? __ldg(p.a_gid + kk) : kk;
+                    ed[t] = make_int2(((int32_t)rrank[own] << 16) | j, gid);
                 }
-                count += __popc(hb);
             }
+            count += __popc(hb);
+        };
+        int w = 0;
+        if (direct) {
+            const int nfull = S >> 5;  // windows with all 32 entries valid
+            for (; w + 4 <= nfull; w += 4) {
+                int own[4], kk[4];
+                uint32_t v[4];
+#pragma unroll
+                for (int u = 0; u < 4; ++u) {
+                    const int base = (w + u) << 5;
+                    own[u] = owner((int)wcur[w + u], base);
+                    kk[u] = base + lane + rdelta[own[u]];
+                }
+#pragma unroll
+                for (int u = 0; u < 4; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
+#pragma unroll
+                for (int u = 0; u < 4; ++u) emit(hs.find_rank(v[u]), own[u], kk[u]);
+            }
+        }
+        int cursor = direct ? 0 : 0;
+        for (; w < nwin; ++w) {  // tail windows (and every window of huge sets)
+            const int base = w << 5;
+            const int c = direct ? (int)wcur[w] : cursor;
+            const int own = min(owner(c, base), NR - 1);
+            if (!direct) {
+                const int own31 = __shfl_sync(kFull, own, 31);
+                cursor = (rstart[own31 + 1] == base + 32) ? own31 + 1 : own31;
+            }
+            const int pos = base + lane;
+            const int kk = pos < S ? pos + rdelta[own] : -1;
+            const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
+            emit(j, own, kk);
         }
         if (lane == 0) {
             p.root_nv[r] = U;
@@ -477,16 +583,18 @@ __global__ void k_stats(const int32_t* __restrict__ level_counts, int32_t depth,
 
 // ---- launchers -----------------------------------------------------------------
 
-void launch_extract(int grid, size_t smem, const ExtractParams& xp, cudaStream_t st) {
-    HGS_CUDA(cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_extract<<<grid, 128, smem, st>>>(xp);
+void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st) {
+    auto kern = packed ? k_extract<true> : k_extract<false>;
+    HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    kern<<<grid, 128, smem, st>>>(xp);
     HGS_CUDA(cudaGetLastError());
 }
 
-int extract_blocks_per_sm(size_t smem) {
-    HGS_CUDA(cudaFuncSetAttribute(k_extract, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+int extract_blocks_per_sm(size_t smem, bool packed) {
+    auto kern = packed ? k_extract<true> : k_extract<false>;
+    HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_extract, 128, smem));
+    HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
     return per_sm > 0 ? per_sm : 1;
 }
 

@@ -27,6 +27,7 @@ struct ExpandParams {
     int32_t R, depth, fanout, n;
     int64_t stride;
     int32_t cache_entries;                // (b,deg) entries cached per lane in smem
+    int32_t recip_smem;                   // recip entries staged in smem (0: read global)
     int32_t* __restrict__ touched;
     int32_t* __restrict__ tcount;
     int32_t* __restrict__ level_counts;
@@ -54,7 +55,7 @@ struct ExtractParams {
     int2* __restrict__ escratch;        // per root: e_stride x (local i<<16 | j, edge id)
     int32_t e_stride;
     int32_t* __restrict__ ticket;
-    int32_t nb_bits, set_cap, row_cap, warp_bytes;
+    int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
 };
 
 // K3: packing + gather.
@@ -86,8 +87,8 @@ struct PackParams {
     int32_t* __restrict__ ticket;
 };
 
-void launch_extract(int grid, size_t smem, const ExtractParams& xp, cudaStream_t st);
-int extract_blocks_per_sm(size_t smem);
+void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st);
+int extract_blocks_per_sm(size_t smem, bool packed);
 void launch_scan(const int32_t* nv, const int32_t* ne, int32_t R, int64_t* tmp, int32_t* voff,
                  int32_t* eoff, int32_t* ticket, cudaStream_t st);
 int64_t scan_tmp_words(int64_t R);

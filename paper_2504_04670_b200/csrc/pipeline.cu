@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <string>
 #include <vector>
 
@@ -30,10 +31,11 @@ struct CallPlan {
     int64_t kmax, max_t, cache_entries;
     int expand_threads;
     size_t expand_smem;
-    int32_t nb_bits, set_cap, row_cap, warp_bytes;
+    int32_t recip_smem;
+    int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
 };
 
-CallPlan plan_call(const DevCsr& walk, int64_t depth, int64_t fanout) {
+CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
     CallPlan c{};
     c.kmax = std::min<int64_t>(fanout, walk.max_deg);
     if (c.kmax > 256) fail(HGS_ERANGE, "hgs: min(fanout, max degree) > 256 is not supported by this build");
@@ -42,34 +44,45 @@ CallPlan plan_call(const DevCsr& walk, int64_t depth, int64_t fanout) {
         fail(HGS_ERANGE, "hgs: per-root tree bound " + std::to_string(c.max_t) +
                              " exceeds this build's limit (32767); reduce depth/fanout");
     c.cache_entries = tree_bound(c.kmax, depth - 1);
+    c.recip_smem = walk.max_deg + 1 <= 4096 ? walk.max_deg + 1 : 0;
+    const size_t rbytes = (size_t)c.recip_smem * sizeof(uint64_t);
     c.expand_threads = 128;
-    c.expand_smem = (size_t)c.cache_entries * 128 * sizeof(int2);
+    c.expand_smem = (size_t)c.cache_entries * 128 * sizeof(int2) + rbytes;
     if (c.expand_smem > 96 * 1024) {
         c.expand_threads = 64;
-        c.expand_smem = (size_t)c.cache_entries * 64 * sizeof(int2);
+        c.expand_smem = (size_t)c.cache_entries * 64 * sizeof(int2) + rbytes;
         if (c.expand_smem > 96 * 1024) {
             c.cache_entries = 0;
-            c.expand_smem = 0;
+            c.expand_smem = rbytes;
             c.expand_threads = 128;
         }
     }
-    // hash set: 4-slot buckets, >= 4 slots per possible key
+    // K2 hash set: 4-slot buckets, HGS_HASH_SLOTS_PER_KEY (default 4) slots per
+    // possible key; entries pack (vertex << rank_bits | rank) into 32 bits when
+    // vertex ids leave room, else (vertex, rank) 64-bit pairs.
+    int spk = 3;
+    if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) spk = std::max(2, atoi(e));
+    c.rank_bits = 1;
+    while (((int64_t)1 << c.rank_bits) < c.max_t) ++c.rank_bits;
+    c.packed = (n + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
     int bits = 2;
-    while ((4 << bits) < 4 * c.max_t) ++bits;
+    while (((int64_t)4 << bits) < spk * c.max_t) ++bits;
     c.nb_bits = bits;
     c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);
-    if (c.max_t > 512) {
-        int n = 1024;
-        while (n < c.max_t) n <<= 1;
-        c.set_cap = n;
+    if (c.max_t > 256) {  // sets above 256 are sorted in place in shared memory
+        int nn = 512;
+        while (nn < c.max_t) nn <<= 1;
+        c.set_cap = nn;
     }
     c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
+    c.win_cap = 2 * c.set_cap;  // u16 window cursors alias the set array
     const size_t slots = (size_t)4 << c.nb_bits;
-    size_t bytes = 4 * slots + 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 4) + 4 * (size_t)c.row_cap +
-                   2 * slots + 2 * (size_t)c.row_cap;
+    size_t bytes = (c.packed ? 4 : 8) * slots + 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) +
+                   4 * (size_t)c.row_cap + 2 * (size_t)c.row_cap;
     bytes = (bytes + 15) / 16 * 16;
     c.warp_bytes = (int32_t)bytes;
     if (4 * bytes > 200 * 1024) fail(HGS_ERANGE, "hgs: per-root working set too large for shared memory");
+    (void)a;
     return c;
 }
 
@@ -88,7 +101,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     const DevCsr& walk = cfg.symmetrize ? g.walk_sym : g.a;
     graph_ensure_recip(g, walk.max_deg);
     if (cfg.gather && !g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
-    const CallPlan c = plan_call(walk, cfg.depth, cfg.fanout);
+    const CallPlan c = plan_call(walk, g.a, g.n_rows, cfg.depth, cfg.fanout);
     const int64_t R = in.R, k = in.k;
     if (R * c.max_t >= ((int64_t)1 << 40)) fail(HGS_ERANGE, "hgs: too many roots for one call");
     cudaStream_t st = s->stream;
@@ -145,6 +158,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         ep.R = (int32_t)R; ep.depth = (int32_t)cfg.depth;
         ep.fanout = (int32_t)std::min<int64_t>(cfg.fanout, 1 << 30);
         ep.n = (int32_t)g.n_rows; ep.stride = c.max_t; ep.cache_entries = (int32_t)c.cache_entries;
+        ep.recip_smem = c.recip_smem;
         ep.touched = s->touched.p; ep.tcount = s->tcount.p; ep.level_counts = s->level_counts.p;
         ep.draws = s->draws.p; ep.decisions = s->decisions.p; ep.ticket = s->ticket.p;
         launch_expand(c.expand_threads, c.expand_smem, c.kmax, ep, cfg.rng == HGS_RNG_PHILOX, st);
@@ -158,11 +172,11 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
         xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
         xp.ticket = s->ticket.p; xp.nb_bits = c.nb_bits; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
-        xp.warp_bytes = c.warp_bytes;
+        xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
         const size_t smem = (size_t)4 * c.warp_bytes;
-        const int per_sm = extract_blocks_per_sm(smem);
+        const int per_sm = extract_blocks_per_sm(smem, c.packed != 0);
         const int64_t grid = std::min<int64_t>((int64_t)per_sm * sm_count(g.device), (R + 3) / 4);
-        launch_extract((int)std::max<int64_t>(grid, 1), smem, xp, st);
+        launch_extract((int)std::max<int64_t>(grid, 1), smem, xp, c.packed != 0, st);
         ++s->launches;
     }
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
