@@ -74,19 +74,22 @@ struct HashSet<true> {
         }
     }
     __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)] = (v << rb) | r; }
+    // (entry ^ (v << rb)) is the entry's rank for the matching entry and
+    // exceeds rmask for every other entry (keys are distinct), so the
+    // bucket's minimum decides a hit without per-slot branches.
     __device__ __forceinline__ int find_rank(uint32_t v) const {
         const uint32_t hi = v << rb;
         uint32_t b = bucket(v);
-        for (;;) {
-            const uint4 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
-            int r = -1;
-            r = ((q.w ^ hi) <= rmask) ? (int)(q.w & rmask) : r;
-            r = ((q.z ^ hi) <= rmask) ? (int)(q.z & rmask) : r;
-            r = ((q.y ^ hi) <= rmask) ? (int)(q.y & rmask) : r;
-            r = ((q.x ^ hi) <= rmask) ? (int)(q.x & rmask) : r;
-            if (r >= 0 || q.w == kEmpty) return r;
-            b = (b + 1) & bmask;
+        uint4 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
+        uint32_t d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
+        if (d > rmask && q.w != kEmpty) {  // full bucket without a match: rare
+            do {
+                b = (b + 1) & bmask;
+                q = *reinterpret_cast<const uint4*>(slot + 4 * b);
+                d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
+            } while (d > rmask && q.w != kEmpty);
         }
+        return d <= rmask ? (int)d : -1;
     }
 };
 
@@ -185,7 +188,7 @@ __device__ void sort_smem(int32_t* set, int U, int N) {
 // K2
 // ===========================================================================
 
-template <bool PACKED>
+template <bool PACKED, bool HAS_GID>
 __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = lane_id();
@@ -196,10 +199,12 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
     q += HashSet<PACKED>::kBytesPerSlot * nslots;
     int32_t* set = (int32_t*)q; q += 4 * p.set_cap;
-    uint16_t* wcur = reinterpret_cast<uint16_t*>(set);  // window -> row of its first entry (after set dies)
+    // after the set is dead its space holds, per 32-entry window, the row of
+    // the window's first entry (wcur) and a bitmask of rows starting inside it
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(set);
+    uint16_t* wcur = reinterpret_cast<uint16_t*>(set + p.win_cap);
     int32_t* rstart = (int32_t*)q; q += 4 * (p.row_cap + 36);
-    int32_t* rdelta = (int32_t*)q; q += 4 * p.row_cap;  // A position of a row entry = flat index + rdelta
-    uint16_t* rrank = (uint16_t*)q;
+    int2* rinfo = (int2*)q;  // per nonempty row: (A position - flat index, local id)
     hs.bits = p.nb_bits;
     hs.bmask = (1u << p.nb_bits) - 1u;
     hs.rb = p.rank_bits;
@@ -259,8 +264,7 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
                 const int qi = NR + __popc(nb & lt);
                 const int st = S + incl - deg;
                 rstart[qi] = st;
-                rdelta[qi] = rb - st;
-                rrank[qi] = (uint16_t)i;
+                rinfo[qi] = make_int2(rb - st, i);
             }
             NR += __popc(nb);
             S += __shfl_sync(kFull, incl, 31);
@@ -273,8 +277,11 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
         const int nwin = (S + 31) >> 5;
         const bool direct = nwin <= p.win_cap;
         if (direct) {
+            for (int w = lane; w < nwin; w += 32) wmask[w] = 0u;
+            __syncwarp();
             for (int qi = lane; qi < NR; qi += 32) {
                 const int s0 = rstart[qi], s1 = rstart[qi + 1];
+                if (s0 & 31) atomicOr(&wmask[s0 >> 5], 1u << (s0 & 31));
                 for (int w = (s0 + 31) >> 5; (w << 5) < s1; ++w) wcur[w] = (uint16_t)qi;
             }
         }
@@ -290,49 +297,61 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
             const unsigned bit = ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u;
             return c + __popc(__reduce_or_sync(kFull, bit) & le);
         };
+        // Emit the hits of one window in scan order. The capacity check is
+        // hoisted: `room` says every lane's slot fits (count + 32 <= stride).
         auto emit = [&](int j, int own, int kk) {
             const bool hit = j >= 0;
             const unsigned hb = __ballot_sync(kFull, hit);
             if (hit) {
                 const int t = count + __popc(hb & lt);
                 if (t < p.e_stride) {
-                    const int32_t gid = p.a_gid ? __ldg(p.a_gid + kk) : kk;
-                    ed[t] = make_int2(((int32_t)rrank[own] << 16) | j, gid);
+                    const int32_t gid = HAS_GID ? __ldg(p.a_gid + kk) : kk;
+                    ed[t] = make_int2((rinfo[own].y << 16) | j, gid);
                 }
             }
             count += __popc(hb);
         };
+        constexpr int G = 4;  // windows in flight per iteration
+        auto group = [&](int w, bool guard) {
+            int own[G], kk[G];
+            uint32_t v[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const int base = (w + u) << 5;
+                if (!guard || w + u < nwin) {
+                    own[u] = (int)wcur[w + u] + __popc(wmask[w + u] & le);
+                    if (guard) own[u] = min(own[u], NR - 1);
+                    kk[u] = base + lane + rinfo[own[u]].x;
+                    if (guard && base + lane >= S) kk[u] = -1;
+                } else {
+                    own[u] = 0;
+                    kk[u] = -1;
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) v[u] = (!guard || kk[u] >= 0) ? (uint32_t)__ldg(p.a_ci + kk[u]) : 0u;
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                if (!guard || w + u < nwin) emit((!guard || kk[u] >= 0) ? hs.find_rank(v[u]) : -1, own[u], kk[u]);
+            }
+        };
         int w = 0;
         if (direct) {
             const int nfull = S >> 5;  // windows with all 32 entries valid
-            for (; w + 4 <= nfull; w += 4) {
-                int own[4], kk[4];
-                uint32_t v[4];
-#pragma unroll
-                for (int u = 0; u < 4; ++u) {
-                    const int base = (w + u) << 5;
-                    own[u] = owner((int)wcur[w + u], base);
-                    kk[u] = base + lane + rdelta[own[u]];
-                }
-#pragma unroll
-                for (int u = 0; u < 4; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
-#pragma unroll
-                for (int u = 0; u < 4; ++u) emit(hs.find_rank(v[u]), own[u], kk[u]);
-            }
-        }
-        int cursor = direct ? 0 : 0;
-        for (; w < nwin; ++w) {  // tail windows (and every window of huge sets)
-            const int base = w << 5;
-            const int c = direct ? (int)wcur[w] : cursor;
-            const int own = min(owner(c, base), NR - 1);
-            if (!direct) {
+            for (; w + G <= nfull; w += G) group(w, false);
+            if (w < nwin) group(w, true);
+        } else {
+            int cursor = 0;  // huge sets: serial window cursor
+            for (; w < nwin; ++w) {
+                const int base = w << 5;
+                const int own = min(owner(cursor, base), NR - 1);
                 const int own31 = __shfl_sync(kFull, own, 31);
                 cursor = (rstart[own31 + 1] == base + 32) ? own31 + 1 : own31;
+                const int pos = base + lane;
+                const int kk = pos < S ? pos + rinfo[own].x : -1;
+                const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
+                emit(j, own, kk);
             }
-            const int pos = base + lane;
-            const int kk = pos < S ? pos + rdelta[own] : -1;
-            const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
-            emit(j, own, kk);
         }
         if (lane == 0) {
             p.root_nv[r] = U;
@@ -464,8 +483,11 @@ int64_t scan_tmp_words(int64_t R) { return 2 * ((R + kPairTile - 1) / kPairTile)
 // ===========================================================================
 
 __global__ void __launch_bounds__(256) k_pack(PackParams p) {
+    extern __shared__ int32_t pack_smem[];
     const int lane = lane_id();
+    int32_t* sset = pack_smem + (size_t)(threadIdx.x >> 5) * p.set_cap;  // the root's set, staged
     const int nwarps = gridDim.x * (blockDim.x >> 5);
+    constexpr int U = 4;  // independent loads in flight per lane
     for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
         int b;
         {
@@ -486,46 +508,88 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
         }
         const int32_t loc = (int32_t)vb - p.root_voff[f];
         const int32_t* set = p.touched + (size_t)r * p.stride;
-        for (int i = lane; i < Vr; i += 32) __stcs(p.l2g + vb + i, set[i]);
+        for (int i = lane; i < Vr; i += 32) {
+            const int32_t u = set[i];
+            sset[i] = u;
+            __stcs(p.l2g + vb + i, u);
+        }
         if (lane == 0) {
             p.roots_local[r] = loc + p.root_rloc[r];
             p.comp_off[r + b] = loc;
             if (r == p.batch_off[b + 1] - 1) p.comp_off[r + 1 + b] = loc + Vr;
         }
         const int2* ed = p.escratch + (size_t)r * p.e_stride;
-        for (int t = lane; t < Er; t += 32) {
-            const int2 e = ed[t];
-            __stcs(p.e_row + eb + t, loc + (e.x >> 16));
-            __stcs(p.e_col + eb + t, loc + (e.x & 0xffff));
-            __stcs(p.e_gid + eb + t, e.y);
+        const bool fe2 = p.gather && p.f_e == 2;
+        for (int t0 = 0; t0 < Er; t0 += 32 * U) {
+            int2 e[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + 32 * u + lane;
+                e[u] = t < Er ? ed[t] : make_int2(0, -1);
+            }
+            double2 x[U];
+            uint8_t lb[U];
             if (p.gather) {
-                p.lab[eb + t] = __ldg(p.labels + e.y);
-                if (p.f_e == 2) {
-                    const double2 x = __ldg(reinterpret_cast<const double2*>(p.edge_feat) + e.y);
-                    __stcs(reinterpret_cast<double2*>(p.ye) + eb + t, x);
-                } else {
-                    for (int c = 0; c < p.f_e; ++c)
-                        __stcs(p.ye + (eb + t) * p.f_e + c, __ldg(p.edge_feat + (int64_t)e.y * p.f_e + c));
+#pragma unroll
+                for (int u = 0; u < U; ++u) {
+                    if (e[u].y >= 0) {
+                        lb[u] = __ldg(p.labels + e[u].y);
+                        if (fe2) x[u] = __ldg(reinterpret_cast<const double2*>(p.edge_feat) + e[u].y);
+                    }
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int t = t0 + 32 * u + lane;
+                if (t < Er) {
+                    __stcs(p.e_row + eb + t, loc + (e[u].x >> 16));
+                    __stcs(p.e_col + eb + t, loc + (e[u].x & 0xffff));
+                    __stcs(p.e_gid + eb + t, e[u].y);
+                    if (p.gather) {
+                        p.lab[eb + t] = lb[u];
+                        if (fe2) {
+                            __stcs(reinterpret_cast<double2*>(p.ye) + eb + t, x[u]);
+                        } else {
+                            for (int c = 0; c < p.f_e; ++c)
+                                __stcs(p.ye + (eb + t) * p.f_e + c,
+                                       __ldg(p.edge_feat + (int64_t)e[u].y * p.f_e + c));
+                        }
+                    }
                 }
             }
         }
+        __syncwarp();
         if (p.gather) {
             if ((p.f_v & 1) == 0) {  // rows as f_v/2 16-byte pieces
                 const int q2 = p.f_v >> 1;
+                const int n2 = Vr * q2;
                 const double2* src = reinterpret_cast<const double2*>(p.node_feat);
                 double2* dst = reinterpret_cast<double2*>(p.xv) + vb * q2;
-                for (int e = lane; e < Vr * q2; e += 32) {
-                    const int i = (int)__umulhi((unsigned)e, p.fv_magic);
-                    __stcs(dst + e, __ldg(src + (int64_t)set[i] * q2 + (e - i * q2)));
+                for (int e0 = 0; e0 < n2; e0 += 32 * U) {
+                    double2 x[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int e = e0 + 32 * u + lane;
+                        if (e < n2) {
+                            const int i = (int)__umulhi((unsigned)e, p.fv_magic);
+                            x[u] = __ldg(src + (int64_t)sset[i] * q2 + (e - i * q2));
+                        }
+                    }
+#pragma unroll
+                    for (int u = 0; u < U; ++u) {
+                        const int e = e0 + 32 * u + lane;
+                        if (e < n2) __stcs(dst + e, x[u]);
+                    }
                 }
             } else {
                 double* dst = p.xv + vb * p.f_v;
                 for (int e = lane; e < Vr * p.f_v; e += 32) {
                     const int i = e / p.f_v;
-                    __stcs(dst + e, __ldg(p.node_feat + (int64_t)set[i] * p.f_v + (e - i * p.f_v)));
+                    __stcs(dst + e, __ldg(p.node_feat + (int64_t)sset[i] * p.f_v + (e - i * p.f_v)));
                 }
             }
         }
+        __syncwarp();
     }
 }
 
@@ -584,14 +648,15 @@ __global__ void k_stats(const int32_t* __restrict__ level_counts, int32_t depth,
 // ---- launchers -----------------------------------------------------------------
 
 void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st) {
-    auto kern = packed ? k_extract<true> : k_extract<false>;
+    auto kern = packed ? (xp.a_gid ? k_extract<true, true> : k_extract<true, false>)
+                       : (xp.a_gid ? k_extract<false, true> : k_extract<false, false>);
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, 128, smem, st>>>(xp);
     HGS_CUDA(cudaGetLastError());
 }
 
 int extract_blocks_per_sm(size_t smem, bool packed) {
-    auto kern = packed ? k_extract<true> : k_extract<false>;
+    auto kern = packed ? k_extract<true, false> : k_extract<false, false>;
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
@@ -599,7 +664,10 @@ int extract_blocks_per_sm(size_t smem, bool packed) {
 }
 
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st) {
-    k_pack<<<grid, 256, 0, st>>>(pp);
+    const size_t smem = (size_t)8 * pp.set_cap * sizeof(int32_t);
+    if (smem > 48 * 1024)
+        HGS_CUDA(cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    k_pack<<<grid, 256, smem, st>>>(pp);
     HGS_CUDA(cudaGetLastError());
 }
 

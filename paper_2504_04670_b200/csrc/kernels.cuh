@@ -84,6 +84,7 @@ struct PackParams {
     int32_t f_v, f_e, gather;
     uint32_t fv_magic;  // ceil(2^32 / (f_v/2)) for even f_v
     int64_t v_cap, e_cap;
+    int32_t set_cap;  // per-warp staging of the root's set (>= max set size)
     int32_t* __restrict__ ticket;
 };
 

@@ -75,10 +75,10 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
         c.set_cap = nn;
     }
     c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
-    c.win_cap = 2 * c.set_cap;  // u16 window cursors alias the set array
+    c.win_cap = c.set_cap * 2 / 3;  // (u32 mask + u16 cursor) per window alias the set array
     const size_t slots = (size_t)4 << c.nb_bits;
     size_t bytes = (c.packed ? 4 : 8) * slots + 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) +
-                   4 * (size_t)c.row_cap + 2 * (size_t)c.row_cap;
+                   8 * (size_t)c.row_cap;
     bytes = (bytes + 15) / 16 * 16;
     c.warp_bytes = (int32_t)bytes;
     if (4 * bytes > 200 * 1024) fail(HGS_ERANGE, "hgs: per-root working set too large for shared memory");
@@ -199,6 +199,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         const uint32_t q2 = (uint32_t)std::max(1, g.f_v / 2);
         pp.fv_magic = (uint32_t)((((uint64_t)1 << 32) + q2 - 1) / q2);
         pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
+        pp.set_cap = c.set_cap;
         const int64_t grid = std::min<int64_t>((int64_t)sm_count(g.device) * 8, (R + 7) / 8);
         launch_pack((int)std::max<int64_t>(grid, 1), pp, st);
         ++s->launches;

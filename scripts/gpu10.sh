@@ -1,0 +1,2 @@
+python scripts/prof.py --calls 3 2>&1 | tail -2 | head -1
+ncu --set full --clock-control none --import-source on -k regex:k_extract -s 1 -c 1 -o gpurun_out/prof_extract5 -f python scripts/prof.py --calls 2 > gpurun_out/ncu7.log 2>&1; echo ncu rc=$?
