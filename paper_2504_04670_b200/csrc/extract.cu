@@ -239,10 +239,15 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
         else if (U <= 64) sort_regs<2>(set, U);
         else if (U <= 128) sort_regs<4>(set, U);
         else if (U <= 256) sort_regs<8>(set, U);
-        else {
+        else {  // large sets: bitonic in the (not yet used) row arrays
             int N = 512;
             while (N < U) N <<= 1;
-            sort_smem(set, U, N);
+            int32_t* scr = rstart;
+            for (int i = lane; i < U; i += 32) scr[i] = set[i];
+            __syncwarp();
+            sort_smem(scr, U, N);
+            for (int i = lane; i < U; i += 32) set[i] = scr[i];
+            __syncwarp();
         }
 
         // ---- ranks, the sorted set back to global, nonempty A rows

@@ -68,12 +68,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     int bits = 2;
     while (((int64_t)4 << bits) < spk * c.max_t) ++bits;
     c.nb_bits = bits;
-    c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);
-    if (c.max_t > 256) {  // sets above 256 are sorted in place in shared memory
-        int nn = 512;
-        while (nn < c.max_t) nn <<= 1;
-        c.set_cap = nn;
-    }
+    c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);  // sets > 256 sort in the row arrays
     c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
     c.win_cap = c.set_cap * 2 / 3;  // (u32 mask + u16 cursor) per window alias the set array
     const size_t slots = (size_t)4 << c.nb_bits;
