@@ -71,7 +71,15 @@ typedef struct {
     int32_t rng;          /* HGS_RNG_* */
     int32_t gather;       /* also gather node/edge features + labels */
     int32_t profile;      /* record per-kernel CUDA event times */
+    int32_t flags;        /* HGS_FLAG_* */
 } hgs_config;
+
+/* shadow_reference semantics for the unsymmetrized walk: sample over the raw
+ * rows of A (explicit zeros included, no negative-value check), as
+ * sampler.cpp:104-106 does, instead of bulk_shadow's row_normalize(spgemm(Q, A))
+ * support (zeros dropped, negatives rejected; sampler.cpp:161). The two
+ * differ only when A stores explicit zeros or negative values. */
+#define HGS_FLAG_SEQ_WALK 1
 
 /* Host destinations for hgs_sample_copy_to_host (any pointer may be NULL). */
 typedef struct {

@@ -269,6 +269,19 @@ or_result* or_bulk_shadow(int64_t n_rows, int64_t n_cols, const int64_t* rp, con
                           int symmetrize, const double* node_feat, int64_t f_v,
                           const double* edge_feat, int64_t f_e, const uint8_t* labels,
                           char* err, int errlen) {
+    return or_bulk_shadow_ex(n_rows, n_cols, rp, ci, values, roots, batch_off, n_batches, seeds,
+                             NULL, rng_kind, depth, fanout, symmetrize, 0, node_feat, f_v,
+                             edge_feat, f_e, labels, err, errlen);
+}
+
+or_result* or_bulk_shadow_ex(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int64_t* ci,
+                             const double* values, const int64_t* roots,
+                             const int64_t* batch_off, int64_t n_batches,
+                             const uint64_t* seeds, const uint64_t* state, int rng_kind,
+                             int64_t depth, int64_t fanout, int symmetrize, int flags,
+                             const double* node_feat, int64_t f_v, const double* edge_feat,
+                             int64_t f_e, const uint8_t* labels, char* err, int errlen) {
+    const int seq_walk = (flags & 1) != 0;
     char msg[256];
     /* SamplerConfig::validate (sampler.cpp:57-62) */
     if (depth < 1) { set_err(err, errlen, "SamplerConfig: depth must be >= 1"); return NULL; }
@@ -312,7 +325,7 @@ or_result* or_bulk_shadow(int64_t n_rows, int64_t n_cols, const int64_t* rp, con
         wci = (int64_t*)malloc(sizeof(int64_t) * (size_t)(2 * nnz + 1));
         or_symmetrize(n, rp, ci, wrp, wci);
     } else {
-        wrp = (int64_t*)rp; wci = (int64_t*)ci; wval = values;
+        wrp = (int64_t*)rp; wci = (int64_t*)ci; wval = seq_walk ? NULL : values;
     }
 
     /* Stacked Q: one row per root (sampler.cpp:132-145). Level l's frontier
@@ -327,7 +340,10 @@ or_result* or_bulk_shadow(int64_t n_rows, int64_t n_cols, const int64_t* rp, con
     or_xoshiro* streams = NULL;
     if (rng_kind == OR_RNG_XOSHIRO) {
         streams = (or_xoshiro*)malloc(sizeof(or_xoshiro) * (size_t)(R ? R : 1));
-        for (int64_t r = 0; r < R; ++r) or_xoshiro_seed(&streams[r], seeds[r]);
+        for (int64_t r = 0; r < R; ++r) {
+            if (state) memcpy(streams[r].s, state + 4 * r, sizeof(streams[r].s));
+            else or_xoshiro_seed(&streams[r], seeds[r]);
+        }
     }
 
     int64_t** lvl_col = (int64_t**)calloc((size_t)depth + 1, sizeof(int64_t*));
@@ -379,7 +395,8 @@ or_result* or_bulk_shadow(int64_t n_rows, int64_t n_cols, const int64_t* rp, con
                 got = choose_with(xo_draw, &c, (uint32_t)deg, kk, pos);
             } else {
                 ph_ctx c = {{(uint32_t)seeds[root], (uint32_t)(seeds[root] >> 32)},
-                            (uint32_t)res->decisions[root], &res->draws[root]};
+                            (uint32_t)(res->decisions[root] + (state ? state[root] : 0)),
+                            &res->draws[root]};
                 got = choose_with(ph_draw, &c, (uint32_t)deg, kk, pos);
             }
             ++res->decisions[root];
@@ -479,6 +496,7 @@ or_result* or_bulk_shadow(int64_t n_rows, int64_t n_cols, const int64_t* rp, con
                 goto fail;
             }
             res->e_gid[e] = id;
+            res->e_val[e] = 1.0; /* gather_features resets values (sampler.cpp:240) */
             res->lab[e] = labels[id];
             memcpy(res->ye + e * f_e, edge_feat + id * f_e, sizeof(double) * (size_t)f_e);
         }

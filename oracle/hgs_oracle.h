@@ -70,6 +70,19 @@ or_result* or_bulk_shadow(int64_t n_rows, int64_t n_cols, const int64_t* rp, con
                           const double* edge_feat, int64_t f_e, const uint8_t* labels,
                           char* err, int errlen);
 
+/* Extended form: state (nullable) resumes non-fresh per-root streams —
+ * xoshiro: 4 state words per root; philox: decisions already consumed per
+ * root. flags & 1 = shadow_reference walk semantics for the unsymmetrized
+ * walk (raw rows of A, explicit zeros kept, no negative check;
+ * sampler.cpp:104-106) instead of bulk_shadow's spgemm support. */
+or_result* or_bulk_shadow_ex(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int64_t* ci,
+                             const double* values, const int64_t* roots,
+                             const int64_t* batch_off, int64_t n_batches,
+                             const uint64_t* seeds, const uint64_t* state, int rng_kind,
+                             int64_t depth, int64_t fanout, int symmetrize, int flags,
+                             const double* node_feat, int64_t f_v, const double* edge_feat,
+                             int64_t f_e, const uint8_t* labels, char* err, int errlen);
+
 /* counts: [0]=n_batches [1]=R [2]=V [3]=E [4]=f_v [5]=f_e [6]=gathered [7]=depth */
 void or_result_counts(const or_result* r, int64_t* counts);
 /* Any pointer may be NULL. Layout (flat over batches, batch-local indices):

@@ -72,6 +72,10 @@ def _oracle() -> C.CDLL:
         lib.or_bulk_shadow.argtypes = [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_int64,
                                        _vp, C.c_int, C.c_int64, C.c_int64, C.c_int, _vp, C.c_int64,
                                        _vp, C.c_int64, _vp, C.c_char_p, C.c_int]
+        lib.or_bulk_shadow_ex.restype = _vp
+        lib.or_bulk_shadow_ex.argtypes = [C.c_int64, C.c_int64, _vp, _vp, _vp, _vp, _vp, C.c_int64,
+                                          _vp, _vp, C.c_int, C.c_int64, C.c_int64, C.c_int, C.c_int,
+                                          _vp, C.c_int64, _vp, C.c_int64, _vp, C.c_char_p, C.c_int]
         lib.or_result_counts.argtypes = [_vp, _i64p]
         lib.or_result_touched_total.restype = C.c_int64
         lib.or_result_touched_total.argtypes = [_vp]
@@ -183,7 +187,8 @@ def _c(a, dt):
 
 
 def bulk_shadow(g: Graph, roots, batch_off, seeds, *, rng=RNG_XOSHIRO, depth=3, fanout=6,
-                symmetrize=True, gather=False, impl="oracle", mode=0) -> Sample:
+                symmetrize=True, gather=False, impl="oracle", mode=0, state=None,
+                seq_walk=False) -> Sample:
     """Run the checker. impl="oracle" (C restatement) or "ref" (reference).
     mode (ref only): 0 bulk_shadow, 1 per-batch shadow_reference, 2 bulk with
     a FrontierObserver capturing Q per level."""
@@ -202,9 +207,11 @@ def bulk_shadow(g: Graph, roots, batch_off, seeds, *, rng=RNG_XOSHIRO, depth=3, 
     err = C.create_string_buffer(512)
     if impl == "oracle":
         lib = _oracle()
-        h = lib.or_bulk_shadow(g.n, n_cols, _ptr(rp), _ptr(ci), _ptr(vals), _ptr(roots),
-                               _ptr(batch_off), k, _ptr(seeds), rng, depth, fanout,
-                               int(symmetrize), _ptr(nf), f_v, _ptr(ef), f_e, _ptr(lab), err, 512)
+        st = _c(state, np.uint64)
+        h = lib.or_bulk_shadow_ex(g.n, n_cols, _ptr(rp), _ptr(ci), _ptr(vals), _ptr(roots),
+                                  _ptr(batch_off), k, _ptr(seeds), _ptr(st), rng, depth, fanout,
+                                  int(symmetrize), 1 if seq_walk else 0, _ptr(nf), f_v, _ptr(ef),
+                                  f_e, _ptr(lab), err, 512)
         if not h:
             raise SamplerError(err.value.decode())
         cnt = np.zeros(8, np.int64)

@@ -6,6 +6,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <cstdlib>
 #include <cstring>
 #include <string>
 #include <vector>
@@ -274,6 +275,9 @@ int hgs_sample_create(hgs_graph* g, void* stream, hgs_sample** out) {
         HGS_CUDA(cudaSetDevice(g->g.device));
         auto* s = new hgs_sample;
         s->graph = g;
+        // test hooks: start with tiny capacities to exercise the regrow path
+        if (const char* e = getenv("HGS_E_STRIDE")) s->e_stride = std::max(1, atoi(e));
+        if (const char* e = getenv("HGS_E_CAP")) s->e_cap = (size_t)std::max(1, atoi(e));
         if (stream) s->stream = (cudaStream_t)stream;
         else {
             HGS_CUDA(cudaStreamCreateWithFlags(&s->stream, cudaStreamNonBlocking));

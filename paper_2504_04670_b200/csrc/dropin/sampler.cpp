@@ -49,7 +49,8 @@ bool values_are_ids(const CsrMatrix& a) {
 std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
                                    const std::vector<std::vector<Index>>& batches,
                                    const SamplerConfig& cfg, ChoiceSource& choice, bool gather,
-                                   const std::vector<double>* values, Index f_v, Index f_e) {
+                                   const std::vector<double>* values, Index f_v, Index f_e,
+                                   bool seq_walk = false) {
     cfg.validate();
     auto* per_root = dynamic_cast<PerRootChoiceSource*>(&choice);
     auto* philox = dynamic_cast<PhiloxChoiceSource*>(&choice);
@@ -87,6 +88,7 @@ std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
     hc.symmetrize = cfg.symmetrize ? 1 : 0;
     hc.rng = philox ? HGS_RNG_PHILOX : HGS_RNG_XOSHIRO;
     hc.gather = gather ? 1 : 0;
+    hc.flags = seq_walk ? HGS_FLAG_SEQ_WALK : 0;
     check(hgs_sample_run(s, &hc, roots.data(), boff.data(), static_cast<int64_t>(batches.size()),
                          seeds.data(), state_ptr));
     int64_t counts[4];
@@ -153,10 +155,16 @@ std::vector<SampledBatch> bulk_shadow(const CsrMatrix& a, const std::vector<std:
 
 SampledBatch shadow_reference(const CsrMatrix& a, std::span<const Index> roots,
                               const SamplerConfig& cfg, ChoiceSource& choice) {
-    // One batch, root ordinal = position (sampler.cpp:96-98) == bulk with k=1.
+    // One batch, root ordinal = position (sampler.cpp:96-98); the walk uses
+    // the raw rows of A when unsymmetrized (sampler.cpp:104-106).
+    cfg.validate();
     std::vector<std::vector<Index>> one{std::vector<Index>(roots.begin(), roots.end())};
-    SamplerConfig c = cfg;
-    return std::move(bulk_shadow(a, one, c, choice).front());
+    const bool ids = values_are_ids(a);
+    GraphGuard g;
+    g.g = upload_csr(a, 0, !ids);
+    SampleGuard s;
+    check(hgs_sample_create(g.g, nullptr, &s.s));
+    return std::move(run_bulk(g.g, s.s, one, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, true).front());
 }
 
 CsrMatrix make_edge_id_matrix(const EventGraph& event) {

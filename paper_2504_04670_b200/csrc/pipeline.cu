@@ -93,7 +93,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     DevGraph& g = s->graph->g;
     HGS_CUDA(cudaSetDevice(g.device));
     if (cfg.symmetrize) graph_build_walk_sym(g);
-    const DevCsr& walk = cfg.symmetrize ? g.walk_sym : g.a;
+    const bool seq_walk = (cfg.flags & HGS_FLAG_SEQ_WALK) != 0;
+    const DevCsr& walk = cfg.symmetrize ? g.walk_sym : (seq_walk ? g.full_pattern() : g.a);
     graph_ensure_recip(g, walk.max_deg);
     if (cfg.gather && !g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
     const CallPlan c = plan_call(walk, g.a, g.n_rows, cfg.depth, cfg.fanout);
@@ -126,7 +127,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     s->batch_eoff.reserve((size_t)k + 1);
     const size_t vneed = (size_t)std::max<int64_t>(1, R * c.max_t);
     if (s->v_cap < vneed) s->v_cap = vneed;
-    if (s->e_cap < s->v_cap * 2) s->e_cap = s->v_cap * 2;
+    if (s->e_cap == 0) s->e_cap = s->v_cap * 2;
     s->l2g.reserve(s->v_cap);
     s->e_row.reserve(s->e_cap);
     s->e_col.reserve(s->e_cap);
@@ -148,7 +149,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     if (R > 0) {
         ExpandParams ep{};
         ep.w_rp = walk.rp.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
-        ep.neg_row = (!cfg.symmetrize && g.has_neg) ? g.neg_row.p : nullptr;
+        ep.neg_row = (!cfg.symmetrize && !seq_walk && g.has_neg) ? g.neg_row.p : nullptr;
         ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
         ep.R = (int32_t)R; ep.depth = (int32_t)cfg.depth;
         ep.fanout = (int32_t)std::min<int64_t>(cfg.fanout, 1 << 30);

@@ -22,6 +22,7 @@ LIB_PATH = os.path.join(_PKG, "lib", "libhgs.so")
 
 HGS_OK, HGS_EINVAL, HGS_ECUDA, HGS_ERANGE = 0, 1, 2, 3
 RNG_XOSHIRO, RNG_PHILOX = 0, 1
+FLAG_SEQ_WALK = 1
 
 # Exported symbols declared in include/hgs.h (checked by tests/test_abi.py).
 EXPORTS = [
@@ -45,7 +46,7 @@ class HgsRuntimeError(RuntimeError):
 class Config(C.Structure):
     _fields_ = [("depth", C.c_int64), ("fanout", C.c_int64), ("batch_size", C.c_int64),
                 ("bulk_batches", C.c_int64), ("symmetrize", C.c_int32), ("rng", C.c_int32),
-                ("gather", C.c_int32), ("profile", C.c_int32)]
+                ("gather", C.c_int32), ("profile", C.c_int32), ("flags", C.c_int32)]
 
 
 class HostOut(C.Structure):
@@ -215,9 +216,9 @@ class Sampler:
 
     @staticmethod
     def config(depth=3, fanout=6, symmetrize=True, rng=RNG_XOSHIRO, gather=False, profile=False,
-               batch_size=1, bulk_batches=1) -> Config:
+               batch_size=1, bulk_batches=1, seq_walk=False) -> Config:
         return Config(depth, fanout, batch_size, bulk_batches, int(symmetrize), int(rng),
-                      int(gather), int(profile))
+                      int(gather), int(profile), FLAG_SEQ_WALK if seq_walk else 0)
 
     def bulk_shadow(self, roots, batch_off, seeds, *, state=None, **cfg) -> SampleCounts:
         """hitgnn::bulk_shadow (+ gather_features) from host arrays; blocks."""

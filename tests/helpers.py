@@ -72,3 +72,39 @@ def compare(dev: dict, ref, *, gather=False, counts=True):
         if not np.array_equal(np.asarray(dev["draws"]).astype(np.int64), ref.draws):
             bad.append("draws")
     return bad
+
+
+# ---------------------------------------------------------------------------
+# golden fixtures (generated from the reference by tests/golden/make_golden.py)
+
+GOLDEN = os.path.join(ROOT, "tests", "golden")
+OUT_FIELDS = ["batch_voff", "batch_eoff", "comp_off", "l2g", "roots_local", "e_row", "e_col",
+              "e_gid", "e_val", "xv", "ye", "lab"]
+
+
+def load_small_cases():
+    import json
+    with open(os.path.join(GOLDEN, "small_cases.json")) as f:
+        index = json.load(f)
+    z = np.load(os.path.join(GOLDEN, "small_cases.npz"))
+    out = []
+    for ent in index:
+        gp, pre = ent["graph"], ent["prefix"]
+        g = O.Graph(n=ent["n"], rp=z[gp + "rp"], ci=z[gp + "ci"],
+                    values=z[gp + "values"] if ent["has_values"] else None,
+                    node_feat=z[gp + "nf"], edge_feat=z[gp + "ef"], labels=z[gp + "lab"])
+        exp = {f: z[pre + "out_" + f] for f in OUT_FIELDS if pre + "out_" + f in z}
+        out.append(dict(ent, g=g, roots=z[pre + "roots"], boff=z[pre + "boff"], seeds=z[pre + "seeds"],
+                        expected=exp))
+    return out
+
+
+def load_json(name):
+    import json
+    with open(os.path.join(GOLDEN, name)) as f:
+        return json.load(f)
+
+
+def sha(a) -> str:
+    import hashlib
+    return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()

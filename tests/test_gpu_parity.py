@@ -1,0 +1,305 @@
+"""GPU parity: the CUDA path through the C ABI (libhgs.so) against the
+reference's golden results and the oracle, bit for bit.
+
+Covers K0 (walk build), both RNG modes, symmetrized / directed walks,
+depths 1-4, fanouts on both choose paths (k <= 8 registers, k > 8 local),
+explicit-zero and negative values, self-loops, isolated roots, empty batches,
+zero-root calls, gather on/off, resumed (non-fresh) streams, the
+capacity-regrow path, error messages, the device-pointer entry point, the
+C1 configuration (digests of the reference's own outputs) and the full C2
+workload against the oracle plus size-independent properties.
+"""
+import os
+
+import numpy as np
+import pytest
+
+from tests.helpers import O, OUT_FIELDS, load_json, load_small_cases, random_graph, sha
+
+pytestmark = pytest.mark.gpu
+
+CMP = ["batch_voff", "batch_eoff", "comp_off", "l2g", "roots_local", "e_row", "e_col", "e_gid"]
+
+
+def hgs():
+    from paper_2504_04670_b200 import hgs as H
+    return H
+
+
+def device_run(g, roots, boff, seeds, *, gather=False, state=None, sampler=None, **kw):
+    H = hgs()
+    if sampler is None:
+        G = H.Graph(g.rp, g.ci, g.values, n_cols=g.n_cols)
+        if gather:
+            G.attach_features(g.node_feat, g.edge_feat, g.labels)
+        sampler = H.Sampler(G)
+    sampler.bulk_shadow(roots, boff, seeds, gather=gather, state=state, **kw)
+    return sampler.to_host(), sampler
+
+
+def assert_same(dev, ref, gather, counts=True, gid=True):
+    for f in CMP:
+        if f == "e_gid" and not gid:
+            continue
+        a = np.asarray(dev[f]).astype(np.int64)
+        b = getattr(ref, f).astype(np.int64)
+        assert a.shape == b.shape and np.array_equal(a, b), f
+    if gather:
+        for f in ("xv", "ye", "lab"):
+            a, b = np.asarray(dev[f]), getattr(ref, f)
+            assert a.shape == b.shape and np.array_equal(a.view(np.uint8), b.view(np.uint8)), f
+    if counts and ref.draws is not None:
+        assert np.array_equal(dev["draws"].astype(np.int64), ref.draws)
+        assert np.array_equal(dev["decisions"].astype(np.int64), ref.decisions)
+
+
+# --------------------------------------------------------------------- K0 ----
+
+@pytest.mark.parametrize("n,m,seed", [(1, 0, 0), (7, 20, 1), (500, 3000, 2), (20000, 250000, 3)])
+def test_walk_build_matches_symmetrize_pattern(n, m, seed):
+    g = random_graph(n, m, seed, self_loops=seed % 2 == 1)
+    G = hgs().Graph(g.rp, g.ci)
+    rp, ci = G.walk(True)
+    orp, oci = O.symmetrize(g)
+    assert np.array_equal(rp, orp) and np.array_equal(ci, oci)
+
+
+def test_walk_build_hub_rows():
+    # a hub with 6000 in- and out-neighbours: radix transpose + row merge
+    n = 8000
+    src = np.concatenate([np.zeros(6000, np.int64), np.arange(1, 6001)])
+    dst = np.concatenate([np.arange(1, 6001), np.zeros(6000, np.int64) + 7])
+    key = np.unique(src * n + dst)
+    u, v = key // n, key % n
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, u + 1, 1)
+    g = O.Graph(n=n, rp=np.cumsum(rp), ci=v)
+    rp2, ci2 = hgs().Graph(g.rp, g.ci).walk(True)
+    orp, oci = O.symmetrize(g)
+    assert np.array_equal(rp2, orp) and np.array_equal(ci2, oci)
+
+
+# ----------------------------------------------------------------- golden ----
+
+@pytest.mark.parametrize("case", load_small_cases(), ids=lambda c: c["name"])
+def test_golden_cases(case):
+    H = hgs()
+    g = case["g"]
+    kw = dict(rng=case["rng"], depth=case["depth"], fanout=case["fanout"], symmetrize=case["sym"])
+    if case["error"]:
+        with pytest.raises(H.SamplerError):
+            device_run(g, case["roots"], case["boff"], case["seeds"], gather=case["gather"], **kw)
+        return
+    dev, _ = device_run(g, case["roots"], case["boff"], case["seeds"], gather=case["gather"], **kw)
+    exp = case["expected"]
+    for f in CMP:
+        if f == "e_gid" and np.all(exp[f] == -1) and exp[f].size:
+            continue
+        assert np.array_equal(np.asarray(dev[f]).astype(np.int64), exp[f]), f
+    if case["gather"]:
+        for f in ("xv", "ye", "lab"):
+            assert np.array_equal(np.asarray(dev[f]).view(np.uint8), exp[f].view(np.uint8)), f
+
+
+# ------------------------------------------------------------ random sweep ----
+
+SWEEP = [  # (n, m, depth, fanout, values)
+    (30, 80, 1, 1, None), (200, 1200, 2, 3, None), (1000, 8000, 3, 6, None),
+    (1000, 8000, 4, 2, "zeros"), (3000, 30000, 3, 8, None), (500, 20000, 2, 9, None),
+    (300, 9000, 2, 17, "zeros"), (5000, 60000, 3, 6, "zeros"),
+]
+
+
+@pytest.mark.parametrize("n,m,depth,fanout,values", SWEEP)
+@pytest.mark.parametrize("rng", [0, 1])
+def test_random_graphs(n, m, depth, fanout, values, rng):
+    rs = np.random.default_rng(n + depth * 7 + fanout + rng)
+    g = random_graph(n, m, n + fanout, self_loops=(n % 3 == 0))
+    if values == "zeros":
+        g.values = rs.uniform(0.5, 2.0, g.m)
+        g.values[rs.random(g.m) < 0.2] = 0.0
+    k = 5
+    b = min(n // k, 64)
+    sizes = [b, 0, b // 2, b, 1]  # includes an empty batch and a single-root batch
+    roots = np.concatenate([rs.permutation(n)[:s] for s in sizes]).astype(np.int64)
+    boff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    seeds = rs.integers(0, 2**63, len(roots), dtype=np.uint64)
+    gather = values is None
+    for sym in (True, False):
+        kw = dict(rng=rng, depth=depth, fanout=fanout, symmetrize=sym)
+        dev, _ = device_run(g, roots, boff, seeds, gather=gather, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=gather, **kw)
+        assert_same(dev, ref, gather)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_resumed_streams(rng):
+    """Non-fresh sources (rng_state): xoshiro states / Philox decision bases."""
+    rs = np.random.default_rng(77)
+    g = random_graph(800, 6000, 4)
+    roots = rs.permutation(800)[:100].astype(np.int64)
+    boff = np.array([0, 60, 100], np.int64)
+    seeds = rs.integers(0, 2**63, 100, dtype=np.uint64)
+    state = (rs.integers(0, 2**63, 400, dtype=np.uint64) if rng == 0
+             else rs.integers(0, 1000, 100).astype(np.uint64))
+    dev, _ = device_run(g, roots, boff, seeds, state=state, rng=rng, depth=3, fanout=5)
+    ref = O.bulk_shadow(g, roots, boff, seeds, state=state, rng=rng, depth=3, fanout=5)
+    assert_same(dev, ref, False)
+
+
+def test_shadow_reference_walk_semantics():
+    """HGS_FLAG_SEQ_WALK: raw-row walk of shadow_reference (zeros kept)."""
+    rs = np.random.default_rng(5)
+    g = random_graph(400, 3000, 8)
+    g.values = rs.uniform(0.5, 2.0, g.m)
+    g.values[rs.random(g.m) < 0.3] = 0.0
+    g.values[rs.random(g.m) < 0.05] = -1.0
+    roots = rs.permutation(400)[:50].astype(np.int64)
+    boff = np.array([0, 50], np.int64)
+    seeds = rs.integers(0, 2**63, 50, dtype=np.uint64)
+    dev, _ = device_run(g, roots, boff, seeds, depth=2, fanout=4, symmetrize=False, seq_walk=True)
+    ref = O.bulk_shadow(g, roots, boff, seeds, depth=2, fanout=4, symmetrize=False, seq_walk=True)
+    assert_same(dev, ref, False)
+    # bulk semantics on the same graph rejects the negative rows it visits
+    with pytest.raises(hgs().SamplerError, match="negative"):
+        device_run(g, roots, boff, seeds, depth=2, fanout=4, symmetrize=False)
+    with pytest.raises(O.SamplerError, match="negative"):
+        O.bulk_shadow(g, roots, boff, seeds, depth=2, fanout=4, symmetrize=False)
+
+
+def test_capacity_regrow(monkeypatch):
+    """Start with 4-edge slots and a 100-edge output: the device reports the
+    overflow and the call is re-run with exact sizes."""
+    monkeypatch.setenv("HGS_E_STRIDE", "4")
+    monkeypatch.setenv("HGS_E_CAP", "100")
+    g = random_graph(2000, 20000, 9)
+    rs = np.random.default_rng(1)
+    roots = rs.permutation(2000)[:300].astype(np.int64)
+    boff = np.array([0, 150, 300], np.int64)
+    seeds = rs.integers(0, 2**63, 300, dtype=np.uint64)
+    dev, S = device_run(g, roots, boff, seeds, depth=3, fanout=6, gather=True)
+    ref = O.bulk_shadow(g, roots, boff, seeds, depth=3, fanout=6, gather=True)
+    assert_same(dev, ref, True)
+    # the regrown workspace is reused without another retry
+    dev2, _ = device_run(g, roots, boff, seeds, depth=3, fanout=6, gather=True, sampler=S)
+    assert_same(dev2, ref, True)
+
+
+def test_error_paths():
+    H = hgs()
+    g = random_graph(50, 200, 3)
+    seeds = np.zeros(4, np.uint64)
+    with pytest.raises(H.SamplerError, match="^sampler: duplicate root 3$"):
+        device_run(g, [1, 3, 3], [0, 3], seeds[:3])
+    with pytest.raises(H.SamplerError, match="^sampler: root 50 out of range$"):
+        device_run(g, [1, 50], [0, 2], seeds[:2])
+    with pytest.raises(H.SamplerError, match="depth must be >= 1"):
+        device_run(g, [1], [0, 1], seeds[:1], depth=0)
+    with pytest.raises(H.SamplerError, match="fanout must be >= 1"):
+        device_run(g, [1], [0, 1], seeds[:1], fanout=0)
+    rect = O.Graph(n=50, rp=g.rp, ci=g.ci, n_cols=60)
+    with pytest.raises(H.SamplerError, match="symmetrize_pattern: matrix must be square"):
+        device_run(rect, [1], [0, 1], seeds[:1])
+    with pytest.raises(H.SamplerError, match=r"spgemm: inner dimensions disagree \(60 vs 50\)"):
+        device_run(rect, [1], [0, 1], seeds[:1], symmetrize=False)
+    # duplicates across batches are allowed (check_roots is per batch)
+    device_run(g, [3, 3], [0, 1, 2], seeds[:2])
+
+
+def test_device_pointer_entry_point():
+    import torch
+    H = hgs()
+    g = random_graph(3000, 25000, 12)
+    rs = np.random.default_rng(2)
+    roots = np.concatenate([rs.permutation(3000)[:200] for _ in range(4)]).astype(np.int64)
+    boff = np.arange(5, dtype=np.int64) * 200
+    seeds = rs.integers(0, 2**63, 800, dtype=np.uint64)
+    G = H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels)
+    st = torch.cuda.Stream()
+    S = H.Sampler(G, stream=st.cuda_stream)
+    dr = torch.from_numpy(roots.astype(np.int32)).cuda()
+    db = torch.from_numpy(boff).cuda()
+    ds = torch.from_numpy(seeds.view(np.int64)).cuda()
+    torch.cuda.synchronize()
+    S.run_device(dr.data_ptr(), db.data_ptr(), 800, 4, ds.data_ptr(), depth=3, fanout=6, gather=True,
+                 profile=True)
+    S.wait()
+    dev = S.to_host()
+    ref = O.bulk_shadow(g, roots, boff, seeds, depth=3, fanout=6, gather=True)
+    assert_same(dev, ref, True)
+    assert S.launches() >= 5
+    assert (S.kernel_times() >= 0).all()
+    st_ = S.stats()
+    assert st_["V"] == ref.V and st_["E"] == ref.E
+
+
+def test_multi_handle_sharding_matches_single_call():
+    """Two sample handles on one graph (as two ranks would be): the shard union
+    equals the single call, batch for batch."""
+    from paper_2504_04670_b200.sharding import shard
+    H = hgs()
+    g = random_graph(4000, 40000, 21)
+    rs = np.random.default_rng(8)
+    k, b = 6, 100
+    roots = np.concatenate([rs.permutation(4000)[:b] for _ in range(k)]).astype(np.int64)
+    boff = np.arange(k + 1, dtype=np.int64) * b
+    seeds = rs.integers(0, 2**63, k * b, dtype=np.uint64)
+    G = H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels)
+    full, _ = device_run(g, roots, boff, seeds, gather=True, sampler=H.Sampler(G), depth=3, fanout=6)
+    parts = []
+    for rank in range(2):
+        r, bo, s = shard(roots, boff, seeds, rank, 2)
+        out, _ = device_run(g, r, bo, s, gather=True, sampler=H.Sampler(G), depth=3, fanout=6)
+        parts.append(out)
+    for f in ("l2g", "e_row", "e_col", "e_gid", "xv", "ye", "lab"):
+        assert np.array_equal(np.concatenate([p[f] for p in parts]), full[f]), f
+
+
+# ------------------------------------------------------------------ C1 / C2 ----
+
+def test_c1_matches_reference_digests():
+    from paper_2504_04670_b200 import workload as W
+    c1 = load_json("c1.json")
+    ev = W.preset_event("C1")
+    roots, boff, seeds = W.bench_roots(ev.n, 256, 16, seed=1, rep=0)
+    H = hgs()
+    S = H.Sampler(H.Graph(ev.rp, ev.ci).attach_features(ev.node_feat, ev.edge_feat, ev.labels))
+    for run in c1["runs"]:
+        S.bulk_shadow(roots, boff, seeds, rng=run["rng"], depth=run["depth"], fanout=6, gather=True)
+        dev = S.to_host()
+        assert (S.counts.V, S.counts.E) == (run["V"], run["E"])
+        for f in ("batch_voff", "batch_eoff", "comp_off", "l2g", "roots_local", "e_row", "e_col",
+                  "e_gid"):
+            assert sha(np.asarray(dev[f]).astype(np.int64)) == run["digests"][f], f
+        for f in ("xv", "ye", "lab"):
+            assert sha(dev[f]) == run["digests"][f], f
+
+
+def test_c2_full_workload():
+    """BASELINE configs[1] at full size: 64 x 1024 roots, d=3, s=6, gather.
+    Bit-exact against the oracle, plus size-independent properties."""
+    from paper_2504_04670_b200 import workload as W
+    ev = W.preset_event("C2")
+    roots, boff, seeds = W.bench_roots(ev.n, 1024, 64, seed=1, rep=0)
+    H = hgs()
+    S = H.Sampler(H.Graph(ev.rp, ev.ci).attach_features(ev.node_feat, ev.edge_feat, ev.labels))
+    S.bulk_shadow(roots, boff, seeds, depth=3, fanout=6, gather=True)
+    dev = S.to_host()
+    # properties: every component sorted, contains its root, edges in-component
+    bv, co, l2g = dev["batch_voff"], dev["comp_off"], dev["l2g"]
+    assert bv[-1] == S.counts.V and dev["batch_eoff"][-1] == S.counts.E
+    for bi in (0, 31, 63):
+        offs = co[boff[bi] + bi: boff[bi + 1] + bi + 1]
+        base = bv[bi]
+        for c in range(0, 1024, 97):
+            seg = l2g[base + offs[c]: base + offs[c + 1]]
+            assert np.all(np.diff(seg) > 0)
+            assert seg[dev["roots_local"][boff[bi] + c] - offs[c]] == roots[boff[bi] + c]
+    rows = dev["e_row"].astype(np.int64)
+    assert np.all(ev.ci[dev["e_gid"]] >= 0)
+    g = O.Graph(n=ev.n, rp=ev.rp, ci=ev.ci, node_feat=ev.node_feat, edge_feat=ev.edge_feat,
+                labels=ev.labels)
+    ref = O.bulk_shadow(g, roots, boff, seeds, depth=3, fanout=6, gather=True)
+    assert (S.counts.V, S.counts.E) == (ref.V, ref.E) == (14330269, 17161199)
+    assert_same(dev, ref, True)
+    del rows
