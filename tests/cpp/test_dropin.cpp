@@ -212,7 +212,7 @@ int main() {
               "symmetrize_pattern: matrix must be square");
         SampledBatch plain;
         plain.local_to_global = {0, 1};
-        plain.adjacency = CooMatrix{2, 2, {{0, 1, 0.5}}};
+        plain.adjacency = CooMatrix{2, 2, {{0, 1, 0.25}}};  // llround(0.25) - 1 = -1
         CHECK(expect_throw<std::invalid_argument>([&] { gather_features(plain, event); }).find(
                   "do not carry edge ids") != std::string::npos);
         std::printf("errors: %s\n", failures ? "see above" : "ok");
