@@ -293,7 +293,8 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
         __syncwarp();
 
         // ---- induced subgraph: scan the flattened rows in 32-entry windows
-        int2* ed = p.escratch + (size_t)r * p.e_stride;
+        int2* const ed = p.escratch + (size_t)r * p.e_stride;
+        const unsigned es = (unsigned)p.e_stride;
         int count = 0;
         // Row owning lane's entry of window w, given the row c holding the
         // window's first entry: c + #row starts in (base, base + lane].
@@ -305,14 +306,11 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
         // Emit the hits of one window in scan order. The capacity check is
         // hoisted: `room` says every lane's slot fits (count + 32 <= stride).
         auto emit = [&](int j, int own, int kk) {
-            const bool hit = j >= 0;
-            const unsigned hb = __ballot_sync(kFull, hit);
-            if (hit) {
-                const int t = count + __popc(hb & lt);
-                if (t < p.e_stride) {
-                    const int32_t gid = HAS_GID ? __ldg(p.a_gid + kk) : kk;
-                    ed[t] = make_int2((rinfo[own].y << 16) | j, gid);
-                }
+            const unsigned hb = __ballot_sync(kFull, j >= 0);
+            const unsigned t = (unsigned)count + __popc(hb & lt);
+            if (j >= 0 && t < es) {
+                const int32_t gid = HAS_GID ? __ldg(p.a_gid + kk) : kk;
+                ed[t] = make_int2((rinfo[own].y << 16) | j, gid);
             }
             count += __popc(hb);
         };
@@ -340,11 +338,39 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
                 if (!guard || w + u < nwin) emit((!guard || kk[u] >= 0) ? hs.find_rank(v[u]) : -1, own[u], kk[u]);
             }
         };
+        // Full groups are software-pipelined: the column loads of group g+1
+        // are in flight while group g is probed and emitted.
+        auto fetch = [&](int w, int (&own)[G], int (&kk)[G], uint32_t (&v)[G]) {
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                own[u] = (int)wcur[w + u] + __popc(wmask[w + u] & le);
+                kk[u] = ((w + u) << 5) + lane + rinfo[own[u]].x;
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
+        };
+        auto consume = [&](const int (&own)[G], const int (&kk)[G], const uint32_t (&v)[G]) {
+#pragma unroll
+            for (int u = 0; u < G; ++u) emit(hs.find_rank(v[u]), own[u], kk[u]);
+        };
         int w = 0;
         if (direct) {
-            const int nfull = S >> 5;  // windows with all 32 entries valid
-            for (; w + G <= nfull; w += G) group(w, false);
-            if (w < nwin) group(w, true);
+            const int nfg = (S >> 5) / G;  // groups whose windows are all full
+            if (nfg > 0) {
+                int ownA[G], kkA[G], ownB[G], kkB[G];
+                uint32_t vA[G], vB[G];
+                fetch(0, ownA, kkA, vA);
+                for (int gi = 0; gi < nfg; gi += 2) {
+                    if (gi + 1 < nfg) fetch((gi + 1) * G, ownB, kkB, vB);
+                    consume(ownA, kkA, vA);
+                    if (gi + 1 < nfg) {
+                        if (gi + 2 < nfg) fetch((gi + 2) * G, ownA, kkA, vA);
+                        consume(ownB, kkB, vB);
+                    }
+                }
+                w = nfg * G;
+            }
+            for (; w < nwin; w += G) group(w, true);
         } else {
             int cursor = 0;  // huge sets: serial window cursor
             for (; w < nwin; ++w) {

@@ -126,39 +126,62 @@ __device__ __forceinline__ T warp_sum(T v) {
 }
 
 // Bitonic sort of 32*E keys held lane-major (lane l owns keys l*E .. l*E+E-1),
-// ascending. Intra-lane stages are register compare-exchanges; inter-lane
-// stages exchange through shuffles.
+// ascending. Merges of width <= E are unrolled register compare-exchanges;
+// wider merges run as (non-unrolled) loops over shuffle stages followed by
+// the E-wide in-register tail, keeping the code small enough to stay in the
+// instruction cache next to the extraction loop.
+template <int E>
+__device__ __forceinline__ void bitonic_lane_tail(uint32_t (&k)[E], bool up) {
+#pragma unroll
+    for (int stride = E >> 1; stride > 0; stride >>= 1) {
+#pragma unroll
+        for (int e = 0; e < E; ++e) {
+            if ((e & stride) == 0) {
+                const int e2 = e | stride;
+                const uint32_t x = k[e], y = k[e2];
+                const bool sw = up ? (x > y) : (x < y);
+                k[e] = sw ? y : x;
+                k[e2] = sw ? x : y;
+            }
+        }
+    }
+}
+
 template <int E>
 __device__ __forceinline__ void warp_bitonic_sort(uint32_t (&k)[E]) {
     const int lane = lane_id();
+    // merges of width 2..E: entirely inside a lane
 #pragma unroll
-    for (int size = 2; size <= 32 * E; size <<= 1) {
+    for (int size = 2; size <= E; size <<= 1) {
 #pragma unroll
         for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            if (stride >= E) {
-                const int lm = stride / E;
-                const bool lower = (lane & lm) == 0;
 #pragma unroll
-                for (int e = 0; e < E; ++e) {
+            for (int e = 0; e < E; ++e) {
+                if ((e & stride) == 0) {
+                    const int e2 = e | stride;
                     const bool up = (((lane * E + e) & size) == 0);
-                    const uint32_t other = __shfl_xor_sync(kFull, k[e], lm);
-                    const bool keep_min = (lower == up);
-                    k[e] = keep_min ? min(k[e], other) : max(k[e], other);
-                }
-            } else {
-#pragma unroll
-                for (int e = 0; e < E; ++e) {
-                    if ((e & stride) == 0) {
-                        const int e2 = e | stride;
-                        const bool up = (((lane * E + e) & size) == 0);
-                        const uint32_t x = k[e], y = k[e2];
-                        const bool sw = up ? (x > y) : (x < y);
-                        k[e] = sw ? y : x;
-                        k[e2] = sw ? x : y;
-                    }
+                    const uint32_t x = k[e], y = k[e2];
+                    const bool sw = up ? (x > y) : (x < y);
+                    k[e] = sw ? y : x;
+                    k[e2] = sw ? x : y;
                 }
             }
         }
+    }
+    // merges of width 2E..32E: shuffle stages, then the in-lane tail
+#pragma unroll 1
+    for (int size = 2 * E; size <= 32 * E; size <<= 1) {
+        const bool up = ((lane * E) & size) == 0;
+#pragma unroll 1
+        for (int lm = size / (2 * E); lm > 0; lm >>= 1) {
+            const bool keep_min = ((lane & lm) == 0) == up;
+#pragma unroll
+            for (int e = 0; e < E; ++e) {
+                const uint32_t other = __shfl_xor_sync(kFull, k[e], lm);
+                k[e] = keep_min ? min(k[e], other) : max(k[e], other);
+            }
+        }
+        bitonic_lane_tail<E>(k, up);
     }
 }
 #endif
