@@ -239,13 +239,21 @@ def run_gpu(args, world, rank, local_rank):
             with torch.cuda.stream(stream):
                 flush.zero_()
             ev0[j].record(stream)
-            step_device(i, True)
+            step_device(i, False)
             ev1[j].record(stream)
             S.wait()
             step_ms.append(ev0[j].elapsed_time(ev1[j]))
-            kern.append(S.kernel_times())
             launches += S.launches()
             stats.append(S.stats())
+        torch.cuda.synchronize()
+        # per-stage kernel times: the same steps again as profiled calls
+        # (one serial chunk, CUDA events between the stages on the stream)
+        for j in range(min(args.steps, 5)):
+            with torch.cuda.stream(stream):
+                flush.zero_()
+            step_device(args.warmup + j, True)
+            S.wait()
+            kern.append(S.kernel_times())
         torch.cuda.synchronize()
         if world > 1:
             dist.barrier()

@@ -138,6 +138,7 @@ int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* 
             }
             rp[u + 1] = (int32_t)ci.size();
         }
+        std::vector<int2> ari;  // (row start, out-degree) per vertex of A
         auto* h = new hgs_graph;
         DevGraph& g = h->g;
         try {
@@ -148,6 +149,10 @@ int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* 
             g.n_cols = n_cols;
             g.nnz = nnz;
             upload_csr(g.a, n, rp, ci, g.stream);
+            ari.resize((size_t)std::max<int32_t>(n, 1));
+            for (int32_t u = 0; u < n; ++u) ari[u] = make_int2(rp[u], rp[u + 1] - rp[u]);
+            g.a_ri.reserve(ari.size());
+            upload(g.a_ri.p, ari.data(), ari.size() * sizeof(int2), g.stream);
             if (zeros) {
                 g.has_gid = true;
                 g.a_gid.reserve(gid.size());
@@ -293,6 +298,8 @@ int hgs_sample_destroy(hgs_sample* s) {
         cudaSetDevice(s->graph->g.device);
         if (s->pending) cudaStreamSynchronize(s->stream);
         for (auto& e : s->ev) if (e) cudaEventDestroy(e);
+        for (auto& e : s->chunk_ev) cudaEventDestroy(e);
+        if (s->aux) cudaStreamDestroy(s->aux);
         if (s->h_state) cudaFreeHost(s->h_state);
         cudaStream_t st = s->own_stream ? s->stream : nullptr;
         delete s;

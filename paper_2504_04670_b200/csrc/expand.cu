@@ -141,7 +141,7 @@ __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
 template <int KCAP, bool PHILOX, bool LOCAL>
 __global__ void __launch_bounds__(128) k_expand(ExpandParams p) {
     extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree), then the recip table
-    const int r = blockIdx.x * blockDim.x + threadIdx.x;
+    const int r = p.r0 + blockIdx.x * blockDim.x + threadIdx.x;
     // bounded() reciprocals in shared memory when the table is small
     uint64_t* srecip = reinterpret_cast<uint64_t*>(cache + (size_t)p.cache_entries * blockDim.x);
     const uint64_t* recip = p.recip;
@@ -243,7 +243,7 @@ static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cu
     auto kern = k_expand<KCAP, PH, LOCAL>;
     if (smem > 48 * 1024)
         HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const unsigned grid = (unsigned)((ep.R + threads - 1) / threads);
+    const unsigned grid = (unsigned)((ep.R - ep.r0 + threads - 1) / threads);
     kern<<<grid, threads, smem, st>>>(ep);
     HGS_CUDA(cudaGetLastError());
 }

@@ -20,6 +20,8 @@
 //   sampler.cpp:211-243) with 16-byte vector stores.
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "kernels.cuh"
 
 namespace hgs {
@@ -145,49 +147,18 @@ struct HashSet<false> {
     }
 };
 
-template <int E>
-__device__ __forceinline__ void sort_regs(int32_t* set, int U) {
-    const int lane = lane_id();
-    uint32_t kk[E];
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int i = lane * E + e;
-        kk[e] = i < U ? (uint32_t)set[i] : 0xffffffffu;
-    }
-    warp_bitonic_sort<E>(kk);
-    __syncwarp();
-#pragma unroll
-    for (int e = 0; e < E; ++e) {
-        const int i = lane * E + e;
-        if (i < U) set[i] = (int32_t)kk[e];
-    }
-    __syncwarp();
-}
-
-__device__ void sort_smem(int32_t* set, int U, int N) {
-    const int lane = lane_id();
-    for (int i = U + lane; i < N; i += 32) set[i] = 0x7fffffff;
-    __syncwarp();
-    for (int size = 2; size <= N; size <<= 1) {
-        for (int stride = size >> 1; stride > 0; stride >>= 1) {
-            for (int t = lane; t < N / 2; t += 32) {
-                const int i = 2 * t - (t & (stride - 1));
-                const int j = i + stride;
-                const bool up = (i & size) == 0;
-                const int32_t a = set[i], b = set[j];
-                if ((a > b) == up) { set[i] = b; set[j] = a; }
-            }
-            __syncwarp();
-        }
-    }
-}
-
 }  // namespace
 
 // ===========================================================================
 // K2
 // ===========================================================================
 
+// Per-warp shared memory of K2 (set_cap == row_cap == max tree size rounded
+// up to 32; the regions are reused phase by phase):
+//   hash   4<<nb_bits slots                   vertex -> rank
+//   keys   set_cap x i32   unsorted keys -> sorted keys -> window masks/cursors
+//   tmp    row_cap+36 x i32  bucketed keys -> row starts (+ sentinels)
+//   aux    row_cap x int2  bucket counters -> per nonempty row (A pos - flat pos, rank<<16)
 template <bool PACKED, bool HAS_GID>
 __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
@@ -198,81 +169,126 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     HashSet<PACKED> hs;
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
     q += HashSet<PACKED>::kBytesPerSlot * nslots;
-    int32_t* set = (int32_t*)q; q += 4 * p.set_cap;
-    // after the set is dead its space holds, per 32-entry window, the row of
-    // the window's first entry (wcur) and a bitmask of rows starting inside it
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(set);
-    uint16_t* wcur = reinterpret_cast<uint16_t*>(set + p.win_cap);
-    int32_t* rstart = (int32_t*)q; q += 4 * (p.row_cap + 36);
-    int2* rinfo = (int2*)q;  // per nonempty row: (A position - flat index, local id)
+    int32_t* keys = (int32_t*)q; q += 4 * p.set_cap;
+    uint32_t* wmask = reinterpret_cast<uint32_t*>(keys);
+    uint16_t* wcur = reinterpret_cast<uint16_t*>(keys + p.win_cap);
+    int32_t* tmp = (int32_t*)q; q += 4 * (p.row_cap + 36);
+    int32_t* rstart = tmp;
+    int32_t* cnt = (int32_t*)q;
+    int2* rinfo = (int2*)q;
     hs.bits = p.nb_bits;
     hs.bmask = (1u << p.nb_bits) - 1u;
     hs.rb = p.rank_bits;
     hs.rmask = (1u << p.rank_bits) - 1u;
     const unsigned lt = (1u << lane) - 1u;
     const unsigned le = (2u << lane) - 1u;
+    constexpr int CH = 4;  // 32-key chunks of row loads in flight
 
     const int nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int r = blockIdx.x * (blockDim.x >> 5) + warp; r < p.R; r += nwarps) {
+    for (int r = p.r0 + blockIdx.x * (blockDim.x >> 5) + warp; r < p.R; r += nwarps) {
         int32_t* tl = p.touched + (size_t)r * p.stride;
         const int T = p.tcount[r];
-        const int32_t root = tl[0];  // before the slot is overwritten by the set
 
-        // ---- dedup: hash-insert the touched list, compact the new keys
+        // ---- dedup: hash-insert the touched list (next chunk's load in
+        // flight), compact the fresh keys, track the id range
         hs.clear(nslots);
         __syncwarp();
         int U = 0;
+        uint32_t lo = 0xffffffffu, hi = 0u;
+        int32_t nxt = lane < T ? tl[lane] : 0;
+        const int32_t root = __shfl_sync(kFull, nxt, 0);
+#pragma unroll 1
         for (int b0 = 0; b0 < T; b0 += 32) {
-            const int idx = b0 + lane;
-            bool fresh = false;
-            int32_t v = 0;
-            if (idx < T) {
-                v = tl[idx];
-                fresh = hs.insert((uint32_t)v);
-            }
+            const int32_t v = nxt;
+            const bool valid = b0 + lane < T;
+            nxt = b0 + 32 + lane < T ? tl[b0 + 32 + lane] : 0;
+            const bool fresh = valid && hs.insert((uint32_t)v);
             const unsigned fb = __ballot_sync(kFull, fresh);
-            if (fresh) set[U + __popc(fb & lt)] = v;
+            if (fresh) {
+                keys[U + __popc(fb & lt)] = v;
+                lo = min(lo, (uint32_t)v);
+                hi = max(hi, (uint32_t)v);
+            }
             U += __popc(fb);
         }
+        lo = __reduce_min_sync(kFull, lo);
+        hi = __reduce_max_sync(kFull, hi);
+        // ---- order-preserving buckets b = (v - lo) >> shift, ~2U of them
+        const int lg = min(p.cnt_lg, max(5, 32 - __clz(max(2 * U - 1, 1))));
+        const int shift = max(0, (32 - __clz(hi - lo)) - lg);
+        const int lp = lg - 5;  // counters per lane = 1 << lp
+        const uint32_t pm = (1u << lp) - 1u;
+        // counter of bucket b lives at ((b & pm) << 5) | (b >> lp): lane l's
+        // consecutive buckets are one bank apart (conflict-free scan)
+        auto cidx = [&](uint32_t b) -> int { return (int)(((b & pm) << 5) | (b >> lp)); };
+        for (int i = lane; i < (32 << lp); i += 32) cnt[i] = 0;
         __syncwarp();
-        if (U <= 32) sort_regs<1>(set, U);
-        else if (U <= 64) sort_regs<2>(set, U);
-        else if (U <= 128) sort_regs<4>(set, U);
-        else if (U <= 256) sort_regs<8>(set, U);
-        else {  // large sets: bitonic in the (not yet used) row arrays
-            int N = 512;
-            while (N < U) N <<= 1;
-            int32_t* scr = rstart;
-            for (int i = lane; i < U; i += 32) scr[i] = set[i];
-            __syncwarp();
-            sort_smem(scr, U, N);
-            for (int i = lane; i < U; i += 32) set[i] = scr[i];
-            __syncwarp();
-        }
+        for (int i = lane; i < U; i += 32) atomicAdd(&cnt[cidx(((uint32_t)keys[i] - lo) >> shift)], 1);
+        __syncwarp();
 
-        // ---- ranks, the sorted set back to global, nonempty A rows
+        // ---- exclusive scan of the bucket counts (lane l owns buckets l<<lp ..)
+        {
+            int s = 0;
+            for (int e = 0; e <= (int)pm; ++e) s += cnt[(e << 5) | lane];
+            const int incl = warp_incl_scan(s);
+            int run = incl - s;
+            for (int e = 0; e <= (int)pm; ++e) {
+                const int c = cnt[(e << 5) | lane];
+                cnt[(e << 5) | lane] = run;
+                run += c;
+            }
+        }
+        __syncwarp();
+        // ---- place keys into their buckets (counter becomes the bucket end)
+        for (int i = lane; i < U; i += 32) {
+            const uint32_t v = (uint32_t)keys[i];
+            tmp[atomicAdd(&cnt[cidx((v - lo) >> shift)], 1)] = (int32_t)v;
+        }
+        __syncwarp();
+        // ---- rank = bucket start + smaller keys of the same bucket
+        for (int i = lane; i < U; i += 32) {
+            const uint32_t v = (uint32_t)tmp[i];
+            const uint32_t b = (v - lo) >> shift;
+            const int e = cnt[cidx(b)];
+            const int s = b ? cnt[cidx(b - 1)] : 0;
+            int rank = s;
+            for (int j = s; j < e; ++j) rank += (uint32_t)tmp[j] < v;
+            keys[rank] = (int32_t)v;
+            hs.set_rank(v, (uint32_t)rank);
+        }
+        __syncwarp();
+
+        // ---- sorted set back to global; nonempty A rows in local order
         int NR = 0, S = 0;
-        for (int b0 = 0; b0 < U; b0 += 32) {
-            const int i = b0 + lane;
-            int32_t rb = 0, deg = 0;
-            if (i < U) {
-                const int32_t u = set[i];
-                hs.set_rank((uint32_t)u, (uint32_t)i);
-                tl[i] = u;
-                rb = __ldg(p.a_rp + u);
-                deg = __ldg(p.a_rp + u + 1) - rb;
+        for (int b0 = 0; b0 < U; b0 += CH * 32) {
+            int2 ri[CH];
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                const int i = b0 + c * 32 + lane;
+                ri[c] = make_int2(0, 0);
+                if (i < U) {
+                    const int32_t u = keys[i];
+                    tl[i] = u;
+                    ri[c] = __ldg(p.a_ri + u);
+                }
             }
-            const bool ne = deg > 0;
-            const unsigned nb = __ballot_sync(kFull, ne);
-            const int incl = warp_incl_scan(deg);
-            if (ne) {
-                const int qi = NR + __popc(nb & lt);
-                const int st = S + incl - deg;
-                rstart[qi] = st;
-                rinfo[qi] = make_int2(rb - st, i);
+#pragma unroll
+            for (int c = 0; c < CH; ++c) {
+                if (b0 + c * 32 >= U) break;
+                const int i = b0 + c * 32 + lane;
+                const int deg = ri[c].y;
+                const bool ne = deg > 0;
+                const unsigned nb = __ballot_sync(kFull, ne);
+                const int incl = warp_incl_scan(deg);
+                if (ne) {
+                    const int qi = NR + __popc(nb & lt);
+                    const int st = S + incl - deg;
+                    rstart[qi] = st;
+                    rinfo[qi] = make_int2(ri[c].x - st, i << 16);
+                }
+                NR += __popc(nb);
+                S += __shfl_sync(kFull, incl, 31);
             }
-            NR += __popc(nb);
-            S += __shfl_sync(kFull, incl, 31);
         }
         if (lane == 0) rstart[NR] = S;
         __syncwarp();
@@ -294,100 +310,90 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
 
         // ---- induced subgraph: scan the flattened rows in 32-entry windows
         int2* const ed = p.escratch + (size_t)r * p.e_stride;
-        const unsigned es = (unsigned)p.e_stride;
-        int count = 0;
-        // Row owning lane's entry of window w, given the row c holding the
-        // window's first entry: c + #row starts in (base, base + lane].
-        auto owner = [&](int c, int base) -> int {
-            const int off = rstart[c + 1 + lane] - base;
-            const unsigned bit = ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u;
-            return c + __popc(__reduce_or_sync(kFull, bit) & le);
+        int2* const ed_end = ed + p.e_stride;
+        int2* edc = ed;  // next free edge slot
+        // Emit the hits of one window in scan order. CHK is set when the
+        // slot might overflow: stores are then bounds-checked, overflow is
+        // reported below and the host re-runs the call with larger slots.
+        auto emit = [&](int j, int rowsh, int kk, auto chk) {
+            const unsigned hb = ballot_nonneg(j);
+            int2* dst = edc + __popc(hb & lt);
+            if (j >= 0 && (!decltype(chk)::value || dst < ed_end))
+                *dst = make_int2(rowsh | j, HAS_GID ? __ldg(p.a_gid + kk) : kk);
+            edc += __popc(hb);
         };
-        // Emit the hits of one window in scan order. The capacity check is
-        // hoisted: `room` says every lane's slot fits (count + 32 <= stride).
-        auto emit = [&](int j, int own, int kk) {
-            const unsigned hb = __ballot_sync(kFull, j >= 0);
-            const unsigned t = (unsigned)count + __popc(hb & lt);
-            if (j >= 0 && t < es) {
-                const int32_t gid = HAS_GID ? __ldg(p.a_gid + kk) : kk;
-                ed[t] = make_int2((rinfo[own].y << 16) | j, gid);
-            }
-            count += __popc(hb);
-        };
-        constexpr int G = 4;  // windows in flight per iteration
-        auto group = [&](int w, bool guard) {
-            int own[G], kk[G];
-            uint32_t v[G];
+        constexpr int G = 4;  // windows in flight per group
+        auto fetch = [&](int w, int (&rs)[G], int (&kk)[G], uint32_t (&v)[G]) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
-                const int base = (w + u) << 5;
-                if (!guard || w + u < nwin) {
-                    own[u] = (int)wcur[w + u] + __popc(wmask[w + u] & le);
-                    if (guard) own[u] = min(own[u], NR - 1);
-                    kk[u] = base + lane + rinfo[own[u]].x;
-                    if (guard && base + lane >= S) kk[u] = -1;
-                } else {
-                    own[u] = 0;
-                    kk[u] = -1;
-                }
-            }
-#pragma unroll
-            for (int u = 0; u < G; ++u) v[u] = (!guard || kk[u] >= 0) ? (uint32_t)__ldg(p.a_ci + kk[u]) : 0u;
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-                if (!guard || w + u < nwin) emit((!guard || kk[u] >= 0) ? hs.find_rank(v[u]) : -1, own[u], kk[u]);
-            }
-        };
-        // Full groups are software-pipelined: the column loads of group g+1
-        // are in flight while group g is probed and emitted.
-        auto fetch = [&](int w, int (&own)[G], int (&kk)[G], uint32_t (&v)[G]) {
-#pragma unroll
-            for (int u = 0; u < G; ++u) {
-                own[u] = (int)wcur[w + u] + __popc(wmask[w + u] & le);
-                kk[u] = ((w + u) << 5) + lane + rinfo[own[u]].x;
+                const int own = (int)wcur[w + u] + __popc(wmask[w + u] & le);
+                const int2 ri = rinfo[own];
+                kk[u] = ((w + u) << 5) + lane + ri.x;
+                rs[u] = ri.y;
             }
 #pragma unroll
             for (int u = 0; u < G; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
         };
-        auto consume = [&](const int (&own)[G], const int (&kk)[G], const uint32_t (&v)[G]) {
+        auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G]) {
+            int j[G];
 #pragma unroll
-            for (int u = 0; u < G; ++u) emit(hs.find_rank(v[u]), own[u], kk[u]);
+            for (int u = 0; u < G; ++u) j[u] = hs.find_rank(v[u]);
+            if (edc + 32 * G <= ed_end) {
+#pragma unroll
+                for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::false_type{});
+            } else {
+#pragma unroll
+                for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::true_type{});
+            }
         };
         int w = 0;
         if (direct) {
-            const int nfg = (S >> 5) / G;  // groups whose windows are all full
+            // full groups, software-pipelined: the column loads of group g+1
+            // are in flight while group g is probed and emitted
+            const int nfg = (S >> 5) / G;
             if (nfg > 0) {
-                int ownA[G], kkA[G], ownB[G], kkB[G];
+                int rsA[G], kkA[G], rsB[G], kkB[G];
                 uint32_t vA[G], vB[G];
-                fetch(0, ownA, kkA, vA);
+                fetch(0, rsA, kkA, vA);
                 for (int gi = 0; gi < nfg; gi += 2) {
-                    if (gi + 1 < nfg) fetch((gi + 1) * G, ownB, kkB, vB);
-                    consume(ownA, kkA, vA);
+                    if (gi + 1 < nfg) fetch((gi + 1) * G, rsB, kkB, vB);
+                    consume(rsA, kkA, vA);
                     if (gi + 1 < nfg) {
-                        if (gi + 2 < nfg) fetch((gi + 2) * G, ownA, kkA, vA);
-                        consume(ownB, kkB, vB);
+                        if (gi + 2 < nfg) fetch((gi + 2) * G, rsA, kkA, vA);
+                        consume(rsB, kkB, vB);
                     }
                 }
                 w = nfg * G;
             }
-            for (; w < nwin; w += G) group(w, true);
+            for (; w < nwin; ++w) {  // < G trailing windows, the last one partial
+                const int base = w << 5;
+                const int own = min((int)wcur[w] + __popc(wmask[w] & le), NR - 1);
+                const int2 ri = rinfo[own];
+                const int kk = base + lane < S ? base + lane + ri.x : -1;
+                const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
+                emit(j, ri.y, kk, std::true_type{});
+            }
         } else {
             int cursor = 0;  // huge sets: serial window cursor
             for (; w < nwin; ++w) {
                 const int base = w << 5;
-                const int own = min(owner(cursor, base), NR - 1);
+                const int c = cursor;
+                const int off = rstart[c + 1 + lane] - base;
+                const unsigned bit = ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u;
+                const int own = min(c + __popc(__reduce_or_sync(kFull, bit) & le), NR - 1);
                 const int own31 = __shfl_sync(kFull, own, 31);
                 cursor = (rstart[own31 + 1] == base + 32) ? own31 + 1 : own31;
-                const int pos = base + lane;
-                const int kk = pos < S ? pos + rinfo[own].x : -1;
+                const int2 ri = rinfo[own];
+                const int kk = base + lane < S ? base + lane + ri.x : -1;
                 const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
-                emit(j, own, kk);
+                emit(j, ri.y, kk, std::true_type{});
             }
         }
+        const int count = (int)(edc - ed);
         if (lane == 0) {
             p.root_nv[r] = U;
             p.root_ne[r] = count;
-            p.root_rloc[r] = hs.find_rank((uint32_t)root);
+            p.root_rloc[r] = T > 0 ? hs.find_rank((uint32_t)root) : -1;
             p.root_scan[r] = S;
             if (count > p.e_stride) {
                 atomicMax(&p.ticket[4], count);
@@ -447,10 +453,15 @@ __global__ void k_scan_reduce(const int32_t* __restrict__ nv, const int32_t* __r
     if (threadIdx.x == 0) { tile_sums[2 * blockIdx.x] = ta; tile_sums[2 * blockIdx.x + 1] = tb; }
 }
 
-__global__ void k_scan_tiles(int64_t* __restrict__ tile_sums, int32_t tiles, int32_t* __restrict__ ticket) {
+// carry: (voff, eoff) at the chunk start, or null for the first chunk
+__global__ void k_scan_tiles(int64_t* __restrict__ tile_sums, int32_t tiles, const int32_t* __restrict__ cv,
+                             const int32_t* __restrict__ ce, int32_t* __restrict__ ticket) {
     __shared__ int64_t sh[66];
     __shared__ int64_t carry[2];
-    if (threadIdx.x == 0) { carry[0] = 0; carry[1] = 0; }
+    if (threadIdx.x == 0) {
+        carry[0] = cv ? (int64_t)*cv : 0;
+        carry[1] = ce ? (int64_t)*ce : 0;
+    }
     __syncthreads();
     for (int t0 = 0; t0 < tiles; t0 += blockDim.x) {
         const int t = t0 + threadIdx.x;
@@ -498,12 +509,13 @@ __global__ void k_scan_apply(const int32_t* __restrict__ nv, const int32_t* __re
     }
 }
 
-void launch_scan(const int32_t* nv, const int32_t* ne, int32_t R, int64_t* tmp, int32_t* voff,
+void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, int64_t* tmp, int32_t* voff,
                  int32_t* eoff, int32_t* ticket, cudaStream_t st) {
+    const int32_t R = r1 - r0;
     const int tiles = (R + kPairTile - 1) / kPairTile;
-    k_scan_reduce<<<tiles, 256, 0, st>>>(nv, ne, R, tmp);
-    k_scan_tiles<<<1, 1024, 0, st>>>(tmp, tiles, ticket);
-    k_scan_apply<<<tiles, 256, 0, st>>>(nv, ne, R, tmp, tiles, voff, eoff);
+    k_scan_reduce<<<tiles, 256, 0, st>>>(nv + r0, ne + r0, R, tmp);
+    k_scan_tiles<<<1, 1024, 0, st>>>(tmp, tiles, r0 ? voff + r0 : nullptr, r0 ? eoff + r0 : nullptr, ticket);
+    k_scan_apply<<<tiles, 256, 0, st>>>(nv + r0, ne + r0, R, tmp, tiles, voff + r0, eoff + r0);
     HGS_CUDA(cudaGetLastError());
 }
 
@@ -519,7 +531,7 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
     int32_t* sset = pack_smem + (size_t)(threadIdx.x >> 5) * p.set_cap;  // the root's set, staged
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     constexpr int U = 4;  // independent loads in flight per lane
-    for (int r = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
+    for (int r = p.r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
         int b;
         {
             int lo = 0, hi = p.k;  // largest b with batch_off[b] <= r
@@ -533,6 +545,7 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
         const int64_t vb = p.root_voff[r], eb = p.root_eoff[r];
         const int Vr = p.root_voff[r + 1] - (int32_t)vb;
         const int Er = p.root_eoff[r + 1] - (int32_t)eb;
+        if (Er > p.e_stride) continue;  // slot overflowed in K2 (reported there): the call is re-run
         if (vb + Vr > p.v_cap || eb + Er > p.e_cap) {
             if (lane == 0) report(p.ticket, kErrCapacity, r, -1);
             continue;

@@ -65,6 +65,7 @@ struct DevGraph {
     int device = 0;
     int64_t n_rows = 0, n_cols = 0, nnz = 0;  // as given by the caller
     DevCsr a;                // extraction matrix: A minus explicit zeros
+    DevBuf<int2> a_ri;       // per vertex of a: (row start, out-degree), one 8-byte load
     DevBuf<int32_t> a_gid;   // a position -> input CSR position (only if zeros dropped)
     bool has_gid = false;
     DevCsr a_full;           // full pattern of A (only if zeros dropped; else == a)
@@ -106,6 +107,15 @@ void scan_exclusive_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t
 constexpr unsigned kFull = 0xffffffffu;
 
 __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
+
+// Full-warp ballot for code the caller knows to be converged: plain
+// vote.sync without the divergence fallback ptxas wraps __ballot_sync in.
+__device__ __forceinline__ unsigned ballot_nonneg(int x) {  // ballot(x >= 0)
+    unsigned r;
+    asm volatile("{ .reg .pred q; setp.ge.s32 q, %1, 0; vote.sync.ballot.b32 %0, q, 0xffffffff; }"
+                 : "=r"(r) : "r"(x));
+    return r;
+}
 
 template <class T>
 __device__ __forceinline__ T warp_incl_scan(T v) {
@@ -229,6 +239,9 @@ struct hgs_sample {
     bool profiled = false;
     cudaEvent_t ev[6] = {};
     int64_t launches = 0;
+    // chunked pipeline: packing runs on a higher-priority side stream
+    cudaStream_t aux = nullptr;
+    std::vector<cudaEvent_t> chunk_ev;
 };
 
 namespace hgs {

@@ -24,7 +24,7 @@ struct ExpandParams {
     const int64_t* __restrict__ roots64;
     const uint64_t* __restrict__ seeds;
     const uint64_t* __restrict__ state;   // nullable: resume states
-    int32_t R, depth, fanout, n;
+    int32_t r0, R, depth, fanout, n;     // roots [r0, R) of the call
     int64_t stride;
     int32_t cache_entries;                // (b,deg) entries cached per lane in smem
     int32_t recip_smem;                   // recip entries staged in smem (0: read global)
@@ -44,10 +44,11 @@ struct ExtractParams {
     const int32_t* __restrict__ a_rp;
     const int32_t* __restrict__ a_ci;
     const int32_t* __restrict__ a_gid;  // nullable
+    const int2* __restrict__ a_ri;      // per vertex: (A row start, out-degree)
     int32_t* __restrict__ touched;      // in: touched lists; out: sorted sets
     const int32_t* __restrict__ tcount;
     int64_t stride;
-    int32_t R;
+    int32_t r0, R;                      // roots [r0, R)
     int32_t* __restrict__ root_nv;
     int32_t* __restrict__ root_ne;
     int32_t* __restrict__ root_rloc;
@@ -56,6 +57,7 @@ struct ExtractParams {
     int32_t e_stride;
     int32_t* __restrict__ ticket;
     int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
+    int32_t cnt_lg;                     // log2 of the bucket-counter capacity (<= 2*row_cap)
 };
 
 // K3: packing + gather.
@@ -68,7 +70,7 @@ struct PackParams {
     const int2* __restrict__ escratch;
     int32_t e_stride;
     const int64_t* __restrict__ batch_off;
-    int32_t k, R;
+    int32_t k, r0, R;                   // roots [r0, R)
     int32_t* __restrict__ l2g;
     int32_t* __restrict__ roots_local;
     int32_t* __restrict__ comp_off;
@@ -90,7 +92,9 @@ struct PackParams {
 
 void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st);
 int extract_blocks_per_sm(size_t smem, bool packed);
-void launch_scan(const int32_t* nv, const int32_t* ne, int32_t R, int64_t* tmp, int32_t* voff,
+// Exclusive scan of (V_r, E_r) over roots [r0, r1) into voff/eoff[r0..r1];
+// for r0 > 0 the carry-in is voff/eoff[r0] as written by the previous chunk.
+void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, int64_t* tmp, int32_t* voff,
                  int32_t* eoff, int32_t* ticket, cudaStream_t st);
 int64_t scan_tmp_words(int64_t R);
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st);

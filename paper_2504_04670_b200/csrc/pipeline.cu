@@ -68,7 +68,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     int bits = 2;
     while (((int64_t)4 << bits) < spk * c.max_t) ++bits;
     c.nb_bits = bits;
-    c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);  // sets > 256 sort in the row arrays
+    c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);
     c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
     c.win_cap = c.set_cap * 2 / 3;  // (u32 mask + u16 cursor) per window alias the set array
     const size_t slots = (size_t)4 << c.nb_bits;
@@ -146,64 +146,107 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     s->profiled = cfg.profile != 0;
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[0], st));
 
-    if (R > 0) {
-        ExpandParams ep{};
-        ep.w_rp = walk.rp.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
-        ep.neg_row = (!cfg.symmetrize && !seq_walk && g.has_neg) ? g.neg_row.p : nullptr;
-        ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
-        ep.R = (int32_t)R; ep.depth = (int32_t)cfg.depth;
-        ep.fanout = (int32_t)std::min<int64_t>(cfg.fanout, 1 << 30);
-        ep.n = (int32_t)g.n_rows; ep.stride = c.max_t; ep.cache_entries = (int32_t)c.cache_entries;
-        ep.recip_smem = c.recip_smem;
-        ep.touched = s->touched.p; ep.tcount = s->tcount.p; ep.level_counts = s->level_counts.p;
-        ep.draws = s->draws.p; ep.decisions = s->decisions.p; ep.ticket = s->ticket.p;
+    ExpandParams ep{};
+    ep.w_rp = walk.rp.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
+    ep.neg_row = (!cfg.symmetrize && !seq_walk && g.has_neg) ? g.neg_row.p : nullptr;
+    ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
+    ep.depth = (int32_t)cfg.depth;
+    ep.fanout = (int32_t)std::min<int64_t>(cfg.fanout, 1 << 30);
+    ep.n = (int32_t)g.n_rows; ep.stride = c.max_t; ep.cache_entries = (int32_t)c.cache_entries;
+    ep.recip_smem = c.recip_smem;
+    ep.touched = s->touched.p; ep.tcount = s->tcount.p; ep.level_counts = s->level_counts.p;
+    ep.draws = s->draws.p; ep.decisions = s->decisions.p; ep.ticket = s->ticket.p;
+
+    ExtractParams xp{};
+    xp.a_rp = g.a.rp.p; xp.a_ci = g.a.ci.p; xp.a_gid = g.has_gid ? g.a_gid.p : nullptr; xp.a_ri = g.a_ri.p;
+    xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t;
+    xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
+    xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
+    xp.ticket = s->ticket.p; xp.nb_bits = c.nb_bits; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
+    xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
+    xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
+    const size_t xsmem = (size_t)4 * c.warp_bytes;
+
+    PackParams pp{};
+    pp.touched = s->touched.p; pp.stride = c.max_t; pp.root_voff = s->root_voff.p;
+    pp.root_eoff = s->root_eoff.p; pp.root_rloc = s->root_rloc.p; pp.escratch = s->escratch.p;
+    pp.e_stride = s->e_stride; pp.batch_off = in.batch_off; pp.k = (int32_t)k;
+    pp.l2g = s->l2g.p; pp.roots_local = s->roots_local.p; pp.comp_off = s->comp_off.p;
+    pp.e_row = s->e_row.p; pp.e_col = s->e_col.p; pp.e_gid = s->e_gid.p;
+    pp.xv = s->xv.p; pp.ye = s->ye.p; pp.lab = s->lab.p;
+    pp.node_feat = g.node_feat.p; pp.edge_feat = g.edge_feat.p; pp.labels = g.labels.p;
+    pp.f_v = g.f_v; pp.f_e = g.f_e; pp.gather = cfg.gather;
+    const uint32_t q2 = (uint32_t)std::max(1, g.f_v / 2);
+    pp.fv_magic = (uint32_t)((((uint64_t)1 << 32) + q2 - 1) / q2);
+    pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
+    pp.set_cap = c.set_cap;
+
+    // Roots go through the stages in chunks: K1 -> K2 -> offset scan of chunk
+    // c on the handle's stream, K3 of chunk c on a higher-priority side
+    // stream, so the memory-bound packing of chunk c runs on the SMs next to
+    // the latency-bound extraction of chunk c+1. A profiled call runs as one
+    // serial chunk so each stage can be timed on its own.
+    // Off by default: measured on B200 at C2, packing next to extraction
+    // slows both (they contend for the LSU pipe), see DESIGN.md.
+    int64_t chunk = R;
+    if (!s->profiled)
+        if (const char* e = getenv("HGS_CHUNK_ROOTS")) chunk = std::max<int64_t>(32, atoll(e));
+    const int64_t nchunks = R > 0 ? (R + chunk - 1) / chunk : 0;
+    const bool split = nchunks > 1;
+    cudaStream_t pst = st;
+    if (split) {
+        if (!s->aux) {
+            int lo = 0, hi = 0;
+            HGS_CUDA(cudaDeviceGetStreamPriorityRange(&lo, &hi));
+            HGS_CUDA(cudaStreamCreateWithPriority(&s->aux, cudaStreamNonBlocking, hi));
+        }
+        while ((int64_t)s->chunk_ev.size() < nchunks + 1) {
+            cudaEvent_t e;
+            HGS_CUDA(cudaEventCreateWithFlags(&e, cudaEventDisableTiming));
+            s->chunk_ev.push_back(e);
+        }
+        pst = s->aux;
+        HGS_CUDA(cudaEventRecord(s->chunk_ev[nchunks], st));  // aux waits for this call's inputs
+        HGS_CUDA(cudaStreamWaitEvent(pst, s->chunk_ev[nchunks], 0));
+    }
+    const int xper_sm = extract_blocks_per_sm(xsmem, c.packed != 0);
+    if (R > 0) {  // K1 over all roots at once: one lane per root, its length is one root's chain
+        ep.r0 = 0; ep.R = (int32_t)R;
         launch_expand(c.expand_threads, c.expand_smem, c.kmax, ep, cfg.rng == HGS_RNG_PHILOX, st);
         ++s->launches;
     }
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[1], st));
-    if (R > 0) {
-        ExtractParams xp{};
-        xp.a_rp = g.a.rp.p; xp.a_ci = g.a.ci.p; xp.a_gid = g.has_gid ? g.a_gid.p : nullptr;
-        xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t; xp.R = (int32_t)R;
-        xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
-        xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
-        xp.ticket = s->ticket.p; xp.nb_bits = c.nb_bits; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
-        xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
-        const size_t smem = (size_t)4 * c.warp_bytes;
-        const int per_sm = extract_blocks_per_sm(smem, c.packed != 0);
-        const int64_t grid = std::min<int64_t>((int64_t)per_sm * sm_count(g.device), (R + 3) / 4);
-        launch_extract((int)std::max<int64_t>(grid, 1), smem, xp, c.packed != 0, st);
+    for (int64_t ci = 0; ci < nchunks; ++ci) {
+        const int32_t r0 = (int32_t)(ci * chunk), r1 = (int32_t)std::min<int64_t>(R, r0 + chunk);
+        const int64_t Rc = r1 - r0;
+        xp.r0 = r0; xp.R = r1;
+        const int64_t xgrid = split ? (Rc + 3) / 4 : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + 3) / 4);
+        launch_extract((int)std::max<int64_t>(xgrid, 1), xsmem, xp, c.packed != 0, st);
         ++s->launches;
-    }
-    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
-    if (R > 0) {
-        launch_scan(s->root_nv.p, s->root_ne.p, (int32_t)R, s->scan_tmp.p, s->root_voff.p, s->root_eoff.p,
+        if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
+        launch_scan(s->root_nv.p, s->root_ne.p, r0, r1, s->scan_tmp.p, s->root_voff.p, s->root_eoff.p,
                     s->ticket.p, st);
         s->launches += 3;
-    }
-    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[3], st));
-    if (R > 0) {
-        PackParams pp{};
-        pp.touched = s->touched.p; pp.stride = c.max_t; pp.root_voff = s->root_voff.p;
-        pp.root_eoff = s->root_eoff.p; pp.root_rloc = s->root_rloc.p; pp.escratch = s->escratch.p;
-        pp.e_stride = s->e_stride; pp.batch_off = in.batch_off; pp.k = (int32_t)k; pp.R = (int32_t)R;
-        pp.l2g = s->l2g.p; pp.roots_local = s->roots_local.p; pp.comp_off = s->comp_off.p;
-        pp.e_row = s->e_row.p; pp.e_col = s->e_col.p; pp.e_gid = s->e_gid.p;
-        pp.xv = s->xv.p; pp.ye = s->ye.p; pp.lab = s->lab.p;
-        pp.node_feat = g.node_feat.p; pp.edge_feat = g.edge_feat.p; pp.labels = g.labels.p;
-        pp.f_v = g.f_v; pp.f_e = g.f_e; pp.gather = cfg.gather;
-        const uint32_t q2 = (uint32_t)std::max(1, g.f_v / 2);
-        pp.fv_magic = (uint32_t)((((uint64_t)1 << 32) + q2 - 1) / q2);
-        pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
-        pp.set_cap = c.set_cap;
-        const int64_t grid = std::min<int64_t>((int64_t)sm_count(g.device) * 8, (R + 7) / 8);
-        launch_pack((int)std::max<int64_t>(grid, 1), pp, st);
+        if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[3], st));
+        if (split) {
+            HGS_CUDA(cudaEventRecord(s->chunk_ev[ci], st));
+            HGS_CUDA(cudaStreamWaitEvent(pst, s->chunk_ev[ci], 0));
+        }
+        pp.r0 = r0; pp.R = r1;
+        const int64_t pgrid = split ? (Rc + 7) / 8 : std::min<int64_t>((int64_t)sm_count(g.device) * 8, (Rc + 7) / 8);
+        launch_pack((int)std::max<int64_t>(pgrid, 1), pp, pst);
         ++s->launches;
+        if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
     }
-    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
+    if (R == 0 && s->profiled)
+        for (int i = 2; i <= 4; ++i) HGS_CUDA(cudaEventRecord(s->ev[i], st));
     launch_finalize(in.batch_off, (int32_t)k, (int32_t)R, s->root_voff.p, s->root_eoff.p, s->batch_voff.p,
-                    s->batch_eoff.p, s->comp_off.p, st);
+                    s->batch_eoff.p, s->comp_off.p, pst);
     ++s->launches;
+    if (split) {  // join: the handle's stream sees the whole call
+        HGS_CUDA(cudaEventRecord(s->chunk_ev[nchunks], pst));
+        HGS_CUDA(cudaStreamWaitEvent(st, s->chunk_ev[nchunks], 0));
+    }
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[5], st));
     if (!s->h_state) HGS_CUDA(cudaMallocHost(&s->h_state, 16 * sizeof(int32_t)));
     HGS_CUDA(cudaMemcpyAsync(s->h_state, s->ticket.p, 8 * sizeof(int32_t), cudaMemcpyDeviceToHost, st));

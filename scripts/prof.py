@@ -25,3 +25,14 @@ for i in range(a.calls):
     c = S.wait()
     print("call", i, c, "kernel ms (expand, extract, finalize, total):", S.kernel_times(), file=sys.stderr)
 print(S.stats(), file=sys.stderr)
+ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
+ts = []
+for i in range(a.calls + 2):
+    with torch.cuda.stream(st):
+        ev[0].record(st)
+        S.run_device(dr.data_ptr(), db.data_ptr(), dr.numel(), db.numel()-1, ds.data_ptr(), depth=3, fanout=6,
+                     rng=1 if a.philox else 0, gather=not a.no_gather, profile=False)
+        ev[1].record(st)
+    S.wait()
+    ts.append(ev[0].elapsed_time(ev[1]))
+print("unprofiled call ms:", " ".join(f"{t:.3f}" for t in ts), file=sys.stderr)

@@ -132,6 +132,46 @@ def test_random_graphs(n, m, depth, fanout, values, rng):
         assert_same(dev, ref, gather)
 
 
+def banded_graph(n, w, seed, outliers=0):
+    """Vertex ids with locality (u -> u+1..u+w) plus a few long-range edges
+    to the top ids: a root's set spans a narrow id range with outliers, which
+    stresses the order-preserving bucketing of K2's set sort."""
+    rs = np.random.default_rng(seed)
+    u = np.repeat(np.arange(n), w)
+    v = u + np.tile(np.arange(1, w + 1), n)
+    keep = (v < n) & (rs.random(len(u)) < 0.7)
+    u, v = u[keep], v[keep]
+    if outliers:
+        ou = rs.integers(0, n, outliers)
+        ov = n - 1 - rs.integers(0, 3, outliers)
+        u, v = np.concatenate([u, ou]), np.concatenate([v, ov])
+    key = np.unique(u.astype(np.int64) * n + v)
+    u, v = key // n, key % n
+    rp = np.zeros(n + 1, np.int64)
+    np.add.at(rp, u + 1, 1)
+    g = O.Graph(n=n, rp=np.cumsum(rp), ci=v.astype(np.int64))
+    g.node_feat = rs.standard_normal((n, 6))
+    g.edge_feat = rs.standard_normal((len(v), 2))
+    g.labels = rs.integers(0, 2, len(v)).astype(np.uint8)
+    return g
+
+
+@pytest.mark.parametrize("n,w,outliers,depth,fanout", [
+    (4000, 8, 0, 3, 6), (4000, 8, 200, 3, 6), (100000, 12, 50, 3, 6), (3000, 30, 0, 2, 17)])
+def test_clustered_vertex_ids(n, w, outliers, depth, fanout):
+    g = banded_graph(n, w, n + w, outliers)
+    rs = np.random.default_rng(w)
+    k, b = 3, 100
+    roots = np.concatenate([rs.permutation(n)[:b] for _ in range(k)]).astype(np.int64)
+    boff = np.arange(k + 1, dtype=np.int64) * b
+    seeds = rs.integers(0, 2**63, k * b, dtype=np.uint64)
+    for sym in (True, False):
+        kw = dict(rng=0, depth=depth, fanout=fanout, symmetrize=sym)
+        dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert_same(dev, ref, True)
+
+
 @pytest.mark.parametrize("rng", [0, 1])
 def test_resumed_streams(rng):
     """Non-fresh sources (rng_state): xoshiro states / Philox decision bases."""
@@ -165,6 +205,26 @@ def test_shadow_reference_walk_semantics():
         device_run(g, roots, boff, seeds, depth=2, fanout=4, symmetrize=False)
     with pytest.raises(O.SamplerError, match="negative"):
         O.bulk_shadow(g, roots, boff, seeds, depth=2, fanout=4, symmetrize=False)
+
+
+@pytest.mark.parametrize("chunk", ["37", "64", "1000"])
+def test_chunked_pipeline(monkeypatch, chunk):
+    """Roots split into chunks (K3 of chunk c on the side stream next to K2 of
+    chunk c+1): identical results for chunk sizes that cut through batches."""
+    monkeypatch.setenv("HGS_CHUNK_ROOTS", chunk)
+    g = random_graph(3000, 30000, 12)
+    rs = np.random.default_rng(int(chunk))
+    sizes = [300, 0, 17, 250, 1, 132]
+    roots = np.concatenate([rs.permutation(3000)[:s] for s in sizes]).astype(np.int64)
+    boff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    seeds = rs.integers(0, 2**63, len(roots), dtype=np.uint64)
+    for rng in (0, 1):
+        kw = dict(rng=rng, depth=3, fanout=6)
+        dev, S = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert_same(dev, ref, True)
+        dev2, _ = device_run(g, roots, boff, seeds, gather=True, sampler=S, **kw)  # reuse the handle
+        assert_same(dev2, ref, True)
 
 
 def test_capacity_regrow(monkeypatch):
