@@ -64,6 +64,23 @@ def build_hgs(force: bool = False) -> str:
     return HGS_SO
 
 
+def build_variant(name: str, defines: list[str]) -> str:
+    """Experiment builds (tuning sweeps): lib/variants/libhgs_<name>.so with
+    extra -D flags; select one at run time with HGS_LIB=<path>."""
+    out = os.path.join(LIB, "variants", f"libhgs_{name}.so")
+    os.makedirs(os.path.dirname(out), exist_ok=True)
+    objs = []
+    for src in sorted(glob.glob(os.path.join(CSRC, "*.cu"))):
+        obj = out + "." + os.path.basename(src) + ".o"
+        _run([NVCC, *ARCH, *NVCC_FLAGS, *[f"-D{d}" for d in defines], "-I", INCLUDE, "-I", CSRC, "-c", src,
+              "-o", obj])
+        objs.append(obj)
+    _run([NVCC, *ARCH, "-shared", "-o", out, *objs])
+    for o in objs:
+        os.remove(o)
+    return out
+
+
 def build_dropin(force: bool = False) -> str | None:
     srcs = sorted(glob.glob(os.path.join(CSRC, "dropin", "*.cpp")))
     if not srcs:

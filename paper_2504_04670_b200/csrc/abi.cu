@@ -12,6 +12,7 @@
 #include <vector>
 
 #include "hgs_internal.cuh"
+#include "kernels.cuh"
 
 using namespace hgs;
 
@@ -194,6 +195,7 @@ int hgs_graph_attach_features(hgs_graph* h, const double* node_feat, int64_t f_v
         upload(g.node_feat.p, node_feat, sizeof(double) * g.n_rows * f_v, g.stream);
         upload(g.edge_feat.p, edge_feat, sizeof(double) * g.nnz * f_e, g.stream);
         upload(g.labels.p, labels, g.nnz, g.stream);
+        build_edge_records(g, g.stream);
         HGS_CUDA(cudaStreamSynchronize(g.stream));
         g.has_features = true;
     });

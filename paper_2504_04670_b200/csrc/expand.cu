@@ -45,7 +45,7 @@ struct RootStream<false> {
             v = x.next();
             ++draws;
         } while (rejected(v, m, rc));
-        return (uint32_t)mod_by_recip(v, m, rc);
+        return mod_small(v, (uint32_t)m, rc);
     }
 };
 
@@ -62,7 +62,7 @@ struct RootStream<true> {
             v = philox_draw(seed, dec, step, att++);
             ++draws;
         } while (rejected(v, m, rc));
-        return (uint32_t)mod_by_recip(v, m, rc);
+        return mod_small(v, (uint32_t)m, rc);
     }
 };
 
@@ -139,7 +139,7 @@ __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
 }
 
 template <int KCAP, bool PHILOX, bool LOCAL>
-__global__ void __launch_bounds__(128) k_expand(ExpandParams p) {
+__global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
     extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree), then the recip table
     const int r = p.r0 + blockIdx.x * blockDim.x + threadIdx.x;
     // bounded() reciprocals in shared memory when the table is small
@@ -174,59 +174,121 @@ __global__ void __launch_bounds__(128) k_expand(ExpandParams p) {
         if (cached) cache[ti] = make_int2(b, p.w_rp[root + 1] - b);
     }
     int T = 1, lvl_begin = 0, lvl_end = 1;
-    for (int level = 0; level < p.depth; ++level) {
-        const bool expand_next = level + 1 < p.depth;
-        const int next_begin = T;
-        for (int idx = lvl_begin; idx < lvl_end; ++idx) {
-            int2 row;
-            if (cached) row = cache[(size_t)idx * bd + ti];
+    bool bad = false;
+    // next expandable row of the level (empty rows make no choose call,
+    // sampler.cpp:75); false at the end of the level or on a negative row
+    auto next_row = [&](int& idx, int2& row, int level) -> bool {
+        while (idx < lvl_end) {
+            const int i = idx++;
+            if (cached) row = cache[(size_t)i * bd + ti];
             else {
-                const int32_t v = out[idx];
+                const int32_t v = out[i];
                 row.x = p.w_rp[v];
                 row.y = p.w_rp[v + 1] - row.x;
             }
-            if (row.y == 0) continue;  // empty rows make no choose call (sampler.cpp:75)
-            if (p.neg_row && p.neg_row[out[idx]]) {
+            if (row.y == 0) continue;
+            if (p.neg_row && p.neg_row[out[i]]) {
                 report(p.ticket, kErrNegative, r, level);
-                p.tcount[r] = T;
-                return;
+                bad = true;
+                return false;
             }
-            const uint32_t deg = (uint32_t)row.y;
-            const uint32_t k = min((uint32_t)p.fanout, deg);
-            rs.begin_decision(ndec);
-            ++ndec;
-            if (!LOCAL) {
-                uint32_t pos[KCAP];
-                choose_small<KCAP, PHILOX>(rs, deg, k, recip, pos);
-                int32_t c[KCAP];
-#pragma unroll
-                for (int q = 0; q < KCAP; ++q) c[q] = q < (int)k ? __ldg(p.w_ci + row.x + pos[q]) : 0;
-#pragma unroll
-                for (int q = 0; q < KCAP; ++q) if (q < (int)k) out[T + q] = c[q];
-                if (expand_next && cached) {
-                    int32_t b0[KCAP], b1[KCAP];
-#pragma unroll
-                    for (int q = 0; q < KCAP; ++q) {
-                        b0[q] = q < (int)k ? __ldg(p.w_rp + c[q]) : 0;
-                        b1[q] = q < (int)k ? __ldg(p.w_rp + c[q] + 1) : 0;
-                    }
-#pragma unroll
-                    for (int q = 0; q < KCAP; ++q)
-                        if (q < (int)k) cache[(size_t)(T + q) * bd + ti] = make_int2(b0[q], b1[q] - b0[q]);
-                }
-                T += (int)k;
-            } else {
+            return true;
+        }
+        return false;
+    };
+    auto decide = [&](const int2& row, uint32_t (&pos)[KCAP]) -> uint32_t {
+        const uint32_t deg = (uint32_t)row.y;
+        const uint32_t k = min((uint32_t)p.fanout, deg);
+        rs.begin_decision(ndec);
+        ++ndec;
+        choose_small<KCAP, PHILOX>(rs, deg, k, recip, pos);
+        return k;
+    };
+    for (int level = 0; level < p.depth; ++level) {
+        const bool in_cache = level + 1 < p.depth && cached;
+        const int next_begin = T;
+        int idx = lvl_begin;
+        int2 row;
+        if (LOCAL) {
+            while (next_row(idx, row, level)) {
+                const uint32_t deg = (uint32_t)row.y;
+                const uint32_t k = min((uint32_t)p.fanout, deg);
+                rs.begin_decision(ndec);
+                ++ndec;
                 uint32_t pos[256];
                 choose_local<PHILOX>(rs, deg, k, recip, pos);
-                for (uint32_t q = 0; q < k; ++q) {
-                    const int32_t c = __ldg(p.w_ci + row.x + pos[q]);
-                    out[T] = c;
-                    if (expand_next && cached) {
-                        const int32_t cb = __ldg(p.w_rp + c);
-                        cache[(size_t)T * bd + ti] = make_int2(cb, __ldg(p.w_rp + c + 1) - cb);
-                    }
-                    ++T;
+                for (uint32_t q = 0; q < k; ++q, ++T) {
+                    if (in_cache) cache[(size_t)T * bd + ti].x = row.x + (int32_t)pos[q];
+                    else out[T] = row.x + (int32_t)pos[q];
                 }
+            }
+        } else if (in_cache) {
+            // park the chosen walk positions in the children's cache slots
+            while (next_row(idx, row, level)) {
+                uint32_t pos[KCAP];
+                const uint32_t k = decide(row, pos);
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q)
+                    if (q < (int)k) cache[(size_t)(T + q) * bd + ti].x = row.x + (int32_t)pos[q];
+                T += (int)k;
+            }
+        } else {
+            // child loads of decision i are in flight during decision i+1:
+            // two register sets, stores of a set one decision late
+            int32_t cA[KCAP], cB[KCAP];
+            int TA = 0, kA = 0, TB = 0, kB = 0;
+            auto issue = [&](const int2& rw, int32_t (&c)[KCAP], int& Tc, int& kc) {
+                uint32_t pos[KCAP];
+                kc = (int)decide(rw, pos);
+                Tc = T;
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q) c[q] = q < kc ? __ldg(p.w_ci + rw.x + pos[q]) : 0;
+                T += kc;
+            };
+            auto flush = [&](const int32_t (&c)[KCAP], int Tc, int& kc) {
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q)
+                    if (q < kc) out[Tc + q] = c[q];
+                kc = 0;
+            };
+            for (;;) {
+                if (!next_row(idx, row, level)) break;
+                issue(row, cA, TA, kA);
+                flush(cB, TB, kB);
+                if (!next_row(idx, row, level)) break;
+                issue(row, cB, TB, kB);
+                flush(cA, TA, kA);
+            }
+            flush(cA, TA, kA);
+            flush(cB, TB, kB);
+        }
+        if (bad) {
+            p.tcount[r] = T;
+            return;
+        }
+        if (LOCAL || in_cache) {
+            // resolve parked walk positions -> vertices (+ next-level rows)
+            constexpr int U = 8;
+            for (int t0 = next_begin; t0 < T; t0 += U) {
+                int32_t e[U], c[U];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (t0 + u < T) e[u] = in_cache ? cache[(size_t)(t0 + u) * bd + ti].x : out[t0 + u];
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (t0 + u < T) c[u] = __ldg(p.w_ci + e[u]);
+                if (in_cache) {
+                    int32_t b0[U], b1[U];
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (t0 + u < T) { b0[u] = __ldg(p.w_rp + c[u]); b1[u] = __ldg(p.w_rp + c[u] + 1); }
+#pragma unroll
+                    for (int u = 0; u < U; ++u)
+                        if (t0 + u < T) cache[(size_t)(t0 + u) * bd + ti] = make_int2(b0[u], b1[u] - b0[u]);
+                }
+#pragma unroll
+                for (int u = 0; u < U; ++u)
+                    if (t0 + u < T) out[t0 + u] = c[u];
             }
         }
         lc[level + 1] = T - next_begin;

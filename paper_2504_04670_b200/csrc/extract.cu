@@ -322,7 +322,10 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
                 *dst = make_int2(rowsh | j, HAS_GID ? __ldg(p.a_gid + kk) : kk);
             edc += __popc(hb);
         };
-        constexpr int G = 4;  // windows in flight per group
+#ifndef HGS_K2_G
+#define HGS_K2_G 4
+#endif
+        constexpr int G = HGS_K2_G;  // windows in flight per group
         auto fetch = [&](int w, int (&rs)[G], int (&kk)[G], uint32_t (&v)[G]) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
@@ -351,6 +354,15 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
             // full groups, software-pipelined: the column loads of group g+1
             // are in flight while group g is probed and emitted
             const int nfg = (S >> 5) / G;
+#if HGS_K2_SINGLE
+            for (int gi = 0; gi < nfg; ++gi) {
+                int rsA[G], kkA[G];
+                uint32_t vA[G];
+                fetch(gi * G, rsA, kkA, vA);
+                consume(rsA, kkA, vA);
+            }
+            w = nfg * G;
+#else
             if (nfg > 0) {
                 int rsA[G], kkA[G], rsB[G], kkB[G];
                 uint32_t vA[G], vB[G];
@@ -365,6 +377,7 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
                 }
                 w = nfg * G;
             }
+#endif
             for (; w < nwin; ++w) {  // < G trailing windows, the last one partial
                 const int base = w << 5;
                 const int own = min((int)wcur[w] + __popc(wmask[w] & le), NR - 1);
@@ -526,11 +539,9 @@ int64_t scan_tmp_words(int64_t R) { return 2 * ((R + kPairTile - 1) / kPairTile)
 // ===========================================================================
 
 __global__ void __launch_bounds__(256) k_pack(PackParams p) {
-    extern __shared__ int32_t pack_smem[];
     const int lane = lane_id();
-    int32_t* sset = pack_smem + (size_t)(threadIdx.x >> 5) * p.set_cap;  // the root's set, staged
     const int nwarps = gridDim.x * (blockDim.x >> 5);
-    constexpr int U = 4;  // independent loads in flight per lane
+    constexpr int U = 8;  // independent loads in flight per lane
     for (int r = p.r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
         int b;
         {
@@ -551,90 +562,158 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
             continue;
         }
         const int32_t loc = (int32_t)vb - p.root_voff[f];
-        const int32_t* set = p.touched + (size_t)r * p.stride;
-        for (int i = lane; i < Vr; i += 32) {
-            const int32_t u = set[i];
-            sset[i] = u;
-            __stcs(p.l2g + vb + i, u);
-        }
         if (lane == 0) {
             p.roots_local[r] = loc + p.root_rloc[r];
             p.comp_off[r + b] = loc;
             if (r == p.batch_off[b + 1] - 1) p.comp_off[r + 1 + b] = loc + Vr;
         }
+        // local_to_global: the sorted set, as K2 left it in the touched slot
+        const int32_t* set = p.touched + (size_t)r * p.stride;
+        for (int i0 = 0; i0 < Vr; i0 += 32 * U) {
+            int32_t u[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + 32 * k + lane;
+                u[k] = i < Vr ? set[i] : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + 32 * k + lane;
+                if (i < Vr) __stcs(p.l2g + vb + i, u[k]);
+            }
+        }
+        // COO edges (block_diag rebasing) and edge ids
         const int2* ed = p.escratch + (size_t)r * p.e_stride;
-        const bool fe2 = p.gather && p.f_e == 2;
         for (int t0 = 0; t0 < Er; t0 += 32 * U) {
             int2 e[U];
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int t = t0 + 32 * u + lane;
-                e[u] = t < Er ? ed[t] : make_int2(0, -1);
-            }
-            double2 x[U];
-            uint8_t lb[U];
-            if (p.gather) {
-#pragma unroll
-                for (int u = 0; u < U; ++u) {
-                    if (e[u].y >= 0) {
-                        lb[u] = __ldg(p.labels + e[u].y);
-                        if (fe2) x[u] = __ldg(reinterpret_cast<const double2*>(p.edge_feat) + e[u].y);
-                    }
-                }
+            for (int k = 0; k < U; ++k) {
+                const int t = t0 + 32 * k + lane;
+                e[k] = t < Er ? ed[t] : make_int2(0, 0);
             }
 #pragma unroll
-            for (int u = 0; u < U; ++u) {
-                const int t = t0 + 32 * u + lane;
+            for (int k = 0; k < U; ++k) {
+                const int t = t0 + 32 * k + lane;
                 if (t < Er) {
-                    __stcs(p.e_row + eb + t, loc + (e[u].x >> 16));
-                    __stcs(p.e_col + eb + t, loc + (e[u].x & 0xffff));
-                    __stcs(p.e_gid + eb + t, e[u].y);
-                    if (p.gather) {
-                        p.lab[eb + t] = lb[u];
-                        if (fe2) {
-                            __stcs(reinterpret_cast<double2*>(p.ye) + eb + t, x[u]);
-                        } else {
-                            for (int c = 0; c < p.f_e; ++c)
-                                __stcs(p.ye + (eb + t) * p.f_e + c,
-                                       __ldg(p.edge_feat + (int64_t)e[u].y * p.f_e + c));
-                        }
-                    }
+                    __stcs(p.e_row + eb + t, loc + (e[k].x >> 16));
+                    __stcs(p.e_col + eb + t, loc + (e[k].x & 0xffff));
+                    __stcs(p.e_gid + eb + t, e[k].y);
                 }
             }
         }
-        __syncwarp();
-        if (p.gather) {
-            if ((p.f_v & 1) == 0) {  // rows as f_v/2 16-byte pieces
-                const int q2 = p.f_v >> 1;
-                const int n2 = Vr * q2;
-                const double2* src = reinterpret_cast<const double2*>(p.node_feat);
-                double2* dst = reinterpret_cast<double2*>(p.xv) + vb * q2;
-                for (int e0 = 0; e0 < n2; e0 += 32 * U) {
-                    double2 x[U];
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int e = e0 + 32 * u + lane;
-                        if (e < n2) {
-                            const int i = (int)__umulhi((unsigned)e, p.fv_magic);
-                            x[u] = __ldg(src + (int64_t)sset[i] * q2 + (e - i * q2));
-                        }
-                    }
-#pragma unroll
-                    for (int u = 0; u < U; ++u) {
-                        const int e = e0 + 32 * u + lane;
-                        if (e < n2) __stcs(dst + e, x[u]);
-                    }
-                }
-            } else {
-                double* dst = p.xv + vb * p.f_v;
-                for (int e = lane; e < Vr * p.f_v; e += 32) {
-                    const int i = e / p.f_v;
-                    __stcs(dst + e, __ldg(p.node_feat + (int64_t)sset[i] * p.f_v + (e - i * p.f_v)));
-                }
-            }
-        }
-        __syncwarp();
     }
+}
+
+// gather_features (sampler.cpp:211-243) over the packed outputs: node rows
+// of l2g, edge rows and labels of the edge ids. Flat grid-stride streams.
+// Random rows come from L2 (the event's features are L2-resident), where the
+// bound is the number of sector requests, not bytes: node rows are read as
+// 16-byte pieces by adjacent threads (one warp instruction touches ~11 rows
+// and their shared sectors), and edge features + label come as one 32-byte
+// record per edge (DevGraph::erec) instead of two requests.
+__global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__ node_feat, int32_t f_v,
+                                                      uint32_t fv_magic, const int32_t* __restrict__ l2g,
+                                                      const int32_t* __restrict__ V_ptr, int64_t v_cap,
+                                                      const int32_t* __restrict__ ticket,
+                                                      double* __restrict__ xv) {
+    if (ticket[1] != 0) return;  // failed call (re-run or reported): l2g may be incomplete
+    const int64_t V = min((int64_t)*V_ptr, v_cap);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;
+    if ((f_v & 1) == 0) {  // rows as f_v/2 16-byte pieces
+        const int q2 = f_v >> 1;
+        const int64_t n2 = V * q2;
+        const bool magic = n2 < ((int64_t)1 << 32);
+        const double2* src = reinterpret_cast<const double2*>(node_feat);
+        double2* dst = reinterpret_cast<double2*>(xv);
+        for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += stride * U) {
+            double2 x[U];
+#pragma unroll
+            for (int u = 0; u < U; ++u) {
+                const int64_t e = e0 + stride * u;
+                if (e < n2) {
+                    const int64_t i = magic ? (int64_t)__umulhi((unsigned)e, fv_magic) : e / q2;
+                    x[u] = __ldg(src + (int64_t)__ldg(l2g + i) * q2 + (e - i * q2));
+                }
+            }
+#pragma unroll
+            for (int u = 0; u < U; ++u)
+                if (e0 + stride * u < n2) __stcs(dst + e0 + stride * u, x[u]);
+        }
+    } else {
+        const int64_t n = V * f_v;
+        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+            const int64_t i = e / f_v;
+            __stcs(xv + e, __ldg(node_feat + (int64_t)l2g[i] * f_v + (e - i * f_v)));
+        }
+    }
+}
+
+// f_e == 2: erec[2g] = the edge's two features, erec[2g+1].x = its label
+__global__ void __launch_bounds__(256) k_gather_edges_rec(const uint4* __restrict__ erec,
+                                                          const int32_t* __restrict__ e_gid,
+                                                          const int32_t* __restrict__ E_ptr, int64_t e_cap,
+                                                          const int32_t* __restrict__ ticket,
+                                                          uint4* __restrict__ ye, uint8_t* __restrict__ lab) {
+    if (ticket[1] != 0) return;
+    const int64_t E = min((int64_t)*E_ptr, e_cap);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    constexpr int U = 4;
+    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < E; t0 += stride * U) {
+        int32_t g[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) g[u] = t0 + stride * u < E ? __ldg(e_gid + t0 + stride * u) : 0;
+        uint4 f[U];
+        uint32_t lb[U];
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            if (t0 + stride * u < E) {
+                f[u] = __ldg(erec + 2 * (int64_t)g[u]);
+                lb[u] = __ldg(&erec[2 * (int64_t)g[u] + 1].x);
+            }
+        }
+#pragma unroll
+        for (int u = 0; u < U; ++u) {
+            const int64_t t = t0 + stride * u;
+            if (t < E) {
+                __stcs(ye + t, f[u]);
+                lab[t] = (uint8_t)lb[u];
+            }
+        }
+    }
+}
+
+__global__ void __launch_bounds__(256) k_gather_edges(const double* __restrict__ edge_feat, int32_t f_e,
+                                                      const uint8_t* __restrict__ labels,
+                                                      const int32_t* __restrict__ e_gid,
+                                                      const int32_t* __restrict__ E_ptr, int64_t e_cap,
+                                                      const int32_t* __restrict__ ticket,
+                                                      double* __restrict__ ye, uint8_t* __restrict__ lab) {
+    if (ticket[1] != 0) return;
+    const int64_t E = min((int64_t)*E_ptr, e_cap);
+    const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < E; t += stride) {
+        const int64_t g = e_gid[t];
+        lab[t] = __ldg(labels + g);
+        for (int c = 0; c < f_e; ++c) __stcs(ye + t * f_e + c, __ldg(edge_feat + g * f_e + c));
+    }
+}
+
+__global__ void k_build_erec(const uint4* __restrict__ edge_feat, const uint8_t* __restrict__ labels,
+                             int64_t m, uint4* __restrict__ erec) {
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < m; e += (int64_t)gridDim.x * blockDim.x) {
+        erec[2 * e] = edge_feat[e];
+        erec[2 * e + 1] = make_uint4(labels[e], 0u, 0u, 0u);
+    }
+}
+
+void build_edge_records(DevGraph& g, cudaStream_t st) {
+    g.erec.release();
+    if (g.f_e != 2 || g.nnz == 0) return;
+    g.erec.reserve((size_t)2 * g.nnz);
+    k_build_erec<<<1184, 256, 0, st>>>(reinterpret_cast<const uint4*>(g.edge_feat.p), g.labels.p, g.nnz,
+                                        g.erec.p);
+    HGS_CUDA(cudaGetLastError());
 }
 
 __global__ void k_finalize(const int64_t* __restrict__ batch_off, int32_t k, int32_t R,
@@ -708,10 +787,22 @@ int extract_blocks_per_sm(size_t smem, bool packed) {
 }
 
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st) {
-    const size_t smem = (size_t)8 * pp.set_cap * sizeof(int32_t);
-    if (smem > 48 * 1024)
-        HGS_CUDA(cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_pack<<<grid, 256, smem, st>>>(pp);
+    k_pack<<<grid, 256, 0, st>>>(pp);
+    HGS_CUDA(cudaGetLastError());
+}
+
+void launch_gather_packed(int sms, const PackParams& pp, const uint4* erec, const int32_t* V_ptr,
+                          const int32_t* E_ptr, cudaStream_t st) {
+    const dim3 grid(sms * 8), block(256);
+    if (pp.f_v > 0)
+        k_gather_nodes<<<grid, block, 0, st>>>(pp.node_feat, pp.f_v, pp.fv_magic, pp.l2g, V_ptr, pp.v_cap,
+                                               pp.ticket, pp.xv);
+    if (erec)
+        k_gather_edges_rec<<<grid, block, 0, st>>>(erec, pp.e_gid, E_ptr, pp.e_cap, pp.ticket,
+                                                   reinterpret_cast<uint4*>(pp.ye), pp.lab);
+    else
+        k_gather_edges<<<grid, block, 0, st>>>(pp.edge_feat, pp.f_e, pp.labels, pp.e_gid, E_ptr, pp.e_cap,
+                                               pp.ticket, pp.ye, pp.lab);
     HGS_CUDA(cudaGetLastError());
 }
 

@@ -79,6 +79,7 @@ struct DevGraph {
     // features (gather_features)
     DevBuf<double> node_feat, edge_feat;
     DevBuf<uint8_t> labels;
+    DevBuf<uint4> erec;      // f_e == 2: per edge 32 B = {features, label}: one sector per gathered edge
     int32_t f_v = 0, f_e = 0;
     bool has_features = false;
     cudaStream_t stream = nullptr;  // ingest stream

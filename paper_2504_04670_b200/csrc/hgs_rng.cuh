@@ -83,11 +83,38 @@ HGS_HD uint64_t mod_by_recip(uint64_t x, uint64_t m, uint64_t recip) {
 
 HGS_HD uint64_t recip_of(uint64_t m) { return ~0ULL / m; }
 
+// x mod m for 1 <= m < 2^31 (any walk degree): only the low 32 bits of the
+// quotient estimate are needed, since x - q*m < 2m < 2^32. Bits 64..95 of
+// x*recip from four 32-bit partial products.
+HGS_HD uint32_t mod_small(uint64_t x, uint32_t m, uint64_t recip) {
+    const uint32_t xl = (uint32_t)x, xh = (uint32_t)(x >> 32);
+    const uint32_t rl = (uint32_t)recip, rh = (uint32_t)(recip >> 32);
+    const uint64_t t1 = (uint64_t)xl * rh, t2 = (uint64_t)xh * rl;
+#if defined(__CUDA_ARCH__)
+    const uint32_t t0 = __umulhi(xl, rl);
+#else
+    const uint32_t t0 = (uint32_t)(((uint64_t)xl * rl) >> 32);
+#endif
+    const uint64_t mid = (uint64_t)t0 + (uint32_t)t1 + (uint32_t)t2;
+    const uint32_t q = xh * rh + (uint32_t)(t1 >> 32) + (uint32_t)(t2 >> 32) + (uint32_t)(mid >> 32);
+    const uint32_t r = xl - q * m;
+    return r >= m ? r - m : r;
+}
+
 // Reject-threshold of Rng::bounded: (0 - m) % m == 2^64 mod m < m. Only
 // needs evaluating when the draw itself is < m (probability < m / 2^64).
+#if defined(__CUDA_ARCH__)
+__device__ __noinline__ bool rejected_slow(uint64_t x, uint64_t m, uint64_t recip) {
+    return x < mod_by_recip(0ULL - m, m, recip);
+}
+#endif
 HGS_HD bool rejected(uint64_t x, uint64_t m, uint64_t recip) {
     if (x >= m) return false;
+#if defined(__CUDA_ARCH__)
+    return rejected_slow(x, m, recip);
+#else
     return x < mod_by_recip(0ULL - m, m, recip);
+#endif
 }
 
 HGS_HD void philox4x32_10(uint32_t c[4], uint32_t k0, uint32_t k1) {

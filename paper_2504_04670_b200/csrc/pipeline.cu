@@ -236,10 +236,14 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         const int64_t pgrid = split ? (Rc + 7) / 8 : std::min<int64_t>((int64_t)sm_count(g.device) * 8, (Rc + 7) / 8);
         launch_pack((int)std::max<int64_t>(pgrid, 1), pp, pst);
         ++s->launches;
-        if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
     }
+    if (R > 0 && cfg.gather) {
+        launch_gather_packed(sm_count(g.device), pp, g.erec.p, s->root_voff.p + R, s->root_eoff.p + R, pst);
+        s->launches += 2;
+    }
+    if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
     if (R == 0 && s->profiled)
-        for (int i = 2; i <= 4; ++i) HGS_CUDA(cudaEventRecord(s->ev[i], st));
+        for (int i = 2; i <= 3; ++i) HGS_CUDA(cudaEventRecord(s->ev[i], st));
     launch_finalize(in.batch_off, (int32_t)k, (int32_t)R, s->root_voff.p, s->root_eoff.p, s->batch_voff.p,
                     s->batch_eoff.p, s->comp_off.p, pst);
     ++s->launches;

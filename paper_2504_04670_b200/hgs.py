@@ -18,7 +18,7 @@ from dataclasses import dataclass
 import numpy as np
 
 _PKG = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(_PKG, "lib", "libhgs.so")
+LIB_PATH = os.environ.get("HGS_LIB") or os.path.join(_PKG, "lib", "libhgs.so")
 
 HGS_OK, HGS_EINVAL, HGS_ECUDA, HGS_ERANGE = 0, 1, 2, 3
 RNG_XOSHIRO, RNG_PHILOX = 0, 1

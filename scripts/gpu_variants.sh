@@ -1,0 +1,5 @@
+# time K2 (and the call) for every lib/variants/*.so plus the default build
+for so in paper_2504_04670_b200/lib/libhgs.so paper_2504_04670_b200/lib/variants/*.so; do
+  echo "== $so"
+  HGS_LIB=$so timeout 300 python scripts/prof.py --calls 3 2>&1 | grep -E "call 2|unprofiled"
+done

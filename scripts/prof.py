@@ -36,3 +36,11 @@ for i in range(a.calls + 2):
     S.wait()
     ts.append(ev[0].elapsed_time(ev[1]))
 print("unprofiled call ms:", " ".join(f"{t:.3f}" for t in ts), file=sys.stderr)
+# calibration: write-only and copy streams on this box
+buf = torch.empty(1 << 30, dtype=torch.uint8, device="cuda"); buf2 = torch.empty_like(buf)
+for name, fn, nbytes in [("memset 1GiB", lambda: buf.zero_(), 1 << 30), ("copy 1GiB", lambda: buf2.copy_(buf), 2 << 30)]:
+    fn(); torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record(); [fn() for _ in range(5)]; e1.record(); torch.cuda.synchronize()
+    ms = e0.elapsed_time(e1) / 5
+    print(f"{name}: {ms:.3f} ms = {nbytes / ms / 1e6:.0f} GB/s", file=sys.stderr)
