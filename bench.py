@@ -59,10 +59,36 @@ def peaks():
     return 6650.0, "fallback"
 
 
+WORKLOAD_TEXT = {
+    "C1": "C1: synthetic 10k-hit event (reference CPU-runnable case)",
+    "C2": "C2: synthetic TrackML-shaped event",
+    "C3": "C3: C2's event, 512 minibatches per step (trainer root/seed streams over consecutive epochs)"
+          " sharded over the GPUs",
+    "C4": "C4: high-pileup synthetic event (windowed generator)",
+    "C5": "C5: multi-event epoch, C2-shaped events resident in HBM, every minibatch of one epoch"
+          " (trainer root/seed streams, device-derived seeds)",
+}
+
+
+def set_workload(name, world):
+    """BASELINE.json configs: C2 (default, weak scaling: 64 minibatches per
+    GPU), C3 (512 minibatches per step split over the GPUs: strong scaling),
+    C1 / C4 (4096-root minibatches on a ~1M-hit event), per GPU."""
+    global WORKLOAD, K_BATCHES, BATCH, DEPTH, FANOUT
+    from paper_2504_04670_b200 import workload as W
+    WORKLOAD = name
+    K_BATCHES, BATCH, DEPTH, FANOUT = W.SHAPE[name]
+    if name == "C3":
+        K_BATCHES = max(1, K_BATCHES // world)
+    if name == "C5":
+        K_BATCHES, BATCH, DEPTH, FANOUT = W.SHAPE["C2"]
+
+
 def config_dict(n_gpus, ev):
-    return {"workload": "C2: synthetic TrackML-shaped event, n=%d hits / m=%d edges, %d minibatches"
+    return {"workload": "%s, n=%d hits / m=%d edges, %d minibatches"
             " x %d seeds per GPU, %d-hop, fanout %d, symmetrized walk, per-root xoshiro streams,"
-            " bulk_shadow+gather_features" % (ev.n, ev.m, K_BATCHES, BATCH, DEPTH, FANOUT),
+            " bulk_shadow+gather_features" % (WORKLOAD_TEXT[WORKLOAD], ev.n, ev.m, K_BATCHES, BATCH, DEPTH,
+                                               FANOUT),
             "minibatches_per_step_per_gpu": K_BATCHES, "roots_per_minibatch": BATCH,
             "depth": DEPTH, "fanout": FANOUT, "parallelism": f"shard{n_gpus} (replicated graph)",
             "l2": "flushed (512 MiB memset) before every timed step"}
@@ -160,10 +186,10 @@ def run_reference(args, world, rank):
     value = nb * len(times) / total
     line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
+            "scaling": "strong" if WORKLOAD == "C3" else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "impl": "reference", "config": config_dict(world, ev),
             "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                             "sample": f"{nb} minibatches x {BATCH} roots of C2 per step, "
+                             "sample": f"{nb} minibatches x {BATCH} roots of {WORKLOAD} per step, "
                                        f"bulk_shadow+gather_features, batch-sharded over "
                                        f"{threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
@@ -209,8 +235,14 @@ def run_gpu(args, world, rank, local_rank):
     nsteps = args.warmup + args.steps
     host_in, dev_in = [], []
     for i in range(nsteps):
-        rep = rank * nsteps + i
-        roots, boff, seeds = W.bench_roots(ev.n, BATCH, K_BATCHES, seed=1, rep=rep)
+        if WORKLOAD == "C3":  # the step's 512 trainer-order minibatches, this rank's slice
+            total_k = W.SHAPE["C3"][0]
+            roots, boff, seeds, _ = W.trainer_roots(ev.n, BATCH, total_k, seed=1, epoch0=8 * i)
+            b0, b1 = rank * K_BATCHES, (rank + 1) * K_BATCHES
+            r0, r1 = int(boff[b0]), int(boff[b1])
+            roots, seeds, boff = roots[r0:r1], seeds[r0:r1], boff[b0:b1 + 1] - r0
+        else:
+            roots, boff, seeds = W.bench_roots(ev.n, BATCH, K_BATCHES, seed=1, rep=rank * nsteps + i)
         host_in.append((roots, boff, seeds))
         dev_in.append((torch.from_numpy(roots.astype(np.int32)).to(dev),
                        torch.from_numpy(boff).to(dev),
@@ -281,14 +313,16 @@ def run_gpu(args, world, rank, local_rank):
             ps[:] = seeds.view(np.int64)
             hin.append((pr, pb, ps.view(np.uint64)))
         e2e_s, h2d, d2h = [], 0, 0
-        for i in range(nsteps):
+        e2e_n = min(nsteps, args.e2e_steps)
+        e2e_warm = args.warmup if e2e_n == nsteps else 1
+        for i in range(e2e_n):
             pr, pb, ps = hin[i]
             torch.cuda.synchronize()
             t1 = time.perf_counter()
             c = S.bulk_shadow(pr, pb, ps, **cfg)
             S.to_host(hout)
             t2 = time.perf_counter()
-            if i >= args.warmup:
+            if i >= e2e_warm:
                 e2e_s.append(t2 - t1)
                 h2d = pr.nbytes + pb.nbytes + ps.nbytes
                 d2h = (4 * 2 * (c.k + 1) + 4 * (c.R + c.k) + 4 * c.V + 4 * c.R + 12 * c.E
@@ -326,7 +360,7 @@ def run_gpu(args, world, rank, local_rank):
     line = {
         "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
-        "scaling": "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
+        "scaling": "strong" if WORKLOAD == "C3" else "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": config_dict(world, ev),
         "edges_per_s": world * edges / (total_ms / 1e3),
         "roofline": {"bound": "hbm", "kernel": {"expand": "k_expand", "extract": "k_extract",
@@ -341,7 +375,7 @@ def run_gpu(args, world, rank, local_rank):
                                     for n in stage_bytes}},
         "gpu_launches": int(launches),
         "clocks": clk.summary(),
-        "e2e": {"value": mb / e2e_total if e2e_total > 0 else None, "unit": UNIT,
+        "e2e": {"value": world * K_BATCHES * len(e2e_s) / e2e_total if e2e_total > 0 else None, "unit": UNIT,
                 "h2d_bytes_per_step": int(h2d), "d2h_bytes_per_step": int(d2h),
                 "path": "hgs_sample_run (host int64 inputs, pinned) + hgs_sample_copy_to_host "
                         "(all outputs, pinned), wall clock"},
@@ -352,10 +386,80 @@ def run_gpu(args, world, rank, local_rank):
         nb = 2 * threads
         t, V, E, kind = cpu_sample_time(ev, nb, threads)
         line["cpu_baseline"] = {"value": nb / t, "unit": UNIT, "cores": threads, "kind": kind,
-                                "sample": f"{nb} minibatches x {BATCH} roots of C2, "
+                                "sample": f"{nb} minibatches x {BATCH} roots of {WORKLOAD}, "
                                           f"bulk_shadow+gather_features, batch-sharded over "
                                           f"{threads} host threads ({t:.1f}s wall)"}
     print(json.dumps(line), flush=True)
+
+
+def run_epoch(args, world, rank, local_rank):
+    """C5: this rank's share of the events (ordinals rank, rank+world, ...)
+    resident on its GPU; one step = one full epoch of sampling over them
+    (EpochSampler: host shuffles + int32 root uploads + device calls, all
+    inside the timed region). Timed with CUDA events (max over ranks)."""
+    import concurrent.futures as cf
+
+    import torch
+    import torch.distributed as dist
+    from paper_2504_04670_b200 import epoch as EP, hgs, workload as W
+
+    dev = torch.device("cuda", local_rank)
+    torch.cuda.set_device(dev)
+    mine = list(range(rank, args.events, world))
+    t0 = time.time()
+    with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
+        evs = list(ex.map(lambda e: W.generate_event(**W.GEN["C2"], event_id=e), mine))
+    log(f"[rank {rank}] {len(evs)} events generated in {time.time() - t0:.1f}s")
+    graphs = [hgs.Graph(e.rp, e.ci, device=local_rank).attach_features(e.node_feat, e.edge_feat, e.labels)
+              for e in evs]
+    n_v = sum(e.n for e in evs)
+    del evs
+    es = EP.EpochSampler(graphs, batch_size=BATCH, bulk_batches=K_BATCHES, depth=DEPTH, fanout=FANOUT, seed=1)
+    for i in range(args.warmup):
+        es.epoch(1000 + i, max_batches_per_event=K_BATCHES)
+    torch.cuda.synchronize()
+    if world > 1:
+        dist.barrier()
+    ms, tots = [], []
+    with Clocks(local_rank) as clk:
+        for j in range(args.steps):
+            e0 = torch.cuda.Event(enable_timing=True)
+            e0.record()
+            for s in es.streams:
+                s.wait_event(e0)
+            tot = es.epoch(j)
+            ends = []
+            for s in es.streams:
+                e1 = torch.cuda.Event(enable_timing=True)
+                e1.record(s)
+                ends.append(e1)
+            torch.cuda.synchronize()
+            ms.append(max(e0.elapsed_time(e1) for e1 in ends))
+            tots.append(tot)
+    total_ms = float(sum(ms))
+    mbs = sum(t["minibatches"] for t in tots)
+    if world > 1:
+        t = torch.tensor([total_ms, float(mbs)], device=dev, dtype=torch.float64)
+        dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
+        dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
+        total_ms, mbs = float(t[0]), int(t[1])
+    if rank != 0:
+        return
+    line = {"metric": METRIC, "value": mbs / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
+            "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
+            "data": "synthetic",
+            "config": {"workload": WORKLOAD_TEXT["C5"] + f": {args.events} events (generate_event C2 preset,"
+                                   f" event_id 0..{args.events - 1}), b={BATCH}, bulk_batches={K_BATCHES},"
+                                   f" {DEPTH}-hop, fanout {FANOUT}, with gather",
+                       "events": args.events, "events_per_gpu": len(graphs), "vertices_per_gpu": n_v,
+                       "minibatches_per_epoch": mbs // args.steps, "parallelism": f"events split over {world} GPU(s)",
+                       "l2": "not flushed (the epoch streams ~100 events, far beyond L2)"},
+            "edges_per_s": world * sum(t["E"] for t in tots) / (total_ms / 1e3),
+            "calls_per_epoch": tots[0]["calls"], "gpu_launches": None, "clocks": clk.summary(),
+            "e2e": None}
+    print(json.dumps(line), flush=True)
+    es.close()
 
 
 def main():
@@ -365,11 +469,19 @@ def main():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--events", type=int, default=100, help="C5: events in the epoch (split over ranks)")
+    ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"],
+                    help="BASELINE.json config (C2 = the headline line)")
+    ap.add_argument("--e2e-steps", type=int, default=None,
+                    help="steps of the host-buffer e2e leg (default: all; fewer for C3/C4)")
     args = ap.parse_args()
     args.warmup = max(args.warmup, 3) if args.impl == "ours" else args.warmup
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    set_workload(args.workload, world)
+    if args.e2e_steps is None:
+        args.e2e_steps = args.warmup + args.steps if args.workload in ("C1", "C2") else 3
     if args.impl == "reference":
         run_reference(args, world, rank)
         return
@@ -379,7 +491,10 @@ def main():
         torch.cuda.set_device(local_rank)
         dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
     try:
-        run_gpu(args, world, rank, local_rank)
+        if args.workload == "C5":
+            run_epoch(args, world, rank, local_rank)
+        else:
+            run_gpu(args, world, rank, local_rank)
     finally:
         if world > 1:
             import torch.distributed as dist

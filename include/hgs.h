@@ -142,6 +142,10 @@ int hgs_graph_gather(hgs_graph* g, const int64_t* l2g, int64_t V, const int64_t*
 /* stream: a cudaStream_t (NULL = a stream owned by the handle). */
 int hgs_sample_create(hgs_graph* g, void* stream, hgs_sample** out);
 int hgs_sample_destroy(hgs_sample* s);
+/* Re-bind a sample handle (its workspace and stream) to another graph on the
+ * same device, e.g. to sample many resident events with a few handles. The
+ * last run must have been waited for. */
+int hgs_sample_bind(hgs_sample* s, hgs_graph* g);
 
 /* bulk_shadow over batches given as flat roots[batch_off[n_batches]] with
  * batch_off[0] = 0 (host pointers). seeds[R]: per-root stream seeds
@@ -159,6 +163,28 @@ int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
 int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d_roots,
                           const int64_t* d_batch_off, int64_t n_roots, int64_t n_batches,
                           const uint64_t* d_seeds);
+/* Per-root stream seeds derived on the device instead of
+ * an uploaded seed array: the seed of flat root r, in batch bi at position
+ * pos = r - batch_off[bi], is
+ *     Rng::derive(seed, {path[0..path_len), batch_base + bi, pos})
+ * (rng.cpp:76-85). The trainer's root_stream_seed (trainer.cpp:200-206) is
+ * path = {0x73616d706c, epoch, event_ordinal} with batch_base = index of the
+ * call's first batch in the epoch; the bench-sampling protocol
+ * (cli.cpp:404-408) is path = {0x7374726d, k, rep}, batch_base = 0. */
+typedef struct {
+    uint64_t seed;
+    uint64_t path[6];
+    int32_t path_len;   /* 0..6 */
+    int64_t batch_base;
+} hgs_seed_spec;
+
+/* hgs_sample_run_device with seeds from a hgs_seed_spec (no seed array). */
+int hgs_sample_run_device_spec(hgs_sample* s, const hgs_config* cfg, const int32_t* d_roots,
+                               const int64_t* d_batch_off, int64_t n_roots, int64_t n_batches,
+                               const hgs_seed_spec* spec);
+/* The same seeds on the host: out[batch_off[n_batches]] (host arrays). */
+int hgs_derive_seeds(const hgs_seed_spec* spec, const int64_t* batch_off, int64_t n_batches, uint64_t* out);
+
 /* Wait for the last run; fills counts[0..3] = R, k, V, E (may be NULL). */
 int hgs_sample_wait(hgs_sample* s, int64_t* counts);
 int hgs_sample_copy_to_host(hgs_sample* s, const hgs_host_out* out);

@@ -19,6 +19,12 @@ typedef struct hgs_event hgs_event;
 int hgs_generate_event(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
                        int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,
                        uint64_t seed, uint64_t event_id, hgs_event** out);
+/* The scalable variant (not in the reference): false-edge candidates from a
+ * phi window of half-width phi_window (reference: 0.45), so the work per hit
+ * stays constant as layers fill up (~1M hits). */
+int hgs_generate_event_windowed(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
+                                int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,
+                                uint64_t seed, uint64_t event_id, double phi_window, hgs_event** out);
 /* sizes: [0]=n [1]=m [2]=f_v [3]=f_e */
 void hgs_event_sizes(const hgs_event* ev, int64_t* sizes);
 /* row_ptr[n+1], col_idx[m] (make_edge_id_matrix CSR), node_feat[n*f_v],

@@ -226,6 +226,9 @@ struct GenConfig {
 // data.cpp:124-268), with a phi-window sweep instead of the all-pairs
 // candidate scan so million-hit events are feasible. Bit-identical output.
 EventGraph generate_event(const GenConfig& cfg, std::uint64_t event_id);
+// Scalable variant (not in the reference): false-edge candidates from a phi
+// window of half-width phi_window (the reference's is 0.45); see eventgen.cpp.
+EventGraph generate_event_windowed(const GenConfig& cfg, std::uint64_t event_id, double phi_window);
 
 // ---- sampler ----------------------------------------------------------------------
 struct SamplerConfig {

@@ -294,6 +294,15 @@ int hgs_sample_create(hgs_graph* g, void* stream, hgs_sample** out) {
     });
 }
 
+int hgs_sample_bind(hgs_sample* s, hgs_graph* g) {
+    return guarded([&] {
+        if (!s || !g) fail(HGS_EINVAL, "hgs_sample_bind: null argument");
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_bind: run not waited for");
+        if (g->g.device != s->graph->g.device) fail(HGS_EINVAL, "hgs_sample_bind: graph is on another device");
+        s->graph = g;
+    });
+}
+
 int hgs_sample_destroy(hgs_sample* s) {
     return guarded([&] {
         if (!s) return;
@@ -390,6 +399,50 @@ int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d
         // remembered for a possible capacity re-run in hgs_sample_wait
         s->last_in = in;
         s->last_cfg = *cfg;
+    });
+}
+
+int hgs_sample_run_device_spec(hgs_sample* s, const hgs_config* cfg, const int32_t* d_roots,
+                               const int64_t* d_batch_off, int64_t n_roots, int64_t n_batches,
+                               const hgs_seed_spec* spec) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        if (!spec) fail(HGS_EINVAL, "hgs_sample_run_device_spec: null seed spec");
+        if (spec->path_len < 0 || spec->path_len > 6)
+            fail(HGS_EINVAL, "hgs_sample_run_device_spec: path_len must be in [0, 6]");
+        if (n_roots > 0 && n_batches < 1)
+            fail(HGS_EINVAL, "hgs_sample_run_device_spec: roots without batches");
+        validate_cfg(cfg);
+        DevGraph& g = s->graph->g;
+        check_square(g, cfg->symmetrize);
+        HGS_CUDA(cudaSetDevice(g.device));
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_run_device_spec: previous run not waited for");
+        s->last_spec = *spec;
+        CallInputs in;
+        in.roots32 = d_roots;
+        in.batch_off = d_batch_off;
+        in.seeds = nullptr;
+        in.spec = &s->last_spec;
+        in.R = n_roots;
+        in.k = n_batches;
+        sample_enqueue(s, *cfg, in);
+        s->last_in = in;
+        s->last_cfg = *cfg;
+    });
+}
+
+int hgs_derive_seeds(const hgs_seed_spec* spec, const int64_t* batch_off, int64_t n_batches, uint64_t* out) {
+    return guarded([&] {
+        if (!spec || (n_batches > 0 && (!batch_off || !out))) fail(HGS_EINVAL, "hgs_derive_seeds: null argument");
+        if (spec->path_len < 0 || spec->path_len > 6) fail(HGS_EINVAL, "hgs_derive_seeds: path_len must be in [0, 6]");
+        uint64_t path[8];
+        for (int i = 0; i < spec->path_len; ++i) path[i] = spec->path[i];
+        for (int64_t b = 0; b < n_batches; ++b)
+            for (int64_t r = batch_off[b]; r < batch_off[b + 1]; ++r) {
+                path[spec->path_len] = (uint64_t)(spec->batch_base + b);
+                path[spec->path_len + 1] = (uint64_t)(r - batch_off[b]);
+                out[r] = derive_seed(spec->seed, path, spec->path_len + 2);
+            }
     });
 }
 

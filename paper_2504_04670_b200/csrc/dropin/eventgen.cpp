@@ -59,7 +59,17 @@ struct Cand {
 }  // namespace
 
 EventGraph generate_event(const GenConfig& cfg, std::uint64_t event_id) {
+    return generate_event_windowed(cfg, event_id, kPhiWindow);
+}
+
+// phi_window == kPhiWindow: the reference generator. A narrower window is the
+// scalable variant for events the reference cannot generate (SURVEY.md §8(d)
+// C4: ~1M hits): the candidate count per inner hit, and with it the cost,
+// stays constant as the layers fill up, so generation is linear in the hits.
+EventGraph generate_event_windowed(const GenConfig& cfg, std::uint64_t event_id, double phi_window) {
     cfg.validate();
+    if (!(phi_window > 0.0 && phi_window <= kPhiWindow))
+        fail_invalid("generate_event: phi window must be in (0, 0.45]");
     Rng rng(Rng::derive(cfg.seed, {0x6576656e74ULL, event_id}));
     const double r_outer = kInnerRadius + kLayerGap * static_cast<double>(cfg.detector_layers - 1);
 
@@ -128,7 +138,7 @@ EventGraph generate_event(const GenConfig& cfg, std::uint64_t event_id) {
         };
         for (Index u : inner) {
             const Hit& hu = hits[u];
-            const double w = kPhiWindow + kSlack;
+            const double w = phi_window + kSlack;
             std::pair<std::ptrdiff_t, std::ptrdiff_t> iv[3] = {
                 index_range(hu.phi - w, hu.phi + w),
                 index_range(hu.phi - w + kTwoPi, hu.phi + w + kTwoPi),
@@ -140,7 +150,7 @@ EventGraph generate_event(const GenConfig& cfg, std::uint64_t event_id) {
                     const Index v = outer[static_cast<std::size_t>(i)];
                     const Hit& hv = hits[v];
                     if (hu.track >= 0 && hu.track == hv.track) continue;
-                    if (std::abs(wrap(hv.phi - hu.phi)) > kPhiWindow) continue;
+                    if (std::abs(wrap(hv.phi - hu.phi)) > phi_window) continue;
                     if (std::abs(hv.z - hu.z) > kZWindow) continue;
                     cand.push_back({static_cast<std::int32_t>(u), static_cast<std::int32_t>(v), distance(hu, hv)});
                 }

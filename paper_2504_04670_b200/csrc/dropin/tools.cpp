@@ -22,6 +22,13 @@ const char* hgs_tools_last_error(void) { return g_tools_err.c_str(); }
 int hgs_generate_event(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
                        int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,
                        uint64_t seed, uint64_t event_id, hgs_event** out) {
+    return hgs_generate_event_windowed(n_tracks, hits_min, hits_max, layers, noise_hits, false_edge_factor, f_v,
+                                       f_e, seed, event_id, 0.45, out);
+}
+
+int hgs_generate_event_windowed(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
+                                int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,
+                                uint64_t seed, uint64_t event_id, double phi_window, hgs_event** out) {
     try {
         hitgnn::GenConfig cfg;
         cfg.n_tracks = n_tracks;
@@ -34,7 +41,7 @@ int hgs_generate_event(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int
         cfg.f_e = f_e;
         cfg.seed = seed;
         auto* e = new hgs_event;
-        e->ev = hitgnn::generate_event(cfg, event_id);
+        e->ev = hitgnn::generate_event_windowed(cfg, event_id, phi_window);
         e->a = hitgnn::make_edge_id_matrix(e->ev);
         *out = e;
         return 0;

@@ -159,8 +159,23 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
         p.tcount[r] = 0;
         return;
     }
+    uint64_t seed;
+    if (p.seeds) seed = p.seeds[r];
+    else {  // Rng::derive(seed, {path..., batch_base + bi, pos}) (rng.cpp:76-85)
+        int lo = 0, hi = p.k - 1;  // batch of r: largest bi with batch_off[bi] <= r
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(p.batch_off + mid) <= r) lo = mid; else hi = mid - 1;
+        }
+        uint64_t path[8];
+        for (int i = 0; i < 6; ++i) path[i] = p.spec.path[i];
+        const int len = p.spec.path_len;
+        path[len] = (uint64_t)(p.spec.batch_base + lo);
+        path[len + 1] = (uint64_t)(r - __ldg(p.batch_off + lo));
+        seed = derive_seed(p.spec.seed, path, len + 2);
+    }
     RootStream<PHILOX> rs;
-    rs.init(p.seeds[r], (!PHILOX && p.state) ? p.state + 4 * (size_t)r : nullptr);
+    rs.init(seed, (!PHILOX && p.state) ? p.state + 4 * (size_t)r : nullptr);
     uint32_t ndec = (PHILOX && p.state) ? (uint32_t)p.state[r] : 0u;
     const uint32_t dec0 = ndec;
 

@@ -96,6 +96,7 @@ struct CallInputs {
     const int64_t* batch_off = nullptr;
     const uint64_t* seeds = nullptr;
     const uint64_t* state = nullptr;
+    const hgs_seed_spec* spec = nullptr;  // seeds derived on the device when seeds == nullptr
     int64_t R = 0, k = 0;
 };
 void graph_ensure_recip(DevGraph& g, int32_t max_m);
@@ -212,6 +213,7 @@ struct hgs_sample {
     hgs::DevBuf<int64_t> roots64, boff64;
     hgs::DevBuf<uint64_t> seeds, rng_state;
     hgs::CallInputs last_in;
+    hgs_seed_spec last_spec{};
     hgs_config last_cfg{};
     // expand scratch
     hgs::DevBuf<int32_t> touched, tcount, level_counts;

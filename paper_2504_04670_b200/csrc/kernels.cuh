@@ -24,6 +24,9 @@ struct ExpandParams {
     const int64_t* __restrict__ roots64;
     const uint64_t* __restrict__ seeds;
     const uint64_t* __restrict__ state;   // nullable: resume states
+    const int64_t* __restrict__ batch_off;  // for device-derived seeds (seeds == nullptr)
+    int32_t k;
+    hgs_seed_spec spec;
     int32_t r0, R, depth, fanout, n;     // roots [r0, R) of the call
     int64_t stride;
     int32_t cache_entries;                // (b,deg) entries cached per lane in smem

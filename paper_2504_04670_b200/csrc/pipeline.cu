@@ -150,6 +150,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     ep.w_rp = walk.rp.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
     ep.neg_row = (!cfg.symmetrize && !seq_walk && g.has_neg) ? g.neg_row.p : nullptr;
     ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
+    ep.batch_off = in.batch_off; ep.k = (int32_t)k;
+    if (in.spec) ep.spec = *in.spec;
     ep.depth = (int32_t)cfg.depth;
     ep.fanout = (int32_t)std::min<int64_t>(cfg.fanout, 1 << 30);
     ep.n = (int32_t)g.n_rows; ep.stride = c.max_t; ep.cache_entries = (int32_t)c.cache_entries;

@@ -32,6 +32,7 @@ EXPORTS = [
     "hgs_sample_create", "hgs_sample_destroy", "hgs_sample_run", "hgs_sample_run_device",
     "hgs_sample_wait", "hgs_sample_copy_to_host", "hgs_sample_device_views",
     "hgs_sample_kernel_times", "hgs_sample_stats", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
+    "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind",
 ]
 
 
@@ -63,6 +64,42 @@ class DeviceViews(C.Structure):
                                             "level_counts")] + [("touched_stride", C.c_int64)]
 
 
+class SeedSpec(C.Structure):
+    """hgs_seed_spec: per-root seed = derive(seed, path + [batch_base + bi, pos])."""
+    _fields_ = [("seed", C.c_uint64), ("path", C.c_uint64 * 6), ("path_len", C.c_int32),
+                ("batch_base", C.c_int64)]
+
+    @classmethod
+    def make(cls, seed: int, path, batch_base: int = 0) -> "SeedSpec":
+        path = [int(x) for x in path]
+        if len(path) > 6:
+            raise SamplerError("seed path longer than 6")
+        arr = (C.c_uint64 * 6)(*(path + [0] * (6 - len(path))))
+        return cls(seed, arr, len(path), batch_base)
+
+
+# Stream prefixes of the reference: trainer root streams (trainer.cpp:22,
+# 200-206: {kStreamSample, epoch, event}) and bench-sampling (cli.cpp:404-408).
+STREAM_SAMPLE = 0x73616D706C
+STREAM_BENCH = 0x7374726D
+
+
+def trainer_seed_spec(seed: int, epoch: int, event_ordinal: int, batch_base: int = 0) -> SeedSpec:
+    return SeedSpec.make(seed, [STREAM_SAMPLE, epoch, event_ordinal], batch_base)
+
+
+def bench_seed_spec(seed: int, k: int, rep: int) -> SeedSpec:
+    return SeedSpec.make(seed, [STREAM_BENCH, k, rep], 0)
+
+
+def derive_seeds(spec: SeedSpec, batch_off) -> np.ndarray:
+    """Host copy of the device-derived seeds (hgs_derive_seeds)."""
+    b = np.ascontiguousarray(batch_off, np.int64)
+    out = np.zeros(int(b[-1]) if len(b) else 0, np.uint64)
+    _check(lib().hgs_derive_seeds(C.byref(spec), _p(b), len(b) - 1, _p(out)))
+    return out
+
+
 _lib_cache: C.CDLL | None = None
 
 
@@ -90,6 +127,9 @@ def lib() -> C.CDLL:
         L.hgs_sample_run.argtypes = [vp, C.POINTER(Config), vp, vp, i64, vp, vp]
         L.hgs_sample_run_device.argtypes = [vp, C.POINTER(Config), vp, vp, i64, i64, vp]
         L.hgs_sample_wait.argtypes = [vp, vp]
+        L.hgs_sample_run_device_spec.argtypes = [vp, C.POINTER(Config), vp, vp, i64, i64, C.POINTER(SeedSpec)]
+        L.hgs_derive_seeds.argtypes = [C.POINTER(SeedSpec), vp, i64, vp]
+        L.hgs_sample_bind.argtypes = [vp, vp]
         L.hgs_sample_copy_to_host.argtypes = [vp, C.POINTER(HostOut)]
         L.hgs_sample_device_views.argtypes = [vp, C.POINTER(DeviceViews)]
         L.hgs_sample_kernel_times.argtypes = [vp, vp]
@@ -239,6 +279,20 @@ class Sampler:
         _check(lib().hgs_sample_run_device(self._h, C.byref(c), C.c_void_p(d_roots),
                                            C.c_void_p(d_batch_off), n_roots, n_batches,
                                            C.c_void_p(d_seeds)))
+
+    def bind(self, graph: "Graph") -> None:
+        """Re-bind this workspace to another graph on the same device."""
+        _check(lib().hgs_sample_bind(self._h, graph._h))
+        self.graph = graph
+
+    def run_device_spec(self, d_roots: int, d_batch_off: int, n_roots: int, n_batches: int,
+                        spec: SeedSpec, **cfg) -> None:
+        """Enqueue with device roots/offsets; per-root seeds derived on the device."""
+        c = self.config(**cfg)
+        self.gathered = bool(c.gather)
+        _check(lib().hgs_sample_run_device_spec(self._h, C.byref(c), C.c_void_p(d_roots),
+                                                C.c_void_p(d_batch_off), n_roots, n_batches,
+                                                C.byref(spec)))
 
     def wait(self) -> SampleCounts:
         a = np.zeros(4, np.int64)

@@ -5,6 +5,7 @@ trainer's seed streams (trainer.cpp:195-206)."""
 from __future__ import annotations
 
 import ctypes as C
+import hashlib
 import os
 from dataclasses import dataclass
 
@@ -21,9 +22,17 @@ GEN = {
                f_v=6, f_e=2, seed=1),
     "C2": dict(n_tracks=13000, hits_min=7, hits_max=10, layers=12, noise=10000,
                false_factor=14.5, f_v=6, f_e=2, seed=1),
+    # C4 "high-pileup ~1M hits / ~15M edges": 8.5x C2's hits per layer. The
+    # reference generator is quadratic in hits per layer (data.cpp:193-221);
+    # this preset uses the windowed variant with C2's candidate density
+    # (phi window scaled by the inverse hit density), so it is linear.
+    "C4": dict(n_tracks=110000, hits_min=7, hits_max=10, layers=12, noise=85000,
+               false_factor=17.5, f_v=6, f_e=2, seed=1, phi_window=0.45 * 23000 / 195000),
 }
+GEN["C3"] = GEN["C2"]
 # sampler shapes: (batches k, roots per batch b, depth d, fanout s)
-SHAPE = {"C1": (16, 256, 2, 6), "C2": (64, 1024, 3, 6), "C3": (512, 1024, 3, 6)}
+SHAPE = {"C1": (16, 256, 2, 6), "C2": (64, 1024, 3, 6), "C3": (512, 1024, 3, 6), "C4": (16, 4096, 3, 6),
+         "C5": (64, 1024, 3, 6)}
 
 _tools: C.CDLL | None = None
 
@@ -38,6 +47,9 @@ def tools() -> C.CDLL:
         vp = C.c_void_p
         L.hgs_generate_event.argtypes = [C.c_int64] * 5 + [C.c_double, C.c_int64, C.c_int64,
                                                            C.c_uint64, C.c_uint64, C.POINTER(vp)]
+        L.hgs_generate_event_windowed.argtypes = [C.c_int64] * 5 + [C.c_double, C.c_int64, C.c_int64,
+                                                                    C.c_uint64, C.c_uint64, C.c_double,
+                                                                    C.POINTER(vp)]
         L.hgs_event_sizes.argtypes = [vp, vp]
         L.hgs_event_copy.argtypes = [vp] * 6
         L.hgs_event_free.argtypes = [vp]
@@ -64,11 +76,13 @@ class Event:
 
 
 def generate_event(n_tracks=1100, hits_min=7, hits_max=10, layers=12, noise=650,
-                   false_factor=11.0, f_v=6, f_e=2, seed=1, event_id=0) -> Event:
+                   false_factor=11.0, f_v=6, f_e=2, seed=1, event_id=0, phi_window=0.45) -> Event:
+    """generate_event (data.cpp:124-268); phi_window < 0.45 selects the
+    scalable windowed variant (not in the reference)."""
     L = tools()
     h = C.c_void_p()
-    if L.hgs_generate_event(n_tracks, hits_min, hits_max, layers, noise, false_factor, f_v, f_e,
-                            seed, event_id, C.byref(h)) != 0:
+    if L.hgs_generate_event_windowed(n_tracks, hits_min, hits_max, layers, noise, false_factor, f_v, f_e,
+                                     seed, event_id, phi_window, C.byref(h)) != 0:
         raise ValueError(L.hgs_tools_last_error().decode())
     sz = np.zeros(4, np.int64)
     L.hgs_event_sizes(h, sz.ctypes.data)
@@ -83,7 +97,27 @@ def generate_event(n_tracks=1100, hits_min=7, hits_max=10, layers=12, noise=650,
 
 
 def preset_event(name: str, event_id: int = 0) -> Event:
-    return generate_event(**GEN[name], event_id=event_id)
+    """The preset's event. Large presets (C4: ~1-2 min to generate) are cached
+    as .npz under $HGS_EVENT_CACHE (default /tmp/hgs_events): a convenience
+    for repeated runs on one box, never needed for correctness or timing."""
+    cfg = GEN[name]
+    if cfg["n_tracks"] < 50000:
+        return generate_event(**cfg, event_id=event_id)
+    d = os.environ.get("HGS_EVENT_CACHE", "/tmp/hgs_events")
+    key = "_".join(f"{k}{v}" for k, v in sorted(cfg.items())) + f"_e{event_id}"
+    path = os.path.join(d, f"{name}_{hashlib.sha1(key.encode()).hexdigest()[:12]}.npz")
+    if os.path.exists(path):
+        z = np.load(path)
+        return Event(n=int(z["n"]), rp=z["rp"], ci=z["ci"], node_feat=z["nf"], edge_feat=z["ef"],
+                     labels=z["lab"])
+    ev = generate_event(**cfg, event_id=event_id)
+    try:
+        os.makedirs(d, exist_ok=True)
+        np.savez(path + ".tmp.npz", n=ev.n, rp=ev.rp, ci=ev.ci, nf=ev.node_feat, ef=ev.edge_feat, lab=ev.labels)
+        os.replace(path + ".tmp.npz", path)
+    except OSError:
+        pass
+    return ev
 
 
 def epoch_root_batches(n: int, b: int, rng_seed: int) -> list[np.ndarray]:
@@ -99,6 +133,35 @@ def derive_grid(seed: int, prefix, k: int, b: int) -> np.ndarray:
     out = np.zeros(k * b, np.uint64)
     tools().hgs_derive_grid(seed, pre.ctypes.data, len(pre), k, b, out.ctypes.data)
     return out
+
+
+STREAM_ROOTS, STREAM_SAMPLE = 0x726F6F7473, 0x73616D706C  # trainer.cpp:21-22
+
+
+def trainer_epoch_batches(n: int, b: int, seed: int, epoch: int, event: int = 0):
+    """Trainer::epoch_minibatch's roots for one (epoch, event) (trainer.cpp:433-437):
+    epoch_root_batches(n, b, roots_rng(seed, epoch, event))."""
+    return epoch_root_batches(n, b, hgs.derive(seed, [STREAM_ROOTS, epoch, event]))
+
+
+def trainer_roots(n: int, b: int, k: int, seed: int = 1, epoch0: int = 0, event: int = 0):
+    """k minibatches in the trainer's order over consecutive epochs epoch0,
+    epoch0+1, ... of one event (C3: 512 minibatches of 1024 roots need ~5
+    epochs of a 120k-hit event). Seeds are root_stream_seed(seed, epoch,
+    event, batch, pos) (trainer.cpp:200-206). Returns roots, batch offsets,
+    seeds and the (epoch, batch) of every minibatch."""
+    roots, seeds, ids = [], [], []
+    epoch = epoch0
+    while len(ids) < k:
+        batches = trainer_epoch_batches(n, b, seed, epoch, event)
+        take = min(len(batches), k - len(ids))
+        roots.extend(batches[:take])
+        seeds.append(derive_grid(seed, [STREAM_SAMPLE, epoch, event], take, len(batches[0])))
+        ids.extend((epoch, bi) for bi in range(take))
+        epoch += 1
+    boff = np.zeros(k + 1, np.int64)
+    boff[1:] = np.cumsum([len(x) for x in roots])
+    return np.concatenate(roots).astype(np.int64), boff, np.concatenate(seeds), ids
 
 
 def bench_roots(n: int, b: int, k: int, seed: int = 1, rep: int = 0):

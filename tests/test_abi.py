@@ -65,6 +65,22 @@ def test_host_helpers_match_oracle():
         assert [f"{int(x):08x}" for x in hgs.philox4x32_10(ctr, key)] == out
 
 
+def test_seed_spec_matches_reference_streams():
+    """hgs_derive_seeds = the reference's per-root stream seeds: the trainer's
+    root_stream_seed (trainer.cpp:200-206) and bench-sampling (cli.cpp:404-408),
+    restated by the oracle's derive (pinned to the reference KATs)."""
+    from paper_2504_04670_b200 import hgs
+    boff = np.array([0, 3, 3, 7, 12], np.int64)
+    for spec, pre, base in [(hgs.trainer_seed_spec(7, 2, 5, batch_base=10), [0x73616D706C, 2, 5], 10),
+                            (hgs.bench_seed_spec(1, 64, 3), [0x7374726D, 64, 3], 0)]:
+        got = hgs.derive_seeds(spec, boff)
+        exp = [O.derive(spec.seed, pre + [base + b, r - boff[b]])
+               for b in range(len(boff) - 1) for r in range(boff[b], boff[b + 1])]
+        assert [int(x) for x in got] == exp
+    with pytest.raises(hgs.SamplerError):
+        hgs.SeedSpec.make(1, [1] * 7)
+
+
 @pytest.mark.skipif(has_gpu(), reason="checks the no-GPU failure path")
 def test_compute_fails_loudly_without_gpu():
     from paper_2504_04670_b200 import hgs

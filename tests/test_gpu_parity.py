@@ -293,6 +293,61 @@ def test_device_pointer_entry_point():
     assert st_["V"] == ref.V and st_["E"] == ref.E
 
 
+@pytest.mark.parametrize("rng", [0, 1])
+def test_device_derived_seeds(rng):
+    """hgs_sample_run_device_spec: per-root seeds derived inside K1 from a
+    stream spec give the same subgraphs as uploading the host-derived seeds
+    (bench-sampling and trainer streams, batch_base offsets, ragged batches)."""
+    import torch
+    H = hgs()
+    g = random_graph(4000, 40000, 21)
+    rs = np.random.default_rng(3)
+    sizes = [100, 37, 0, 64, 1]
+    roots = np.concatenate([rs.permutation(4000)[:s] for s in sizes]).astype(np.int64)
+    boff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    G = H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels)
+    S = H.Sampler(G)
+    dr = torch.from_numpy(roots.astype(np.int32)).cuda()
+    db = torch.from_numpy(boff).cuda()
+    for spec in (H.bench_seed_spec(1, 5, 2), H.trainer_seed_spec(9, 1, 4, batch_base=17)):
+        seeds = H.derive_seeds(spec, boff)
+        kw = dict(rng=rng, depth=3, fanout=5, gather=True)
+        S.run_device_spec(dr.data_ptr(), db.data_ptr(), len(roots), len(sizes), spec, **kw)
+        S.wait()
+        dev = S.to_host()
+        ref = O.bulk_shadow(g, roots, boff, seeds, **kw)
+        assert_same(dev, ref, True)
+
+
+def test_epoch_sampler_matches_trainer_streams():
+    """EpochSampler (C5 path): several resident events, every minibatch of an
+    epoch in trainer order (trainer.cpp:433-459) with device-derived
+    root_stream_seed streams, chunked over two handles; each chunk equals the
+    oracle's bulk_shadow on the same roots and host-derived trainer seeds."""
+    from paper_2504_04670_b200 import epoch as EP, workload as W
+    H = hgs()
+    graphs_o = [random_graph(n, 8 * n, 30 + n) for n in (700, 1300, 500)]
+    graphs = [H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels) for g in graphs_o]
+    es = EP.EpochSampler(graphs, batch_size=64, bulk_batches=3, depth=3, fanout=4, seed=11, gather=True)
+    seen = []
+
+    def check(ch):
+        g = graphs_o[ch.event_ordinal]
+        batches = W.trainer_epoch_batches(g.n, 64, 11, 2, ch.event_ordinal)[ch.batch_base:ch.batch_base + ch.n_batches]
+        roots = np.concatenate(batches).astype(np.int64)
+        boff = np.concatenate([[0], np.cumsum([len(b) for b in batches])]).astype(np.int64)
+        spec = H.trainer_seed_spec(11, 2, ch.event_ordinal, batch_base=ch.batch_base)
+        ref = O.bulk_shadow(g, roots, boff, H.derive_seeds(spec, boff), depth=3, fanout=4, gather=True)
+        assert_same(ch.sampler.to_host(), ref, True)
+        seen.append((ch.event_ordinal, ch.batch_base))
+
+    tot = es.epoch(2, on_chunk=check)
+    es.close()
+    exp = sum((g.n // 64 + 2) // 3 for g in graphs_o)
+    assert tot["calls"] == exp == len(seen)
+    assert tot["minibatches"] == sum(g.n // 64 for g in graphs_o)
+
+
 def test_multi_handle_sharding_matches_single_call():
     """Two sample handles on one graph (as two ranks would be): the shard union
     equals the single call, batch for batch."""
