@@ -80,6 +80,10 @@ typedef struct {
  * support (zeros dropped, negatives rejected; sampler.cpp:161). The two
  * differ only when A stores explicit zeros or negative values. */
 #define HGS_FLAG_SEQ_WALK 1
+/* Keep a copy of every root's BFS-order touched list (K2 overwrites the
+ * working copy with the sorted set) for hgs_sample_copy_frontiers: the
+ * FrontierObserver hook of bulk_shadow (sampler.cpp:149-158, 186). */
+#define HGS_FLAG_KEEP_FRONTIERS 2
 
 /* Host destinations for hgs_sample_copy_to_host (any pointer may be NULL). */
 typedef struct {
@@ -184,6 +188,13 @@ int hgs_sample_run_device_spec(hgs_sample* s, const hgs_config* cfg, const int32
                                const hgs_seed_spec* spec);
 /* The same seeds on the host: out[batch_off[n_batches]] (host arrays). */
 int hgs_derive_seeds(const hgs_seed_spec* spec, const int64_t* batch_off, int64_t n_batches, uint64_t* out);
+
+/* Frontiers of the last run made with HGS_FLAG_KEEP_FRONTIERS (host arrays):
+ * touched[R*stride] = per root its root then the chosen vertices of levels
+ * 1..d in the reference's BFS order (touched[r*stride + i], i < tcount[r]),
+ * level_counts[R*(depth+1)] = rows per level. *stride receives the stride. */
+int hgs_sample_copy_frontiers(hgs_sample* s, int32_t* touched, int32_t* tcount, int32_t* level_counts,
+                              int64_t* stride);
 
 /* Wait for the last run; fills counts[0..3] = R, k, V, E (may be NULL). */
 int hgs_sample_wait(hgs_sample* s, int64_t* counts);

@@ -42,6 +42,19 @@ int64_t hgs_epoch_root_batches(int64_t n, int64_t batch_size, uint64_t rng_seed,
 void hgs_derive_grid(uint64_t seed, const uint64_t* prefix, int32_t prefix_len, int64_t k,
                      int64_t b, uint64_t* seeds);
 
+/* The drop-in hitgnn::bulk_shadow (GPU) with a FrontierObserver recording
+ * each level's FrontierSet; arrays per level: which = 0 Q col_idx, 1 F
+ * row_ptr, 2 F col_idx, 3 P row_ptr, 4 P col_idx (int64), 5 P values (f64).
+ * rng: 0 PerRootChoiceSource, 1 PhiloxChoiceSource. values NULL = edge ids. */
+typedef struct hgs_frontiers hgs_frontiers;
+int hgs_tools_frontiers(int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                        const double* values, const int64_t* roots, const int64_t* batch_off, int64_t n_batches,
+                        const uint64_t* seeds, int32_t rng, int64_t depth, int64_t fanout, int32_t symmetrize,
+                        hgs_frontiers** out);
+int64_t hgs_tools_frontiers_levels(const hgs_frontiers* f);
+int64_t hgs_tools_frontier_array(const hgs_frontiers* f, int64_t level, int32_t which, void* out);
+void hgs_tools_frontiers_free(hgs_frontiers* f);
+
 #ifdef __cplusplus
 }
 #endif

@@ -304,6 +304,7 @@ private:
     int device_ = 0;
     std::vector<double> values_;  // non-id values of a general A (may be empty)
     bool ids_ = true;
+    std::unique_ptr<CsrMatrix> host_a_;  // host copy of A for FrontierObserver's P
 };
 
 }  // namespace gpu

@@ -116,6 +116,8 @@ def _ref() -> C.CDLL:
         lib.ref_result_level_size.restype = C.c_int64
         lib.ref_result_level_size.argtypes = [_vp, C.c_int64]
         lib.ref_result_level_copy.argtypes = [_vp, C.c_int64, _i64p]
+        lib.ref_result_level_array.restype = C.c_int64
+        lib.ref_result_level_array.argtypes = [_vp, C.c_int64, C.c_int, _vp]
         lib.ref_result_free.argtypes = [_vp]
         lib.ref_time_sample.restype = C.c_double
         lib.ref_time_sample.argtypes = [C.c_int64, _vp, _vp, _vp, C.c_int64, _vp, C.c_int64, _vp,
@@ -168,6 +170,7 @@ class Sample:
     level_counts: np.ndarray | None = None
     touched: np.ndarray | None = None
     level_q: list = field(default_factory=list)
+    levels: list = field(default_factory=list)  # ref mode 2: per level dict of Q/F/P arrays
 
     @property
     def V(self) -> int:
@@ -180,6 +183,10 @@ class Sample:
 
 class SamplerError(ValueError):
     pass
+
+
+# FrontierSet arrays per level (sampler.hpp:52-58), in shim/tools order
+FRONTIER_ARRAYS = ["q_ci", "f_rp", "f_ci", "p_rp", "p_ci", "p_val"]
 
 
 def _c(a, dt):
@@ -247,6 +254,14 @@ def bulk_shadow(g: Graph, roots, batch_off, seeds, *, rng=RNG_XOSHIRO, depth=3, 
         q = np.zeros(lib.ref_result_level_size(h, lvl), np.int64)
         lib.ref_result_level_copy(h, lvl, q)
         s.level_q.append(q)
+        if mode == 2:
+            d = {}
+            for which, name in enumerate(FRONTIER_ARRAYS):
+                n = lib.ref_result_level_array(h, lvl, which, None)
+                a = np.zeros(n, np.float64 if which == 5 else np.int64)
+                lib.ref_result_level_array(h, lvl, which, a.ctypes.data)
+                d[name] = a
+            s.levels.append(d)
     lib.ref_result_free(h)
     return s
 

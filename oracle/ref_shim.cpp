@@ -84,6 +84,9 @@ struct Result {
     std::vector<std::uint8_t> lab;
     std::vector<std::vector<std::int64_t>> level_q;  // observer: Q col ids per level
     std::vector<std::int64_t> level_f_nnz;
+    // observer, full: per level F (row_ptr, col_idx) and P (row_ptr, col_idx, values)
+    std::vector<std::vector<std::int64_t>> level_f_rp, level_f_ci, level_p_rp, level_p_ci;
+    std::vector<std::vector<double>> level_p_val;
 };
 
 void put_err(char* err, int len, const std::string& s) {
@@ -275,6 +278,11 @@ void* ref_bulk_shadow(std::int64_t n_rows, std::int64_t n_cols, const std::int64
                 obs = [&](R::Index, const R::FrontierSet& fs) {
                     res->level_q.push_back(fs.q.col_idx);
                     res->level_f_nnz.push_back(fs.f.nnz());
+                    res->level_f_rp.push_back(fs.f.row_ptr);
+                    res->level_f_ci.push_back(fs.f.col_idx);
+                    res->level_p_rp.push_back(fs.p.row_ptr);
+                    res->level_p_ci.push_back(fs.p.col_idx);
+                    res->level_p_val.push_back(fs.p.values);
                 };
             out = R::bulk_shadow(a, batches, cfg, *src, obs);
         }
@@ -317,6 +325,26 @@ std::int64_t ref_result_level_size(const void* h, std::int64_t level) {
 void ref_result_level_copy(const void* h, std::int64_t level, std::int64_t* out) {
     const auto& q = static_cast<const Result*>(h)->level_q[level];
     std::copy(q.begin(), q.end(), out);
+}
+// which: 0 Q col_idx, 1 F row_ptr, 2 F col_idx, 3 P row_ptr, 4 P col_idx
+// (int64), 5 P values (double). Returns the length; copies when out != null.
+std::int64_t ref_result_level_array(const void* h, std::int64_t level, int which, void* out) {
+    const auto* r = static_cast<const Result*>(h);
+    const std::vector<std::int64_t>* v = nullptr;
+    switch (which) {
+        case 0: v = &r->level_q[level]; break;
+        case 1: v = &r->level_f_rp[level]; break;
+        case 2: v = &r->level_f_ci[level]; break;
+        case 3: v = &r->level_p_rp[level]; break;
+        case 4: v = &r->level_p_ci[level]; break;
+        default: {
+            const auto& d = r->level_p_val[level];
+            if (out) std::copy(d.begin(), d.end(), static_cast<double*>(out));
+            return static_cast<std::int64_t>(d.size());
+        }
+    }
+    if (out) std::copy(v->begin(), v->end(), static_cast<std::int64_t*>(out));
+    return static_cast<std::int64_t>(v->size());
 }
 void ref_result_free(void* h) { delete static_cast<Result*>(h); }
 

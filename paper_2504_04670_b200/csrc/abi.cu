@@ -446,6 +446,28 @@ int hgs_derive_seeds(const hgs_seed_spec* spec, const int64_t* batch_off, int64_
     });
 }
 
+int hgs_sample_copy_frontiers(hgs_sample* s, int32_t* touched, int32_t* tcount, int32_t* level_counts,
+                              int64_t* stride) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_copy_frontiers: run not waited for");
+        if (!s->frontier_kept) fail(HGS_EINVAL, "hgs_sample_copy_frontiers: last run did not keep frontiers");
+        HGS_CUDA(cudaSetDevice(s->graph->g.device));
+        const size_t R = (size_t)s->R;
+        cudaStream_t st = s->stream;
+        if (stride) *stride = s->touched_stride;
+        if (touched && R)
+            HGS_CUDA(cudaMemcpyAsync(touched, s->frontier.p, sizeof(int32_t) * R * s->touched_stride,
+                                     cudaMemcpyDeviceToHost, st));
+        if (tcount && R)
+            HGS_CUDA(cudaMemcpyAsync(tcount, s->tcount.p, sizeof(int32_t) * R, cudaMemcpyDeviceToHost, st));
+        if (level_counts && R)
+            HGS_CUDA(cudaMemcpyAsync(level_counts, s->level_counts.p, sizeof(int32_t) * R * (s->depth + 1),
+                                     cudaMemcpyDeviceToHost, st));
+        HGS_CUDA(cudaStreamSynchronize(st));
+    });
+}
+
 int hgs_sample_wait(hgs_sample* s, int64_t* counts) {
     return guarded([&] {
         if (!s) fail(HGS_EINVAL, "hgs: null sample handle");

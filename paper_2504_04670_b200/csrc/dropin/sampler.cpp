@@ -46,11 +46,95 @@ bool values_are_ids(const CsrMatrix& a) {
 
 // Run one bulk call on a resident graph and materialise SampledBatch values.
 // values == nullptr: values are edge ids (gid + 1), as make_edge_id_matrix.
+// FrontierObserver (sampler.cpp:149-158, 186) from the device's frontiers:
+// per level l = 1..d, Q = the level's chosen vertices (one row each, roots in
+// order, BFS order within a root), F = per root the canonical set of the
+// root and everything touched so far, P = row_normalize(spgemm(Q_{l-1}, walk))
+// restated for one-hot rows: the walk row of the parent with zeros dropped,
+// each value divided by the row's sequential sum (sparse.cpp:78-144, 193-206).
+void emit_frontiers(hgs_graph* g, hgs_sample* s, const CsrMatrix& a, const std::vector<Index>& roots,
+                    const SamplerConfig& cfg, const FrontierObserver& observer) {
+    const std::size_t R = roots.size();
+    const Index d = cfg.depth;
+    int64_t stride = 0;
+    check(hgs_sample_copy_frontiers(s, nullptr, nullptr, nullptr, &stride));
+    std::vector<int32_t> touched(R * static_cast<std::size_t>(stride)), tcount(R),
+        lc(R * static_cast<std::size_t>(d + 1));
+    check(hgs_sample_copy_frontiers(s, touched.data(), tcount.data(), lc.data(), &stride));
+    CsrMatrix walk;
+    const CsrMatrix* w = &a;
+    if (cfg.symmetrize) {
+        int64_t info[8];
+        check(hgs_graph_info(g, info));
+        walk = CsrMatrix(a.n_rows, a.n_cols);
+        walk.col_idx.resize(static_cast<std::size_t>(info[3]));
+        check(hgs_graph_walk(g, 1, walk.row_ptr.data(), walk.col_idx.data()));
+        walk.values.assign(walk.col_idx.size(), 1.0);
+        w = &walk;
+    }
+    auto level_begin = [&](std::size_t r, Index l) {  // offset of level l in root r's list
+        Index off = 0;
+        for (Index j = 0; j < l; ++j) off += lc[r * (d + 1) + j];
+        return off;
+    };
+    for (Index level = 1; level <= d; ++level) {
+        FrontierSet fs;
+        // Q: the level's rows
+        Index nq = 0;
+        for (std::size_t r = 0; r < R; ++r) nq += lc[r * (d + 1) + level];
+        fs.q = CsrMatrix(nq, a.n_cols);
+        fs.q.col_idx.reserve(static_cast<std::size_t>(nq));
+        for (std::size_t r = 0; r < R; ++r) {
+            const Index b = level_begin(r, level), n = lc[r * (d + 1) + level];
+            for (Index i = 0; i < n; ++i) fs.q.col_idx.push_back(touched[r * stride + b + i]);
+        }
+        fs.q.values.assign(fs.q.col_idx.size(), 1.0);
+        for (Index i = 0; i < nq; ++i) fs.q.row_ptr[i + 1] = i + 1;
+        // F: root + touched through this level, canonical, values 1
+        fs.f = CsrMatrix(static_cast<Index>(R), a.n_cols);
+        for (std::size_t r = 0; r < R; ++r) {
+            const Index end = level_begin(r, level + 1);
+            std::vector<Index> row(touched.begin() + r * stride, touched.begin() + r * stride + end);
+            if (row.empty()) row.push_back(roots[r]);
+            std::sort(row.begin(), row.end());
+            row.erase(std::unique(row.begin(), row.end()), row.end());
+            fs.f.col_idx.insert(fs.f.col_idx.end(), row.begin(), row.end());
+            fs.f.row_ptr[r + 1] = static_cast<Index>(fs.f.col_idx.size());
+        }
+        fs.f.values.assign(fs.f.col_idx.size(), 1.0);
+        // P: one row per frontier row of level-1
+        Index np = 0;
+        for (std::size_t r = 0; r < R; ++r) np += lc[r * (d + 1) + level - 1];
+        fs.p = CsrMatrix(np, a.n_cols);
+        Index row = 0;
+        for (std::size_t r = 0; r < R; ++r) {
+            const Index b = level_begin(r, level - 1), n = lc[r * (d + 1) + level - 1];
+            for (Index i = 0; i < n; ++i, ++row) {
+                const Index v = touched[r * stride + b + i];
+                const std::size_t k0 = fs.p.col_idx.size();
+                double sum = 0.0;
+                for (Index k = w->row_ptr[v]; k < w->row_ptr[v + 1]; ++k) {
+                    const double x = w->values.empty() ? 1.0 : w->values[k];
+                    if (x == 0.0) continue;  // spgemm drops exact zeros
+                    fs.p.col_idx.push_back(w->col_idx[k]);
+                    fs.p.values.push_back(x);
+                    sum += x;
+                }
+                if (sum != 0.0)
+                    for (std::size_t k = k0; k < fs.p.values.size(); ++k) fs.p.values[k] /= sum;
+                fs.p.row_ptr[row + 1] = static_cast<Index>(fs.p.col_idx.size());
+            }
+        }
+        observer(level, fs);
+    }
+}
+
 std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
                                    const std::vector<std::vector<Index>>& batches,
                                    const SamplerConfig& cfg, ChoiceSource& choice, bool gather,
                                    const std::vector<double>* values, Index f_v, Index f_e,
-                                   bool seq_walk = false) {
+                                   bool seq_walk = false, const FrontierObserver* observer = nullptr,
+                                   const CsrMatrix* a_host = nullptr) {
     cfg.validate();
     auto* per_root = dynamic_cast<PerRootChoiceSource*>(&choice);
     auto* philox = dynamic_cast<PhiloxChoiceSource*>(&choice);
@@ -88,7 +172,7 @@ std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
     hc.symmetrize = cfg.symmetrize ? 1 : 0;
     hc.rng = philox ? HGS_RNG_PHILOX : HGS_RNG_XOSHIRO;
     hc.gather = gather ? 1 : 0;
-    hc.flags = seq_walk ? HGS_FLAG_SEQ_WALK : 0;
+    hc.flags = (seq_walk ? HGS_FLAG_SEQ_WALK : 0) | (observer ? HGS_FLAG_KEEP_FRONTIERS : 0);
     check(hgs_sample_run(s, &hc, roots.data(), boff.data(), static_cast<int64_t>(batches.size()),
                          seeds.data(), state_ptr));
     int64_t counts[4];
@@ -112,6 +196,7 @@ std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
     check(hgs_sample_copy_to_host(s, &o));
     if (per_root) per_root->advance(draws);
     else philox->advance(decisions);
+    if (observer) emit_frontiers(g, s, *a_host, roots, cfg, *observer);
 
     std::vector<SampledBatch> out(static_cast<std::size_t>(k));
     for (Index b = 0; b < k; ++b) {
@@ -143,14 +228,14 @@ std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
 std::vector<SampledBatch> bulk_shadow(const CsrMatrix& a, const std::vector<std::vector<Index>>& batches,
                                       const SamplerConfig& cfg, ChoiceSource& choice,
                                       const FrontierObserver& observer) {
-    if (observer) fail_invalid("bulk_shadow: FrontierObserver is not supported by the GPU sampler yet");
     cfg.validate();
     const bool ids = values_are_ids(a);
     GraphGuard g;
     g.g = upload_csr(a, 0, !ids);
     SampleGuard s;
     check(hgs_sample_create(g.g, nullptr, &s.s));
-    return run_bulk(g.g, s.s, batches, cfg, choice, false, ids ? nullptr : &a.values, 0, 0);
+    return run_bulk(g.g, s.s, batches, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, false,
+                    observer ? &observer : nullptr, &a);
 }
 
 SampledBatch shadow_reference(const CsrMatrix& a, std::span<const Index> roots,
@@ -248,6 +333,7 @@ namespace gpu {
 DeviceEvent::DeviceEvent(const EventGraph& event, int device) : device_(device) {
     const CsrMatrix a = make_edge_id_matrix(event);
     graph_ = upload_csr(a, device, false);
+    host_a_ = std::make_unique<CsrMatrix>(a);
     n_ = event.n;
     nnz_ = event.m();
     f_v_ = event.node_features.cols;
@@ -263,6 +349,7 @@ DeviceEvent::DeviceEvent(const CsrMatrix& a, int device) : device_(device) {
     ids_ = values_are_ids(a);
     if (!ids_) values_ = a.values;
     graph_ = upload_csr(a, device, !ids_);
+    host_a_ = std::make_unique<CsrMatrix>(a);
     n_ = a.n_rows;
     nnz_ = a.nnz();
     hgs_sample* s = nullptr;
@@ -278,10 +365,10 @@ DeviceEvent::~DeviceEvent() {
 std::vector<SampledBatch> DeviceEvent::bulk_shadow(const std::vector<std::vector<Index>>& batches,
                                                    const SamplerConfig& cfg, ChoiceSource& choice,
                                                    bool gather, const FrontierObserver& observer) {
-    if (observer) fail_invalid("bulk_shadow: FrontierObserver is not supported by the GPU sampler yet");
     if (gather && f_v_ == 0 && f_e_ == 0) fail_invalid("gather_features: no features attached to the graph");
     return run_bulk(static_cast<hgs_graph*>(graph_), static_cast<hgs_sample*>(sampler_), batches, cfg,
-                    choice, gather, ids_ ? nullptr : &values_, f_v_, f_e_);
+                    choice, gather, ids_ ? nullptr : &values_, f_v_, f_e_, false,
+                    observer ? &observer : nullptr, host_a_.get());
 }
 
 }  // namespace gpu

@@ -6,6 +6,11 @@
 #include "hitgnn/core.hpp"
 #include "../hgs_rng.cuh"
 
+struct hgs_frontiers {
+    std::vector<std::vector<int64_t>> a[5];  // q_ci, f_rp, f_ci, p_rp, p_ci per level
+    std::vector<std::vector<double>> p_val;
+};
+
 struct hgs_event {
     hitgnn::EventGraph ev;
     hitgnn::CsrMatrix a;
@@ -89,5 +94,68 @@ void hgs_derive_grid(uint64_t seed, const uint64_t* prefix, int32_t plen, int64_
             seeds[bi * b + pos] = hgs::derive_seed(seed, path.data(), plen + 2);
         }
 }
+
+// hitgnn::bulk_shadow (the GPU drop-in) with a FrontierObserver recording
+// every level's FrontierSet (sampler.hpp:52-58); per-root seeds, rng 0 =
+// PerRootChoiceSource, 1 = PhiloxChoiceSource.
+int hgs_tools_frontiers(int64_t n_rows, int64_t n_cols, const int64_t* rp, const int64_t* ci, const double* values,
+                        const int64_t* roots, const int64_t* batch_off, int64_t n_batches, const uint64_t* seeds,
+                        int32_t rng, int64_t depth, int64_t fanout, int32_t symmetrize, hgs_frontiers** out) {
+    try {
+        hitgnn::CsrMatrix a(n_rows, n_cols);
+        a.row_ptr.assign(rp, rp + n_rows + 1);
+        a.col_idx.assign(ci, ci + rp[n_rows]);
+        a.values.resize(a.col_idx.size());
+        for (size_t k = 0; k < a.values.size(); ++k) a.values[k] = values ? values[k] : double(k) + 1.0;
+        std::vector<std::vector<hitgnn::Index>> batches;
+        for (int64_t b = 0; b < n_batches; ++b) batches.emplace_back(roots + batch_off[b], roots + batch_off[b + 1]);
+        std::vector<uint64_t> sd(seeds, seeds + batch_off[n_batches]);
+        hitgnn::SamplerConfig cfg;
+        cfg.depth = depth;
+        cfg.fanout = fanout;
+        cfg.symmetrize = symmetrize != 0;
+        auto* f = new hgs_frontiers;
+        hitgnn::FrontierObserver obs = [&](hitgnn::Index, const hitgnn::FrontierSet& fs) {
+            f->a[0].push_back(fs.q.col_idx);
+            f->a[1].push_back(fs.f.row_ptr);
+            f->a[2].push_back(fs.f.col_idx);
+            f->a[3].push_back(fs.p.row_ptr);
+            f->a[4].push_back(fs.p.col_idx);
+            f->p_val.push_back(fs.p.values);
+        };
+        try {
+            if (rng == 1) {
+                hitgnn::PhiloxChoiceSource src(std::move(sd));
+                hitgnn::bulk_shadow(a, batches, cfg, src, obs);
+            } else {
+                hitgnn::PerRootChoiceSource src(std::move(sd));
+                hitgnn::bulk_shadow(a, batches, cfg, src, obs);
+            }
+        } catch (...) {
+            delete f;
+            throw;
+        }
+        *out = f;
+        return 0;
+    } catch (const std::exception& ex) {
+        g_tools_err = ex.what();
+        return 1;
+    }
+}
+
+int64_t hgs_tools_frontiers_levels(const hgs_frontiers* f) { return static_cast<int64_t>(f->p_val.size()); }
+
+int64_t hgs_tools_frontier_array(const hgs_frontiers* f, int64_t level, int32_t which, void* out) {
+    if (which == 5) {
+        const auto& d = f->p_val[level];
+        if (out) std::copy(d.begin(), d.end(), static_cast<double*>(out));
+        return static_cast<int64_t>(d.size());
+    }
+    const auto& v = f->a[which][level];
+    if (out) std::copy(v.begin(), v.end(), static_cast<int64_t*>(out));
+    return static_cast<int64_t>(v.size());
+}
+
+void hgs_tools_frontiers_free(hgs_frontiers* f) { delete f; }
 
 }  // extern "C"

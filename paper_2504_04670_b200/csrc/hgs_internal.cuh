@@ -217,6 +217,8 @@ struct hgs_sample {
     hgs_config last_cfg{};
     // expand scratch
     hgs::DevBuf<int32_t> touched, tcount, level_counts;
+    hgs::DevBuf<int32_t> frontier;  // BFS-order copy of touched (HGS_FLAG_KEEP_FRONTIERS)
+    bool frontier_kept = false;
     hgs::DevBuf<uint32_t> draws, decisions;
     int64_t touched_stride = 0;
     // extract scratch + offsets

@@ -217,6 +217,12 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         launch_expand(c.expand_threads, c.expand_smem, c.kmax, ep, cfg.rng == HGS_RNG_PHILOX, st);
         ++s->launches;
     }
+    s->frontier_kept = (cfg.flags & HGS_FLAG_KEEP_FRONTIERS) != 0;
+    if (s->frontier_kept && R > 0) {  // K2 sorts the touched lists in place
+        s->frontier.reserve((size_t)R * c.max_t);
+        HGS_CUDA(cudaMemcpyAsync(s->frontier.p, s->touched.p, sizeof(int32_t) * (size_t)R * c.max_t,
+                                 cudaMemcpyDeviceToDevice, st));
+    }
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[1], st));
     for (int64_t ci = 0; ci < nchunks; ++ci) {
         const int32_t r0 = (int32_t)(ci * chunk), r1 = (int32_t)std::min<int64_t>(R, r0 + chunk);

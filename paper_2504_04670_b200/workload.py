@@ -57,6 +57,13 @@ def tools() -> C.CDLL:
         L.hgs_epoch_root_batches.restype = C.c_int64
         L.hgs_epoch_root_batches.argtypes = [C.c_int64, C.c_int64, C.c_uint64, vp]
         L.hgs_derive_grid.argtypes = [C.c_uint64, vp, C.c_int32, C.c_int64, C.c_int64, vp]
+        L.hgs_tools_frontiers.argtypes = [C.c_int64, C.c_int64, vp, vp, vp, vp, vp, C.c_int64, vp, C.c_int32,
+                                          C.c_int64, C.c_int64, C.c_int32, C.POINTER(vp)]
+        L.hgs_tools_frontiers_levels.restype = C.c_int64
+        L.hgs_tools_frontiers_levels.argtypes = [vp]
+        L.hgs_tools_frontier_array.restype = C.c_int64
+        L.hgs_tools_frontier_array.argtypes = [vp, C.c_int64, C.c_int32, vp]
+        L.hgs_tools_frontiers_free.argtypes = [vp]
         _tools = L
     return _tools
 
@@ -94,6 +101,39 @@ def generate_event(n_tracks=1100, hits_min=7, hits_max=10, layers=12, noise=650,
                      ev.edge_feat.ctypes.data, ev.labels.ctypes.data)
     L.hgs_event_free(h)
     return ev
+
+
+FRONTIER_ARRAYS = ["q_ci", "f_rp", "f_ci", "p_rp", "p_ci", "p_val"]
+
+
+def dropin_frontiers(rp, ci, values, roots, batch_off, seeds, *, rng=0, depth=3, fanout=6,
+                     symmetrize=True, n_cols=None) -> list[dict]:
+    """The C++ drop-in hitgnn::bulk_shadow (GPU) with a FrontierObserver: per
+    level the FrontierSet's Q col_idx, F and P CSR arrays (sampler.hpp:52-58)."""
+    L = tools()
+    rp = np.ascontiguousarray(rp, np.int64)
+    ci = np.ascontiguousarray(ci, np.int64)
+    va = None if values is None else np.ascontiguousarray(values, np.float64)
+    r = np.ascontiguousarray(roots, np.int64)
+    b = np.ascontiguousarray(batch_off, np.int64)
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    n = len(rp) - 1
+    h = C.c_void_p()
+    if L.hgs_tools_frontiers(n, n if n_cols is None else n_cols, rp.ctypes.data, ci.ctypes.data,
+                             None if va is None else va.ctypes.data, r.ctypes.data, b.ctypes.data, len(b) - 1,
+                             sd.ctypes.data, rng, depth, fanout, int(symmetrize), C.byref(h)) != 0:
+        raise ValueError(L.hgs_tools_last_error().decode())
+    out = []
+    for lvl in range(L.hgs_tools_frontiers_levels(h)):
+        d = {}
+        for which, name in enumerate(FRONTIER_ARRAYS):
+            m = L.hgs_tools_frontier_array(h, lvl, which, None)
+            a = np.zeros(m, np.float64 if which == 5 else np.int64)
+            L.hgs_tools_frontier_array(h, lvl, which, a.ctypes.data)
+            d[name] = a
+        out.append(d)
+    L.hgs_tools_frontiers_free(h)
+    return out
 
 
 def preset_event(name: str, event_id: int = 0) -> Event:

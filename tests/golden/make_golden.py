@@ -112,7 +112,49 @@ def cases():
     return out
 
 
+def frontier_cases():
+    """FrontierObserver fixtures (sampler.hpp:52-58; sampler.cpp:149-158, 186):
+    the reference's per-level Q / F / P of small bulk calls."""
+    out = []
+    g = random_graph(300, 1500, 41)
+    rs = np.random.default_rng(41)
+    roots = np.concatenate([rs.permutation(300)[:20] for _ in range(3)]).astype(np.int64)
+    boff = np.array([0, 20, 40, 60], np.int64)
+    seeds = rs.integers(0, 2**63, 60, dtype=np.uint64)
+    out.append(dict(name="sym_xoshiro", g=g, roots=roots, boff=boff, seeds=seeds, depth=3, fanout=4, rng=0,
+                    sym=True))
+    out.append(dict(name="ids_philox", g=g, roots=roots, boff=boff, seeds=seeds, depth=3, fanout=3, rng=1,
+                    sym=False))
+    gz = random_graph(200, 1200, 42, values_kind="zeros")
+    out.append(dict(name="values_zeros", g=gz, roots=roots[:30] % 200, boff=np.array([0, 15, 30], np.int64),
+                    seeds=seeds[:30], depth=2, fanout=5, rng=0, sym=False))
+    return out
+
+
+def write_frontiers():
+    arrays, index = {}, []
+    for c in frontier_cases():
+        g = c["g"]
+        s = O.bulk_shadow(g, c["roots"], c["boff"], c["seeds"], rng=c["rng"], depth=c["depth"],
+                          fanout=c["fanout"], symmetrize=c["sym"], impl="ref", mode=2)
+        pre = c["name"] + "/"
+        arrays[pre + "rp"], arrays[pre + "ci"] = g.rp, g.ci
+        if g.values is not None:
+            arrays[pre + "values"] = g.values
+        arrays[pre + "roots"], arrays[pre + "boff"], arrays[pre + "seeds"] = c["roots"], c["boff"], c["seeds"]
+        index.append({"name": c["name"], "n": g.n, "depth": c["depth"], "fanout": c["fanout"], "rng": c["rng"],
+                      "sym": c["sym"], "values": g.values is not None,
+                      "levels": [{k: digest(v) for k, v in lv.items()} for lv in s.levels]})
+    np.savez_compressed(os.path.join(HERE, "frontiers.npz"), **arrays)
+    with open(os.path.join(HERE, "frontiers.json"), "w") as f:
+        json.dump(index, f, indent=1)
+    print("frontier fixtures written:", len(index))
+
+
 def main():
+    if "--frontiers" in sys.argv:
+        write_frontiers()
+        return
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built: run `make -f oracle/Makefile` where /root/reference exists")
     # ---- known answers
@@ -201,6 +243,7 @@ def main():
     with open(os.path.join(HERE, "c1.json"), "w") as f:
         json.dump(c1, f, indent=1)
     print("golden fixtures written:", len(index), "small cases;", len(c1["runs"]), "C1 runs")
+    write_frontiers()
 
 
 if __name__ == "__main__":

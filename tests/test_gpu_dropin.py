@@ -33,3 +33,30 @@ def test_dropin_against_oracle():
     print(res.stdout)
     assert res.returncode == 0, res.stdout + res.stderr
     assert "ALL OK" in res.stdout
+
+
+@pytest.mark.gpu
+def test_dropin_frontier_observer_matches_reference():
+    """hitgnn::bulk_shadow's FrontierObserver on the GPU drop-in (device
+    frontiers exported with HGS_FLAG_KEEP_FRONTIERS, Q/F/P materialised on
+    the host) reproduces the reference's per-level FrontierSet bit for bit:
+    digests of the reference's own Q, F and P (tests/golden/frontiers.json)."""
+    import hashlib
+    import json
+
+    import numpy as np
+    from paper_2504_04670_b200 import workload as W
+    d = os.path.join(ROOT, "tests", "golden")
+    with open(os.path.join(d, "frontiers.json")) as f:
+        idx = json.load(f)
+    z = np.load(os.path.join(d, "frontiers.npz"))
+    dg = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for c in idx:
+        p = c["name"] + "/"
+        lv = W.dropin_frontiers(z[p + "rp"], z[p + "ci"], z[p + "values"] if c["values"] else None,
+                                z[p + "roots"], z[p + "boff"], z[p + "seeds"], rng=c["rng"], depth=c["depth"],
+                                fanout=c["fanout"], symmetrize=c["sym"])
+        assert len(lv) == len(c["levels"]) == c["depth"]
+        for got, exp in zip(lv, c["levels"]):
+            for k in W.FRONTIER_ARRAYS:
+                assert dg(got[k]) == exp[k], (c["name"], k)

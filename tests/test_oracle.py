@@ -7,6 +7,8 @@
    (tests/test_sparse.cpp: induced_subgraph brute-force edge scan,
    symmetrize_pattern pattern property) and SPEC.md's known answers.
 """
+import os
+
 import numpy as np
 import pytest
 
@@ -243,3 +245,42 @@ def test_error_messages_match_reference():
     O.bulk_shadow(g, [1, 1], [0, 1, 2], np.zeros(2, np.uint64))
     with pytest.raises(O.SamplerError, match="depth must be >= 1"):
         O.bulk_shadow(g, [1], [0, 1], np.zeros(1, np.uint64), depth=0)
+
+
+def _frontier_cases():
+    import json
+    d = os.path.join(os.path.dirname(__file__), "golden")
+    with open(os.path.join(d, "frontiers.json")) as f:
+        idx = json.load(f)
+    z = np.load(os.path.join(d, "frontiers.npz"))
+    for c in idx:
+        p = c["name"] + "/"
+        g = O.Graph(n=c["n"], rp=z[p + "rp"], ci=z[p + "ci"], values=z[p + "values"] if c["values"] else None)
+        yield c, g, z[p + "roots"], z[p + "boff"], z[p + "seeds"]
+
+
+def test_oracle_frontiers_match_reference_observer():
+    """The oracle's per-root BFS touched lists, regrouped level by level in
+    root order, are the reference FrontierObserver's Q (sampler.cpp:164-186);
+    the union up to a level is its F. Checked against the reference's golden
+    digests (tests/golden/frontiers.json)."""
+    import hashlib
+    dg = lambda a: hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()  # noqa: E731
+    for c, g, roots, boff, seeds in _frontier_cases():
+        s = O.bulk_shadow(g, roots, boff, seeds, rng=c["rng"], depth=c["depth"], fanout=c["fanout"],
+                          symmetrize=c["sym"])
+        lc = s.level_counts
+        R = lc.shape[0]
+        starts = np.concatenate([[0], np.cumsum(lc.sum(axis=1))])
+        for lvl in range(1, c["depth"] + 1):
+            q, f_rp, f_ci = [], [0], []
+            for r in range(R):
+                t = s.touched[starts[r]:starts[r + 1]]
+                b = int(lc[r, :lvl].sum())
+                q.extend(t[b:b + lc[r, lvl]])
+                f_ci.extend(sorted(set(t[:b + lc[r, lvl]].tolist())))
+                f_rp.append(len(f_ci))
+            exp = c["levels"][lvl - 1]
+            assert dg(np.array(q, np.int64)) == exp["q_ci"], (c["name"], lvl)
+            assert dg(np.array(f_rp, np.int64)) == exp["f_rp"], (c["name"], lvl)
+            assert dg(np.array(f_ci, np.int64)) == exp["f_ci"], (c["name"], lvl)
