@@ -213,6 +213,23 @@ int hgs_sample_stats(hgs_sample* s, int64_t* stats, int32_t n);
 /* Number of kernels the last run launched (for gpu_launches accounting). */
 int hgs_sample_launches(hgs_sample* s, int64_t* n);
 
+/* ---- sample_rows ------------------------------------------------------------
+ * hitgnn::sample_rows (sampler.hpp:60-66, sampler.cpp:64-86) on the device,
+ * host arrays in and out. P: n_rows x n_cols CSR (values only checked for
+ * negatives, as the reference does). For every row with a nonempty support,
+ * k = min(s, |support|) distinct positions from choose(|support|, k) on
+ * stream row_streams[r] — begin_root(row_streams[r]) is announced only for
+ * nonempty rows, like the reference — sorted and mapped to the row's
+ * columns. Rows on one stream are decided in row order; streams run in
+ * parallel. seeds[n_streams]; rng_state as in hgs_sample_run (nullable).
+ * Outputs: out_off[n_rows+1] (offsets of each row's choices), out_cols[...],
+ * and per stream the RNG draws / choose calls consumed (nullable). Rows wider
+ * than 256 with s > 256 are HGS_ERANGE. */
+int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values, int64_t s, int32_t rng, const uint64_t* seeds, int64_t n_streams,
+                    const uint64_t* rng_state, const int64_t* row_streams, int64_t* out_off, int64_t* out_cols,
+                    uint32_t* draws, uint32_t* decisions);
+
 /* ---- RNG helpers (host, no GPU needed) -------------------------------------- */
 uint64_t hgs_derive(uint64_t seed, const uint64_t* path, int32_t len);
 void hgs_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

@@ -160,6 +160,7 @@ public:
     std::size_t size() const { return seeds_.size(); }
     const std::vector<std::uint64_t>& seeds() const { return seeds_; }
     bool fresh() const { return fresh_; }
+    std::size_t current() const { return current_; }
     // 4 state words per root (materialises pending device advances).
     std::vector<std::uint64_t> states();
     // Record that the device consumed draws[r] outputs of every stream r.
@@ -188,6 +189,7 @@ public:
     const std::vector<std::uint64_t>& seeds() const { return seeds_; }
     const std::vector<std::uint64_t>& decisions() const { return decisions_; }
     bool fresh() const { return fresh_; }
+    std::size_t current() const { return current_; }
     void advance(std::span<const std::uint32_t> decisions);
 
 private:
@@ -273,6 +275,9 @@ SampledBatch shadow_reference(const CsrMatrix& a, std::span<const Index> roots,
                               const SamplerConfig& cfg, ChoiceSource& choice);
 void gather_features(SampledBatch& batch, const EventGraph& event);
 CsrMatrix make_edge_id_matrix(const EventGraph& event);
+// sample_rows (reference sampler.hpp:60-66) on the GPU (hgs_sample_rows).
+std::vector<std::vector<Index>> sample_rows(const CsrMatrix& p, Index s, ChoiceSource& choice,
+                                            std::span<const Index> row_streams = {});
 std::vector<std::vector<Index>> epoch_root_batches(Index n_vertices, Index batch_size, Rng& rng);
 
 namespace gpu {

@@ -63,6 +63,9 @@ def _oracle() -> C.CDLL:
         lib.or_derive.argtypes = [C.c_uint64, _u64p, C.c_int]
         lib.or_choose_philox.restype = C.c_uint32
         lib.or_choose_philox.argtypes = [C.c_uint64, C.c_uint32, C.c_uint32, C.c_uint32, _u32p]
+        lib.or_choose_xoshiro.restype = C.c_uint32
+        lib.or_choose_xoshiro.argtypes = [_vp, C.c_uint32, C.c_uint32, _vp]
+        lib.or_xoshiro_seed.argtypes = [_vp, C.c_uint64]
         lib.or_philox4x32_10.argtypes = [_u32p, _u32p, _u32p]
         lib.or_epoch_root_batches.restype = C.c_int64
         lib.or_epoch_root_batches.argtypes = [C.c_int64, C.c_int64, C.c_uint64, _i64p]
@@ -278,6 +281,63 @@ def _alloc(k, R, V, E, f_v, f_e, gathered) -> Sample:
 
 # --------------------------------------------------------------------------
 # RNG helpers
+
+
+class _Xo(C.Structure):
+    _fields_ = [("s", C.c_uint64 * 4)]
+
+
+def sample_rows(rp, ci, s: int, seeds, row_streams=None, *, values=None, rng=RNG_XOSHIRO, state=None,
+                current: int = 0):
+    """sample_rows (sampler.cpp:64-86) over one ChoiceSource of per-root
+    streams (PerRootChoiceSource / PhiloxChoiceSource): returns (per-row choice
+    lists, per-stream draws-or-states, per-stream decisions)."""
+    lib = _oracle()
+    if s < 1:
+        raise SamplerError("sample_rows: s must be >= 1")
+    n_rows = len(rp) - 1
+    if row_streams is not None and len(row_streams) != n_rows:
+        raise SamplerError("sample_rows: row_streams length must equal row count")
+    if values is not None and np.any(np.asarray(values) < 0.0):
+        raise SamplerError("sample_rows: row with negative mass")
+    ns = len(seeds)
+    xs = []
+    for i in range(ns):
+        x = _Xo()
+        if state is not None and rng == RNG_XOSHIRO:
+            for w in range(4):
+                x.s[w] = int(state[4 * i + w])
+        else:
+            lib.or_xoshiro_seed(C.byref(x), C.c_uint64(int(seeds[i])))
+        xs.append(x)
+    dec = [int(state[i]) if (state is not None and rng != RNG_XOSHIRO) else 0 for i in range(ns)]
+    ndec = [0] * ns
+    out = []
+    buf = np.zeros(max(int(s), 1), np.uint32)
+    for r in range(n_rows):
+        b, e = int(rp[r]), int(rp[r + 1])
+        if e == b:
+            out.append([])
+            continue
+        if row_streams is not None:
+            st = int(row_streams[r])
+            if st < 0 or st >= ns:
+                raise SamplerError("PerRootChoiceSource: root ordinal out of range" if rng == RNG_XOSHIRO
+                                   else "PhiloxChoiceSource: root ordinal out of range")
+            current = st
+        if ns == 0:
+            raise SamplerError("PerRootChoiceSource: no streams configured" if rng == RNG_XOSHIRO
+                               else "PhiloxChoiceSource: no streams configured")
+        k = min(int(s), e - b)
+        if rng == RNG_XOSHIRO:
+            got = lib.or_choose_xoshiro(C.byref(xs[current]), e - b, k, buf.ctypes.data)
+        else:
+            got = lib.or_choose_philox(C.c_uint64(int(seeds[current])), dec[current], e - b, k, buf)
+            dec[current] += 1
+        ndec[current] += 1
+        out.append([int(ci[b + int(x)]) for x in buf[:got]])
+    states = np.array([x.s[w] for x in xs for w in range(4)], np.uint64)
+    return out, states, np.array(ndec, np.int64), current
 
 
 def derive(seed: int, path, impl="oracle") -> int:

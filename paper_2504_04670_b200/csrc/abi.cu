@@ -468,6 +468,95 @@ int hgs_sample_copy_frontiers(hgs_sample* s, int32_t* touched, int32_t* tcount, 
     });
 }
 
+int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                    const double* values, int64_t s, int32_t rng, const uint64_t* seeds, int64_t n_streams,
+                    const uint64_t* rng_state, const int64_t* row_streams, int64_t* out_off, int64_t* out_cols,
+                    uint32_t* draws, uint32_t* decisions) {
+    return guarded([&] {
+        // validation in the reference's order and words (sampler.cpp:67-72)
+        if (s < 1) fail(HGS_EINVAL, "sample_rows: s must be >= 1");
+        if (n_rows < 0 || !row_ptr || !out_off || !row_streams) fail(HGS_EINVAL, "hgs_sample_rows: null argument");
+        const int64_t nnz = row_ptr[n_rows];
+        if (values)
+            for (int64_t k = 0; k < nnz; ++k)
+                if (values[k] < 0.0) fail(HGS_EINVAL, "sample_rows: row with negative mass");
+        const char* src = rng == HGS_RNG_PHILOX ? "PhiloxChoiceSource" : "PerRootChoiceSource";
+        // choices per row, stream groups (counting sort by stream, row order kept)
+        out_off[0] = 0;
+        int64_t maxdeg = 0;
+        std::vector<int64_t> cnt((size_t)std::max<int64_t>(n_streams, 0) + 1, 0);
+        for (int64_t r = 0; r < n_rows; ++r) {
+            const int64_t deg = row_ptr[r + 1] - row_ptr[r];
+            out_off[r + 1] = out_off[r] + std::min<int64_t>(s, deg);
+            if (deg == 0) continue;
+            maxdeg = std::max(maxdeg, deg);
+            const int64_t st = row_streams[r];
+            if (n_streams == 0) fail(HGS_EINVAL, std::string(src) + ": no streams configured");
+            if (st < 0 || st >= n_streams) fail(HGS_EINVAL, std::string(src) + ": root ordinal out of range");
+            ++cnt[st + 1];
+        }
+        if (std::min<int64_t>(s, maxdeg) > 256)
+            fail(HGS_ERANGE, "hgs_sample_rows: more than 256 choices per row is not supported by this build");
+        if (maxdeg >= ((int64_t)1 << 31)) fail(HGS_ERANGE, "hgs_sample_rows: row too wide");
+        std::vector<int64_t> sptr{0}, sid, srows;
+        std::vector<int64_t> start(cnt.size(), 0);
+        for (size_t i = 1; i < cnt.size(); ++i) start[i] = start[i - 1] + cnt[i];
+        srows.resize((size_t)start.back());
+        std::vector<int64_t> fill(start.begin(), start.end() - 1);
+        for (int64_t r = 0; r < n_rows; ++r)
+            if (row_ptr[r + 1] > row_ptr[r]) srows[(size_t)fill[row_streams[r]]++] = r;
+        for (int64_t st = 0; st < n_streams; ++st)
+            if (cnt[st + 1]) { sid.push_back(st); sptr.push_back(start[st + 1]); }
+        const int64_t groups = (int64_t)sid.size();
+        std::vector<uint32_t> gd(groups), gc(groups);
+        if (groups > 0) {
+            HGS_CUDA(cudaSetDevice(device));
+            cudaStream_t st;
+            HGS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
+            DevBuf<int64_t> d_rp, d_ci, d_srows, d_sptr, d_sid, d_off, d_out;
+            DevBuf<uint64_t> d_seeds, d_state, d_recip;
+            DevBuf<uint32_t> d_draws, d_dec;
+            std::vector<uint64_t> recip((size_t)maxdeg + 1, 0);
+            for (int64_t m = 1; m <= maxdeg; ++m) recip[m] = recip_of((uint64_t)m);
+            auto up = [&](auto& buf, const auto* src_, size_t n) {
+                buf.reserve(std::max<size_t>(n, 1));
+                upload(buf.p, src_, n * sizeof(*src_), st);
+            };
+            up(d_rp, row_ptr, (size_t)n_rows + 1);
+            up(d_ci, col_idx, (size_t)nnz);
+            up(d_srows, srows.data(), srows.size());
+            up(d_sptr, sptr.data(), sptr.size());
+            up(d_sid, sid.data(), sid.size());
+            up(d_off, out_off, (size_t)n_rows + 1);
+            up(d_seeds, seeds, (size_t)n_streams);
+            up(d_recip, recip.data(), recip.size());
+            if (rng_state) up(d_state, rng_state, (size_t)n_streams * (rng == HGS_RNG_PHILOX ? 1 : 4));
+            d_out.reserve(std::max<int64_t>(out_off[n_rows], 1));
+            d_draws.reserve(groups);
+            d_dec.reserve(groups);
+            RowsParams p{};
+            p.row_ptr = d_rp.p; p.col = d_ci.p; p.srows = d_srows.p; p.sptr = d_sptr.p; p.sid = d_sid.p;
+            p.out_off = d_off.p; p.out_cols = d_out.p; p.seeds = d_seeds.p;
+            p.state = rng_state ? d_state.p : nullptr; p.recip = d_recip.p;
+            p.fanout = (int32_t)std::min<int64_t>(s, 1 << 30); p.groups = (int32_t)groups;
+            p.draws = d_draws.p; p.decisions = d_dec.p;
+            launch_sample_rows(p, rng == HGS_RNG_PHILOX, st);
+            if (out_off[n_rows] > 0)
+                HGS_CUDA(cudaMemcpyAsync(out_cols, d_out.p, sizeof(int64_t) * out_off[n_rows], cudaMemcpyDeviceToHost, st));
+            HGS_CUDA(cudaMemcpyAsync(gd.data(), d_draws.p, sizeof(uint32_t) * groups, cudaMemcpyDeviceToHost, st));
+            HGS_CUDA(cudaMemcpyAsync(gc.data(), d_dec.p, sizeof(uint32_t) * groups, cudaMemcpyDeviceToHost, st));
+            HGS_CUDA(cudaStreamSynchronize(st));
+            HGS_CUDA(cudaStreamDestroy(st));
+        }
+        if (draws) std::fill(draws, draws + n_streams, 0u);
+        if (decisions) std::fill(decisions, decisions + n_streams, 0u);
+        for (int64_t g = 0; g < groups; ++g) {
+            if (draws) draws[sid[g]] = gd[g];
+            if (decisions) decisions[sid[g]] = gc[g];
+        }
+    });
+}
+
 int hgs_sample_wait(hgs_sample* s, int64_t* counts) {
     return guarded([&] {
         if (!s) fail(HGS_EINVAL, "hgs: null sample handle");

@@ -252,6 +252,61 @@ SampledBatch shadow_reference(const CsrMatrix& a, std::span<const Index> roots,
     return std::move(run_bulk(g.g, s.s, one, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, true).front());
 }
 
+std::vector<std::vector<Index>> sample_rows(const CsrMatrix& p, Index s, ChoiceSource& choice,
+                                            std::span<const Index> row_streams) {
+    if (s < 1) fail_invalid("sample_rows: s must be >= 1");
+    if (!row_streams.empty() && static_cast<Index>(row_streams.size()) != p.n_rows)
+        fail_invalid("sample_rows: row_streams length must equal row count");
+    for (double v : p.values)
+        if (v < 0.0) fail_invalid("sample_rows: row with negative mass");
+    auto* per_root = dynamic_cast<PerRootChoiceSource*>(&choice);
+    auto* philox = dynamic_cast<PhiloxChoiceSource*>(&choice);
+    if (!per_root && !philox)
+        fail_invalid("sample_rows: the GPU sampler needs a PerRootChoiceSource or PhiloxChoiceSource");
+    const std::size_t n_streams = per_root ? per_root->size() : philox->size();
+    const std::size_t cur = per_root ? per_root->current() : philox->current();
+    std::vector<Index> streams(row_streams.begin(), row_streams.end());
+    if (streams.empty()) streams.assign(static_cast<std::size_t>(p.n_rows), static_cast<Index>(cur));
+    Index last = -1, total = 0;
+    for (Index r = 0; r < p.n_rows; ++r) {
+        const Index deg = p.row_ptr[r + 1] - p.row_ptr[r];
+        if (deg == 0) continue;
+        total += std::min(s, deg);
+        if (last < 0) {  // the reference's first begin_root / choose sees these first
+            if (!row_streams.empty() && (streams[r] < 0 || static_cast<std::size_t>(streams[r]) >= n_streams))
+                fail_invalid(per_root ? "PerRootChoiceSource: root ordinal out of range"
+                                      : "PhiloxChoiceSource: root ordinal out of range");
+            if (n_streams == 0)
+                fail_invalid(per_root ? "PerRootChoiceSource: no streams configured"
+                                      : "PhiloxChoiceSource: no streams configured");
+        }
+        last = r;
+    }
+    std::vector<std::uint64_t> state;
+    const std::uint64_t* state_ptr = nullptr;
+    if (per_root && !per_root->fresh()) {
+        state = per_root->states();
+        state_ptr = state.data();
+    } else if (philox && !philox->fresh()) {
+        state.assign(philox->decisions().begin(), philox->decisions().end());
+        state_ptr = state.data();
+    }
+    const std::vector<std::uint64_t>& seeds = per_root ? per_root->seeds() : philox->seeds();
+    std::vector<int64_t> off(static_cast<std::size_t>(p.n_rows) + 1), cols(static_cast<std::size_t>(std::max<Index>(total, 1)));
+    std::vector<std::uint32_t> draws(n_streams + 1), decs(n_streams + 1);
+    check(hgs_sample_rows(0, p.n_rows, p.n_cols, p.row_ptr.data(), p.col_idx.data(), nullptr, s,
+                          philox ? HGS_RNG_PHILOX : HGS_RNG_XOSHIRO, seeds.data(), static_cast<int64_t>(n_streams),
+                          state_ptr, streams.data(), off.data(), cols.data(), draws.data(), decs.data()));
+    draws.resize(n_streams);
+    decs.resize(n_streams);
+    if (per_root) per_root->advance(draws);
+    else philox->advance(decs);
+    if (last >= 0 && !row_streams.empty()) choice.begin_root(static_cast<std::uint64_t>(streams[last]));
+    std::vector<std::vector<Index>> out(static_cast<std::size_t>(p.n_rows));
+    for (Index r = 0; r < p.n_rows; ++r) out[r].assign(cols.begin() + off[r], cols.begin() + off[r + 1]);
+    return out;
+}
+
 CsrMatrix make_edge_id_matrix(const EventGraph& event) {
     event.validate();
     CsrMatrix out(event.n, event.n);

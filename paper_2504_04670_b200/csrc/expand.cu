@@ -315,6 +315,48 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
     p.decisions[r] = ndec - dec0;
 }
 
+// sample_rows (sampler.cpp:64-86): one lane per choice stream, deciding that
+// stream's nonempty rows in row order (begin_root(row_streams[r]) then
+// choose(|support|, min(s, |support|)), positions -> the row's columns).
+template <bool PHILOX>
+__global__ void __launch_bounds__(128) k_sample_rows(RowsParams p) {
+    const int g = blockIdx.x * blockDim.x + threadIdx.x;
+    if (g >= p.groups) return;
+    const int64_t stream = p.sid[g];
+    RootStream<PHILOX> rs;
+    rs.init(p.seeds[stream], (!PHILOX && p.state) ? p.state + 4 * stream : nullptr);
+    uint32_t ndec = (PHILOX && p.state) ? (uint32_t)p.state[stream] : 0u;
+    const uint32_t dec0 = ndec;
+    for (int64_t i = p.sptr[g]; i < p.sptr[g + 1]; ++i) {
+        const int64_t r = p.srows[i];
+        const int64_t b = p.row_ptr[r];
+        const uint32_t deg = (uint32_t)(p.row_ptr[r + 1] - b);
+        const uint32_t k = min((uint32_t)p.fanout, deg);
+        rs.begin_decision(ndec);
+        ++ndec;
+        int64_t* dst = p.out_cols + p.out_off[r];
+        if (k <= 8) {
+            uint32_t pos[8];
+            choose_small<8, PHILOX>(rs, deg, k, p.recip, pos);
+            for (uint32_t q = 0; q < k; ++q) dst[q] = p.col[b + pos[q]];
+        } else {
+            uint32_t pos[256];
+            choose_local<PHILOX>(rs, deg, k, p.recip, pos);
+            for (uint32_t q = 0; q < k; ++q) dst[q] = p.col[b + pos[q]];
+        }
+    }
+    p.draws[g] = rs.draws;
+    p.decisions[g] = ndec - dec0;
+}
+
+void launch_sample_rows(const RowsParams& p, bool philox, cudaStream_t st) {
+    const unsigned grid = (unsigned)((p.groups + 127) / 128);
+    if (grid == 0) return;
+    if (philox) k_sample_rows<true><<<grid, 128, 0, st>>>(p);
+    else k_sample_rows<false><<<grid, 128, 0, st>>>(p);
+    HGS_CUDA(cudaGetLastError());
+}
+
 template <int KCAP, bool PH, bool LOCAL>
 static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cudaStream_t st) {
     auto kern = k_expand<KCAP, PH, LOCAL>;

@@ -42,6 +42,24 @@ struct ExpandParams {
 void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
                    cudaStream_t st);
 
+// sample_rows on the device: rows grouped by choice stream.
+struct RowsParams {
+    const int64_t* __restrict__ row_ptr;  // P's pattern
+    const int64_t* __restrict__ col;
+    const int64_t* __restrict__ srows;    // nonempty rows, grouped by stream, row order within
+    const int64_t* __restrict__ sptr;     // [groups + 1]
+    const int64_t* __restrict__ sid;      // stream ordinal of each group
+    const int64_t* __restrict__ out_off;  // per row: offset of its choices
+    int64_t* __restrict__ out_cols;
+    const uint64_t* __restrict__ seeds;
+    const uint64_t* __restrict__ state;   // nullable: resume (xoshiro 4 words / philox decisions)
+    const uint64_t* __restrict__ recip;
+    int32_t fanout, groups;
+    uint32_t* __restrict__ draws;         // per group
+    uint32_t* __restrict__ decisions;
+};
+void launch_sample_rows(const RowsParams& p, bool philox, cudaStream_t st);
+
 // K2: dedup + induced-subgraph extraction into per-root scratch.
 struct ExtractParams {
     const int32_t* __restrict__ a_rp;

@@ -32,7 +32,8 @@ EXPORTS = [
     "hgs_sample_create", "hgs_sample_destroy", "hgs_sample_run", "hgs_sample_run_device",
     "hgs_sample_wait", "hgs_sample_copy_to_host", "hgs_sample_device_views",
     "hgs_sample_kernel_times", "hgs_sample_stats", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
-    "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind",
+    "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind", "hgs_sample_copy_frontiers",
+    "hgs_sample_rows",
 ]
 
 
@@ -100,6 +101,27 @@ def derive_seeds(spec: SeedSpec, batch_off) -> np.ndarray:
     return out
 
 
+def sample_rows(row_ptr, col_idx, s: int, seeds, row_streams, *, values=None, rng=RNG_XOSHIRO,
+                state=None, n_cols=None, device=0):
+    """hitgnn::sample_rows on the device (hgs_sample_rows): per-row chosen
+    columns as (offsets, cols) plus per-stream draws / decisions consumed."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    va = None if values is None else np.ascontiguousarray(values, np.float64)
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    rs = np.ascontiguousarray(row_streams, np.int64)
+    st = None if state is None else np.ascontiguousarray(state, np.uint64)
+    n = len(rp) - 1
+    off = np.zeros(n + 1, np.int64)
+    deg = np.diff(rp)
+    cols = np.zeros(max(int(np.minimum(deg, max(int(s), 0)).sum()), 1), np.int64)
+    dr = np.zeros(max(len(sd), 1), np.uint32)
+    dc = np.zeros(max(len(sd), 1), np.uint32)
+    _check(lib().hgs_sample_rows(device, n, n if n_cols is None else n_cols, _p(rp), _p(ci), _p(va), int(s), rng,
+                                 _p(sd), len(sd), _p(st), _p(rs), _p(off), _p(cols), _p(dr), _p(dc)))
+    return off, cols[:off[-1]], dr[:len(sd)], dc[:len(sd)]
+
+
 _lib_cache: C.CDLL | None = None
 
 
@@ -130,6 +152,7 @@ def lib() -> C.CDLL:
         L.hgs_sample_run_device_spec.argtypes = [vp, C.POINTER(Config), vp, vp, i64, i64, C.POINTER(SeedSpec)]
         L.hgs_derive_seeds.argtypes = [C.POINTER(SeedSpec), vp, i64, vp]
         L.hgs_sample_bind.argtypes = [vp, vp]
+        L.hgs_sample_rows.argtypes = [C.c_int, i64, i64, vp, vp, vp, i64, i32, vp, i64, vp, vp, vp, vp, vp, vp]
         L.hgs_sample_copy_to_host.argtypes = [vp, C.POINTER(HostOut)]
         L.hgs_sample_device_views.argtypes = [vp, C.POINTER(DeviceViews)]
         L.hgs_sample_kernel_times.argtypes = [vp, vp]

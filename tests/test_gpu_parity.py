@@ -348,6 +348,37 @@ def test_epoch_sampler_matches_trainer_streams():
     assert tot["minibatches"] == sum(g.n // 64 for g in graphs_o)
 
 
+@pytest.mark.parametrize("rng", [0, 1])
+@pytest.mark.parametrize("s", [1, 3, 6, 17])
+def test_sample_rows(rng, s):
+    """hgs_sample_rows (sample_rows, sampler.cpp:64-86): rows on shared
+    streams decided in row order, empty rows make no choose call, fresh and
+    resumed sources; equals the oracle restatement."""
+    H = hgs()
+    rs = np.random.default_rng(100 + s + rng)
+    n = 400
+    deg = rs.integers(0, 40, n)
+    deg[rs.random(n) < 0.15] = 0
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rs.choice(5000, d, replace=False)) for d in deg]).astype(np.int64)
+    seeds = rs.integers(0, 2**63, 37, dtype=np.uint64)
+    streams = rs.integers(0, 37, n).astype(np.int64)
+    for state in (None, "resume"):
+        st = None
+        if state:
+            st = (rs.integers(0, 2**63, 4 * 37, dtype=np.uint64) if rng == 0
+                  else rs.integers(0, 500, 37).astype(np.uint64))
+        off, cols, draws, decs = H.sample_rows(rp, ci, s, seeds, streams, rng=rng, state=st, n_cols=5000)
+        ref, _, ndec, _ = O.sample_rows(rp, ci, s, seeds, streams, rng=rng, state=st)
+        got = [cols[off[r]:off[r + 1]].tolist() for r in range(n)]
+        assert got == ref
+        assert np.array_equal(decs.astype(np.int64), ndec)
+    with pytest.raises(H.SamplerError, match="s must be >= 1"):
+        H.sample_rows(rp, ci, 0, seeds, streams)
+    with pytest.raises(H.SamplerError, match="root ordinal out of range"):
+        H.sample_rows(rp, ci, 2, seeds[:3], streams)
+
+
 def test_multi_handle_sharding_matches_single_call():
     """Two sample handles on one graph (as two ranks would be): the shard union
     equals the single call, batch for batch."""
