@@ -139,8 +139,7 @@ int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* 
             }
             rp[u + 1] = (int32_t)ci.size();
         }
-        std::vector<int4> ari;      // per vertex of A: padded start, quads, delta, degree
-        std::vector<int32_t> apad;  // A's col_idx, rows padded to multiples of 4
+        std::vector<int2> ari;  // (row start, out-degree) per vertex of A
         auto* h = new hgs_graph;
         DevGraph& g = h->g;
         try {
@@ -151,23 +150,10 @@ int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* 
             g.n_cols = n_cols;
             g.nnz = nnz;
             upload_csr(g.a, n, rp, ci, g.stream);
-            // padded copy of A for K2's 16-byte row loads + per-vertex row info
             ari.resize((size_t)std::max<int32_t>(n, 1));
-            int64_t padded = 0;
-            for (int32_t u = 0; u < n; ++u) padded += (int64_t)(rp[u + 1] - rp[u] + 3) / 4 * 4;
-            if (padded >= ((int64_t)1 << 31) - 4) fail(HGS_ERANGE, "hgs_graph_create: padded A exceeds 2^31 entries");
-            apad.assign((size_t)std::max<int64_t>(padded, 4), n);
-            int32_t pos = 0;
-            for (int32_t u = 0; u < n; ++u) {
-                const int32_t deg = rp[u + 1] - rp[u], nq = (deg + 3) / 4;
-                ari[u] = make_int4(pos, nq, rp[u] - pos, deg);
-                std::copy(ci.begin() + rp[u], ci.begin() + rp[u + 1], apad.begin() + pos);
-                pos += 4 * nq;
-            }
-            g.a_ri4.reserve(ari.size());
-            upload(g.a_ri4.p, ari.data(), ari.size() * sizeof(int4), g.stream);
-            g.a_pad.reserve(apad.size());
-            upload(g.a_pad.p, apad.data(), apad.size() * sizeof(int32_t), g.stream);
+            for (int32_t u = 0; u < n; ++u) ari[u] = make_int2(rp[u], rp[u + 1] - rp[u]);
+            g.a_ri.reserve(ari.size());
+            upload(g.a_ri.p, ari.data(), ari.size() * sizeof(int2), g.stream);
             if (zeros) {
                 g.has_gid = true;
                 g.a_gid.reserve(gid.size());

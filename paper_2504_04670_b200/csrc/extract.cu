@@ -41,11 +41,10 @@ struct HashSet;
 template <>
 struct HashSet<true> {
     uint32_t* slot;
-    uint32_t nb, rmask;  // nb buckets of 4 slots (any count)
-    int rb;
+    uint32_t bmask, rmask;
+    int bits, rb;
     static constexpr int kBytesPerSlot = 4;
-    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return __umulhi(v * 0x9E3779B1u, nb); }
-    __device__ __forceinline__ uint32_t next(uint32_t b) const { return b + 1 == nb ? 0u : b + 1; }
+    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
     __device__ __forceinline__ void clear(int nslots) const {
         for (int i = lane_id(); i < nslots / 4; i += 32)
             reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
@@ -60,7 +59,7 @@ struct HashSet<true> {
                 if (prev == kEmpty) return true;
                 if ((prev ^ hi) <= rmask) return false;
             }
-            b = next(b);
+            b = (b + 1) & bmask;
         }
     }
     __device__ __forceinline__ int find_slot(uint32_t v) const {
@@ -73,7 +72,7 @@ struct HashSet<true> {
             if ((q.z ^ hi) <= rmask) return 4 * b + 2;
             if ((q.w ^ hi) <= rmask) return 4 * b + 3;
             if (q.w == kEmpty) return -1;
-            b = next(b);
+            b = (b + 1) & bmask;
         }
     }
     __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)] = (v << rb) | r; }
@@ -87,7 +86,7 @@ struct HashSet<true> {
         uint32_t d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
         if (d > rmask && q.w != kEmpty) {  // full bucket without a match: rare
             do {
-                b = next(b);
+                b = (b + 1) & bmask;
                 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
                 d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
             } while (d > rmask && q.w != kEmpty);
@@ -99,11 +98,10 @@ struct HashSet<true> {
 template <>
 struct HashSet<false> {
     uint2* slot;  // (vertex, rank)
-    uint32_t nb, rmask;
-    int rb;
+    uint32_t bmask, rmask;
+    int bits, rb;
     static constexpr int kBytesPerSlot = 8;
-    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return __umulhi(v * 0x9E3779B1u, nb); }
-    __device__ __forceinline__ uint32_t next(uint32_t b) const { return b + 1 == nb ? 0u : b + 1; }
+    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
     __device__ __forceinline__ void clear(int nslots) const {
         for (int i = lane_id(); i < nslots; i += 32) slot[i] = make_uint2(kEmpty, 0);
     }
@@ -116,7 +114,7 @@ struct HashSet<false> {
                 if (prev == kEmpty) return true;
                 if (prev == v) return false;
             }
-            b = next(b);
+            b = (b + 1) & bmask;
         }
     }
     __device__ __forceinline__ int find_slot(uint32_t v) const {
@@ -129,7 +127,7 @@ struct HashSet<false> {
             if (q1.x == v) return 4 * b + 2;
             if (q1.z == v) return 4 * b + 3;
             if (q1.z == kEmpty) return -1;
-            b = next(b);
+            b = (b + 1) & bmask;
         }
     }
     __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)].y = r; }
@@ -144,7 +142,7 @@ struct HashSet<false> {
             r = (q0.z == v) ? (int)q0.w : r;
             r = (q0.x == v) ? (int)q0.y : r;
             if (r >= 0 || q1.z == kEmpty) return r;
-            b = next(b);
+            b = (b + 1) & bmask;
         }
     }
 };
@@ -157,21 +155,17 @@ struct HashSet<false> {
 
 // Per-warp shared memory of K2 (set_cap == row_cap == max tree size rounded
 // up to 32; the regions are reused phase by phase):
-//   hash   4*n_buckets slots                  vertex -> rank
+//   hash   4<<nb_bits slots                   vertex -> rank
 //   keys   set_cap x i32   unsorted keys -> sorted keys -> window masks/cursors
 //   tmp    row_cap+36 x i32  bucketed keys -> row starts (+ sentinels)
 //   aux    row_cap x int2  bucket counters -> per nonempty row (A pos - flat pos, rank<<16)
-#ifndef HGS_K2_MINB
-#define HGS_K2_MINB 6  // 4-warp blocks per SM the register budget is sized for
-#endif
-
-template <bool PACKED>
-__global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
+template <bool PACKED, bool HAS_GID>
+__global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     unsigned char* q = smem_raw + (size_t)warp * p.warp_bytes;
-    const int nslots = 4 * p.n_buckets;
+    const int nslots = 4 << p.nb_bits;
     HashSet<PACKED> hs;
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
     q += HashSet<PACKED>::kBytesPerSlot * nslots;
@@ -182,7 +176,8 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
     int32_t* rstart = tmp;
     int32_t* cnt = (int32_t*)q;
     int2* rinfo = (int2*)q;
-    hs.nb = (uint32_t)p.n_buckets;
+    hs.bits = p.nb_bits;
+    hs.bmask = (1u << p.nb_bits) - 1u;
     hs.rb = p.rank_bits;
     hs.rmask = (1u << p.rank_bits) - 1u;
     const unsigned lt = (1u << lane) - 1u;
@@ -218,7 +213,6 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         }
         lo = __reduce_min_sync(kFull, lo);
         hi = __reduce_max_sync(kFull, hi);
-
         // ---- order-preserving buckets b = (v - lo) >> shift, ~2U of them
         const int lg = min(p.cnt_lg, max(5, 32 - __clz(max(2 * U - 1, 1))));
         const int shift = max(0, (32 - __clz(hi - lo)) - lg);
@@ -264,49 +258,44 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         }
         __syncwarp();
 
-        // ---- sorted set back to global; per local vertex its padded-A
-        // delta (for K3's edge ids); nonempty rows in local order, measured
-        // in 4-entry quads of the padded A (rows start 16-byte aligned)
-        int NR = 0, SQ = 0, S = 0;
-        int32_t* gd = p.gdscr + (size_t)r * p.stride;
+        // ---- sorted set back to global; nonempty A rows in local order
+        int NR = 0, S = 0;
         for (int b0 = 0; b0 < U; b0 += CH * 32) {
-            int4 ri[CH];
+            int2 ri[CH];
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 const int i = b0 + c * 32 + lane;
-                ri[c] = make_int4(0, 0, 0, 0);
+                ri[c] = make_int2(0, 0);
                 if (i < U) {
                     const int32_t u = keys[i];
                     tl[i] = u;
-                    ri[c] = __ldg(p.a_ri4 + u);
+                    ri[c] = __ldg(p.a_ri + u);
                 }
             }
 #pragma unroll
             for (int c = 0; c < CH; ++c) {
                 if (b0 + c * 32 >= U) break;
                 const int i = b0 + c * 32 + lane;
-                const int nq = ri[c].y;
-                if (i < U) gd[i] = ri[c].z;
-                const bool ne = nq > 0;
+                const int deg = ri[c].y;
+                const bool ne = deg > 0;
                 const unsigned nb = __ballot_sync(kFull, ne);
-                const int incl = warp_incl_scan(nq);
+                const int incl = warp_incl_scan(deg);
                 if (ne) {
                     const int qi = NR + __popc(nb & lt);
-                    const int qs = SQ + incl - nq;
-                    rstart[qi] = qs;
-                    rinfo[qi] = make_int2(ri[c].x - 4 * qs, i << 16);
+                    const int st = S + incl - deg;
+                    rstart[qi] = st;
+                    rinfo[qi] = make_int2(ri[c].x - st, i << 16);
                 }
                 NR += __popc(nb);
-                SQ += __shfl_sync(kFull, incl, 31);
-                S += __reduce_add_sync(kFull, (unsigned)ri[c].w);
+                S += __shfl_sync(kFull, incl, 31);
             }
         }
-        if (lane == 0) rstart[NR] = SQ;
+        if (lane == 0) rstart[NR] = S;
         __syncwarp();
 
-        // ---- window cursors: row holding the first quad of each 32-quad window
+        // ---- window cursors: row holding the first entry of each 32-window
         for (int i = NR + 1 + lane; i <= NR + 32; i += 32) rstart[i] = 0x7fffffff;  // sentinels
-        const int nwin = (SQ + 31) >> 5;
+        const int nwin = (S + 31) >> 5;
         const bool direct = nwin <= p.win_cap;
         if (direct) {
             for (int w = lane; w < nwin; w += 32) wmask[w] = 0u;
@@ -319,62 +308,87 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         }
         __syncwarp();
 
-        // ---- induced subgraph: every lane takes one quad (4 consecutive
-        // entries of one row, one 16-byte load) per window; hits come out in
-        // the reference's CSR order (lane-major, then within the quad)
+        // ---- induced subgraph: scan the flattened rows in 32-entry windows
         int2* const ed = p.escratch + (size_t)r * p.e_stride;
         int2* const ed_end = ed + p.e_stride;
         int2* edc = ed;  // next free edge slot
-        const uint32_t pad = (uint32_t)p.n;  // never a set vertex
-        // CHK: the slot might overflow, stores are bounds-checked (the
-        // overflow is reported below and the call re-run with larger slots)
-        auto process = [&](const uint4& q, int kk, int rowsh, auto chk) {
-            const int j0 = hs.find_rank(q.x), j1 = hs.find_rank(q.y);
-            const int j2 = hs.find_rank(q.z), j3 = hs.find_rank(q.w);
-            const unsigned h = (j0 >= 0) + (j1 >= 0) + (j2 >= 0) + (j3 >= 0);
-            const unsigned c0 = ballot_nz(h & 1u), c1 = ballot_nz(h & 2u), c2 = ballot_nz(h & 4u);
-            int2* d = edc + (__popc(c0 & lt) + 2 * __popc(c1 & lt) + 4 * __popc(c2 & lt));
-            auto put = [&](int j, int e) {
-                if (j >= 0) {
-                    if (!decltype(chk)::value || d < ed_end) *d = make_int2(rowsh | j, kk + e);
-                    ++d;
-                }
-            };
-            put(j0, 0);
-            put(j1, 1);
-            put(j2, 2);
-            put(j3, 3);
-            edc += __popc(c0) + 2 * __popc(c1) + 4 * __popc(c2);
+        // Emit the hits of one window in scan order. CHK is set when the
+        // slot might overflow: stores are then bounds-checked, overflow is
+        // reported below and the host re-runs the call with larger slots.
+        auto emit = [&](int j, int rowsh, int kk, auto chk) {
+            const unsigned hb = ballot_nonneg(j);
+            int2* dst = edc + __popc(hb & lt);
+            if (j >= 0 && (!decltype(chk)::value || dst < ed_end))
+                *dst = make_int2(rowsh | j, HAS_GID ? __ldg(p.a_gid + kk) : kk);
+            edc += __popc(hb);
         };
-        auto run = [&](const uint4& q, int kk, int rowsh) {
-            if (edc + 128 <= ed_end) process(q, kk, rowsh, std::false_type{});
-            else process(q, kk, rowsh, std::true_type{});
+#ifndef HGS_K2_G
+#define HGS_K2_G 4
+#endif
+        constexpr int G = HGS_K2_G;  // windows in flight per group
+        auto fetch = [&](int w, int (&rs)[G], int (&kk)[G], uint32_t (&v)[G]) {
+#pragma unroll
+            for (int u = 0; u < G; ++u) {
+                const int own = (int)wcur[w + u] + __popc(wmask[w + u] & le);
+                const int2 ri = rinfo[own];
+                kk[u] = ((w + u) << 5) + lane + ri.x;
+                rs[u] = ri.y;
+            }
+#pragma unroll
+            for (int u = 0; u < G; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
         };
+        auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G]) {
+            int j[G];
+#pragma unroll
+            for (int u = 0; u < G; ++u) j[u] = hs.find_rank(v[u]);
+            if (edc + 32 * G <= ed_end) {
+#pragma unroll
+                for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::false_type{});
+            } else {
+#pragma unroll
+                for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::true_type{});
+            }
+        };
+        int w = 0;
         if (direct) {
-            auto fetch = [&](int w, uint4& q, int& kk, int& rowsh) {
-                const int qd = (w << 5) + lane;
+            // full groups, software-pipelined: the column loads of group g+1
+            // are in flight while group g is probed and emitted
+            const int nfg = (S >> 5) / G;
+#if HGS_K2_SINGLE
+            for (int gi = 0; gi < nfg; ++gi) {
+                int rsA[G], kkA[G];
+                uint32_t vA[G];
+                fetch(gi * G, rsA, kkA, vA);
+                consume(rsA, kkA, vA);
+            }
+            w = nfg * G;
+#else
+            if (nfg > 0) {
+                int rsA[G], kkA[G], rsB[G], kkB[G];
+                uint32_t vA[G], vB[G];
+                fetch(0, rsA, kkA, vA);
+                for (int gi = 0; gi < nfg; gi += 2) {
+                    if (gi + 1 < nfg) fetch((gi + 1) * G, rsB, kkB, vB);
+                    consume(rsA, kkA, vA);
+                    if (gi + 1 < nfg) {
+                        if (gi + 2 < nfg) fetch((gi + 2) * G, rsA, kkA, vA);
+                        consume(rsB, kkB, vB);
+                    }
+                }
+                w = nfg * G;
+            }
+#endif
+            for (; w < nwin; ++w) {  // < G trailing windows, the last one partial
+                const int base = w << 5;
                 const int own = min((int)wcur[w] + __popc(wmask[w] & le), NR - 1);
                 const int2 ri = rinfo[own];
-                kk = 4 * qd + ri.x;
-                rowsh = ri.y;
-                q = qd < SQ ? __ldg(reinterpret_cast<const uint4*>(p.a_pad + kk)) : make_uint4(pad, pad, pad, pad);
-            };
-            // software-pipelined: window w+1's loads are in flight while w is probed
-            uint4 qA, qB;
-            int kkA, kkB, rsA, rsB;
-            if (nwin > 0) fetch(0, qA, kkA, rsA);
-            for (int w = 0; w < nwin; w += 2) {
-                if (w + 1 < nwin) fetch(w + 1, qB, kkB, rsB);
-                run(qA, kkA, rsA);
-                if (w + 1 < nwin) {
-                    if (w + 2 < nwin) fetch(w + 2, qA, kkA, rsA);
-                    run(qB, kkB, rsB);
-                }
+                const int kk = base + lane < S ? base + lane + ri.x : -1;
+                const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
+                emit(j, ri.y, kk, std::true_type{});
             }
         } else {
             int cursor = 0;  // huge sets: serial window cursor
-#pragma unroll 1
-            for (int w = 0; w < nwin; ++w) {
+            for (; w < nwin; ++w) {
                 const int base = w << 5;
                 const int c = cursor;
                 const int off = rstart[c + 1 + lane] - base;
@@ -383,11 +397,9 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 const int own31 = __shfl_sync(kFull, own, 31);
                 cursor = (rstart[own31 + 1] == base + 32) ? own31 + 1 : own31;
                 const int2 ri = rinfo[own];
-                const int qd = base + lane;
-                const int kk = 4 * qd + ri.x;
-                const uint4 q = qd < SQ ? __ldg(reinterpret_cast<const uint4*>(p.a_pad + kk))
-                                        : make_uint4(pad, pad, pad, pad);
-                process(q, kk, ri.y, std::true_type{});
+                const int kk = base + lane < S ? base + lane + ri.x : -1;
+                const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
+                emit(j, ri.y, kk, std::true_type{});
             }
         }
         const int count = (int)(edc - ed);
@@ -527,7 +539,6 @@ int64_t scan_tmp_words(int64_t R) { return 2 * ((R + kPairTile - 1) / kPairTile)
 // ===========================================================================
 
 __global__ void __launch_bounds__(256) k_pack(PackParams p) {
-    extern __shared__ int32_t pack_smem[];
     const int lane = lane_id();
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     constexpr int U = 8;  // independent loads in flight per lane
@@ -571,13 +582,6 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
                 if (i < Vr) __stcs(p.l2g + vb + i, u[k]);
             }
         }
-        // per local vertex: edge id = padded-A position + its row's delta
-        int32_t* sgd = pack_smem + (size_t)(threadIdx.x >> 5) * p.set_cap;
-        {
-            const int32_t* gd = p.gdscr + (size_t)r * p.stride;
-            for (int i = lane; i < Vr; i += 32) sgd[i] = gd[i];
-            __syncwarp();
-        }
         // COO edges (block_diag rebasing) and edge ids
         const int2* ed = p.escratch + (size_t)r * p.e_stride;
         for (int t0 = 0; t0 < Er; t0 += 32 * U) {
@@ -591,11 +595,9 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
             for (int k = 0; k < U; ++k) {
                 const int t = t0 + 32 * k + lane;
                 if (t < Er) {
-                    int32_t gid = e[k].y + sgd[e[k].x >> 16];
-                    if (p.a_gid) gid = __ldg(p.a_gid + gid);  // zeros were dropped from A
                     __stcs(p.e_row + eb + t, loc + (e[k].x >> 16));
                     __stcs(p.e_col + eb + t, loc + (e[k].x & 0xffff));
-                    __stcs(p.e_gid + eb + t, gid);
+                    __stcs(p.e_gid + eb + t, e[k].y);
                 }
             }
         }
@@ -769,14 +771,15 @@ __global__ void k_stats(const int32_t* __restrict__ level_counts, int32_t depth,
 // ---- launchers -----------------------------------------------------------------
 
 void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st) {
-    auto kern = packed ? k_extract<true> : k_extract<false>;
+    auto kern = packed ? (xp.a_gid ? k_extract<true, true> : k_extract<true, false>)
+                       : (xp.a_gid ? k_extract<false, true> : k_extract<false, false>);
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, 128, smem, st>>>(xp);
     HGS_CUDA(cudaGetLastError());
 }
 
 int extract_blocks_per_sm(size_t smem, bool packed) {
-    auto kern = packed ? k_extract<true> : k_extract<false>;
+    auto kern = packed ? k_extract<true, false> : k_extract<false, false>;
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
@@ -784,10 +787,7 @@ int extract_blocks_per_sm(size_t smem, bool packed) {
 }
 
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st) {
-    const size_t smem = (size_t)8 * pp.set_cap * sizeof(int32_t);
-    if (smem > 48 * 1024)
-        HGS_CUDA(cudaFuncSetAttribute(k_pack, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    k_pack<<<grid, 256, smem, st>>>(pp);
+    k_pack<<<grid, 256, 0, st>>>(pp);
     HGS_CUDA(cudaGetLastError());
 }
 

@@ -65,8 +65,7 @@ struct DevGraph {
     int device = 0;
     int64_t n_rows = 0, n_cols = 0, nnz = 0;  // as given by the caller
     DevCsr a;                // extraction matrix: A minus explicit zeros
-    DevBuf<int32_t> a_pad;   // a's col_idx with every row padded to a multiple of 4 (pad = n)
-    DevBuf<int4> a_ri4;      // per vertex: (padded row start, quads, row start - padded start, degree)
+    DevBuf<int2> a_ri;       // per vertex of a: (row start, out-degree), one 8-byte load
     DevBuf<int32_t> a_gid;   // a position -> input CSR position (only if zeros dropped)
     bool has_gid = false;
     DevCsr a_full;           // full pattern of A (only if zeros dropped; else == a)
@@ -113,12 +112,6 @@ __device__ __forceinline__ int lane_id() { return threadIdx.x & 31; }
 
 // Full-warp ballot for code the caller knows to be converged: plain
 // vote.sync without the divergence fallback ptxas wraps __ballot_sync in.
-__device__ __forceinline__ unsigned ballot_nz(unsigned x) {  // ballot(x != 0)
-    unsigned r;
-    asm volatile("{ .reg .pred q; setp.ne.u32 q, %1, 0; vote.sync.ballot.b32 %0, q, 0xffffffff; }"
-                 : "=r"(r) : "r"(x));
-    return r;
-}
 __device__ __forceinline__ unsigned ballot_nonneg(int x) {  // ballot(x >= 0)
     unsigned r;
     asm volatile("{ .reg .pred q; setp.ge.s32 q, %1, 0; vote.sync.ballot.b32 %0, q, 0xffffffff; }"
@@ -230,7 +223,6 @@ struct hgs_sample {
     int64_t touched_stride = 0;
     // extract scratch + offsets
     hgs::DevBuf<int32_t> root_nv, root_ne, root_rloc;
-    hgs::DevBuf<int32_t> gdscr;  // per root, per local vertex: A position - padded position
     hgs::DevBuf<int2> escratch;
     int32_t e_stride = 512;
     hgs::DevBuf<int64_t> scan_tmp;

@@ -65,10 +65,7 @@ struct ExtractParams {
     const int32_t* __restrict__ a_rp;
     const int32_t* __restrict__ a_ci;
     const int32_t* __restrict__ a_gid;  // nullable
-    const int32_t* __restrict__ a_pad;  // padded col_idx (rows 16-byte aligned)
-    const int4* __restrict__ a_ri4;     // per vertex: (padded start, quads, delta to A, degree)
-    int32_t* __restrict__ gdscr;        // out: per root / local vertex the delta to A positions
-    int32_t n;                          // vertices (the pad value)
+    const int2* __restrict__ a_ri;      // per vertex: (A row start, out-degree)
     int32_t* __restrict__ touched;      // in: touched lists; out: sorted sets
     const int32_t* __restrict__ tcount;
     int64_t stride;
@@ -80,7 +77,7 @@ struct ExtractParams {
     int2* __restrict__ escratch;        // per root: e_stride x (local i<<16 | j, edge id)
     int32_t e_stride;
     int32_t* __restrict__ ticket;
-    int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
+    int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
     int32_t cnt_lg;                     // log2 of the bucket-counter capacity (<= 2*row_cap)
 };
 
@@ -93,8 +90,6 @@ struct PackParams {
     const int32_t* __restrict__ root_rloc;
     const int2* __restrict__ escratch;
     int32_t e_stride;
-    const int32_t* __restrict__ gdscr;  // per root / local vertex: padded -> A position delta
-    const int32_t* __restrict__ a_gid;  // nullable: A position -> input CSR position
     const int64_t* __restrict__ batch_off;
     int32_t k, r0, R;                   // roots [r0, R)
     int32_t* __restrict__ l2g;

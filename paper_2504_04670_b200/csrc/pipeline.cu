@@ -32,7 +32,7 @@ struct CallPlan {
     int expand_threads;
     size_t expand_smem;
     int32_t recip_smem;
-    int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
+    int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
 };
 
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
@@ -57,21 +57,21 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
             c.expand_threads = 128;
         }
     }
-    // K2 hash set: 4-slot buckets, a power of two of them with at least
-    // HGS_HASH_SLOTS_PER_KEY (default 3) slots per possible key; entries pack
-    // (vertex << rank_bits | rank) into 32 bits when vertex ids leave room,
-    // else (vertex, rank) pairs.
+    // K2 hash set: 4-slot buckets, HGS_HASH_SLOTS_PER_KEY (default 4) slots per
+    // possible key; entries pack (vertex << rank_bits | rank) into 32 bits when
+    // vertex ids leave room, else (vertex, rank) 64-bit pairs.
     int spk = 3;
     if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) spk = std::max(2, atoi(e));
     c.rank_bits = 1;
     while (((int64_t)1 << c.rank_bits) < c.max_t) ++c.rank_bits;
     c.packed = (n + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
-    c.n_buckets = 4;
-    while (4 * (int64_t)c.n_buckets < spk * c.max_t) c.n_buckets *= 2;
+    int bits = 2;
+    while (((int64_t)4 << bits) < spk * c.max_t) ++bits;
+    c.nb_bits = bits;
     c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);
     c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
-    c.win_cap = c.set_cap * 2 / 3;  // (u32 mask + u16 cursor) per 32-quad window alias the set array
-    const size_t slots = (size_t)4 * c.n_buckets;
+    c.win_cap = c.set_cap * 2 / 3;  // (u32 mask + u16 cursor) per window alias the set array
+    const size_t slots = (size_t)4 << c.nb_bits;
     size_t bytes = (c.packed ? 4 : 8) * slots + 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) +
                    8 * (size_t)c.row_cap;
     bytes = (bytes + 15) / 16 * 16;
@@ -108,7 +108,6 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     s->touched_stride = c.max_t;
     const size_t R1 = (size_t)R + 1;
     s->touched.reserve((size_t)std::max<int64_t>(R, 1) * c.max_t);
-    s->gdscr.reserve((size_t)std::max<int64_t>(R, 1) * c.max_t);
     s->tcount.reserve(R1);
     s->level_counts.reserve(R1 * (cfg.depth + 1));
     s->draws.reserve(R1);
@@ -161,12 +160,11 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     ep.draws = s->draws.p; ep.decisions = s->decisions.p; ep.ticket = s->ticket.p;
 
     ExtractParams xp{};
-    xp.a_rp = g.a.rp.p; xp.a_ci = g.a.ci.p; xp.a_gid = nullptr;
-    xp.a_pad = g.a_pad.p; xp.a_ri4 = g.a_ri4.p; xp.gdscr = s->gdscr.p; xp.n = (int32_t)g.n_rows;
+    xp.a_rp = g.a.rp.p; xp.a_ci = g.a.ci.p; xp.a_gid = g.has_gid ? g.a_gid.p : nullptr; xp.a_ri = g.a_ri.p;
     xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t;
     xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
     xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
-    xp.ticket = s->ticket.p; xp.n_buckets = c.n_buckets; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
+    xp.ticket = s->ticket.p; xp.nb_bits = c.nb_bits; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
     xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
     xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
     const size_t xsmem = (size_t)4 * c.warp_bytes;
@@ -175,7 +173,6 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     pp.touched = s->touched.p; pp.stride = c.max_t; pp.root_voff = s->root_voff.p;
     pp.root_eoff = s->root_eoff.p; pp.root_rloc = s->root_rloc.p; pp.escratch = s->escratch.p;
     pp.e_stride = s->e_stride; pp.batch_off = in.batch_off; pp.k = (int32_t)k;
-    pp.gdscr = s->gdscr.p; pp.a_gid = g.has_gid ? g.a_gid.p : nullptr;
     pp.l2g = s->l2g.p; pp.roots_local = s->roots_local.p; pp.comp_off = s->comp_off.p;
     pp.e_row = s->e_row.p; pp.e_col = s->e_col.p; pp.e_gid = s->e_gid.p;
     pp.xv = s->xv.p; pp.ye = s->ye.p; pp.lab = s->lab.p;
