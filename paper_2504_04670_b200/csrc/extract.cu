@@ -184,8 +184,14 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     const unsigned le = (2u << lane) - 1u;
     constexpr int CH = 4;  // 32-key chunks of row loads in flight
 
-    const int nwarps = gridDim.x * (blockDim.x >> 5);
-    for (int r = p.r0 + blockIdx.x * (blockDim.x >> 5) + warp; r < p.R; r += nwarps) {
+    // roots are handed out dynamically (per-root work varies ~6x), which
+    // shortens the tail of the persistent grid
+    auto next_root = [&]() -> int {
+        int r = 0;
+        if (lane == 0) r = p.r0 + atomicAdd(p.work, 1);
+        return __shfl_sync(kFull, r, 0);
+    };
+    for (int r = next_root(); r < p.R; r = next_root()) {
         int32_t* tl = p.touched + (size_t)r * p.stride;
         const int T = p.tcount[r];
 

@@ -229,6 +229,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         const int64_t Rc = r1 - r0;
         xp.r0 = r0; xp.R = r1;
         const int64_t xgrid = split ? (Rc + 3) / 4 : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + 3) / 4);
+        xp.work = s->ticket.p + 5;
+        HGS_CUDA(cudaMemsetAsync(xp.work, 0, sizeof(int32_t), st));
         launch_extract((int)std::max<int64_t>(xgrid, 1), xsmem, xp, c.packed != 0, st);
         ++s->launches;
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
