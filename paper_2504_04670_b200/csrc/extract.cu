@@ -619,11 +619,11 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
 // record per edge (DevGraph::erec) instead of two requests.
 __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__ node_feat, int32_t f_v,
                                                       uint32_t fv_magic, const int32_t* __restrict__ l2g,
-                                                      const int32_t* __restrict__ V_ptr, int64_t v_cap,
-                                                      const int32_t* __restrict__ ticket,
+                                                      const int32_t* __restrict__ vb, const int32_t* __restrict__ ve,
+                                                      int64_t v_cap, const int32_t* __restrict__ ticket,
                                                       double* __restrict__ xv) {
     if (ticket[1] != 0) return;  // failed call (re-run or reported): l2g may be incomplete
-    const int64_t V = min((int64_t)*V_ptr, v_cap);
+    const int64_t V0 = min((int64_t)*vb, v_cap), V = min((int64_t)*ve, v_cap);  // vertices [V0, V)
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = 4;
     if ((f_v & 1) == 0) {  // rows as f_v/2 16-byte pieces
@@ -632,7 +632,7 @@ __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__
         const bool magic = n2 < ((int64_t)1 << 32);
         const double2* src = reinterpret_cast<const double2*>(node_feat);
         double2* dst = reinterpret_cast<double2*>(xv);
-        for (int64_t e0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += stride * U) {
+        for (int64_t e0 = V0 * q2 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += stride * U) {
             double2 x[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
@@ -648,7 +648,7 @@ __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__
         }
     } else {
         const int64_t n = V * f_v;
-        for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+        for (int64_t e = V0 * f_v + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
             const int64_t i = e / f_v;
             __stcs(xv + e, __ldg(node_feat + (int64_t)l2g[i] * f_v + (e - i * f_v)));
         }
@@ -658,14 +658,14 @@ __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__
 // f_e == 2: erec[2g] = the edge's two features, erec[2g+1].x = its label
 __global__ void __launch_bounds__(256) k_gather_edges_rec(const uint4* __restrict__ erec,
                                                           const int32_t* __restrict__ e_gid,
-                                                          const int32_t* __restrict__ E_ptr, int64_t e_cap,
-                                                          const int32_t* __restrict__ ticket,
+                                                          const int32_t* __restrict__ eb_, const int32_t* __restrict__ ee,
+                                                          int64_t e_cap, const int32_t* __restrict__ ticket,
                                                           uint4* __restrict__ ye, uint8_t* __restrict__ lab) {
     if (ticket[1] != 0) return;
-    const int64_t E = min((int64_t)*E_ptr, e_cap);
+    const int64_t E0 = min((int64_t)*eb_, e_cap), E = min((int64_t)*ee, e_cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = 4;
-    for (int64_t t0 = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < E; t0 += stride * U) {
+    for (int64_t t0 = E0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < E; t0 += stride * U) {
         int32_t g[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) g[u] = t0 + stride * u < E ? __ldg(e_gid + t0 + stride * u) : 0;
@@ -692,13 +692,13 @@ __global__ void __launch_bounds__(256) k_gather_edges_rec(const uint4* __restric
 __global__ void __launch_bounds__(256) k_gather_edges(const double* __restrict__ edge_feat, int32_t f_e,
                                                       const uint8_t* __restrict__ labels,
                                                       const int32_t* __restrict__ e_gid,
-                                                      const int32_t* __restrict__ E_ptr, int64_t e_cap,
-                                                      const int32_t* __restrict__ ticket,
+                                                      const int32_t* __restrict__ eb_, const int32_t* __restrict__ ee,
+                                                      int64_t e_cap, const int32_t* __restrict__ ticket,
                                                       double* __restrict__ ye, uint8_t* __restrict__ lab) {
     if (ticket[1] != 0) return;
-    const int64_t E = min((int64_t)*E_ptr, e_cap);
+    const int64_t E0 = min((int64_t)*eb_, e_cap), E = min((int64_t)*ee, e_cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
-    for (int64_t t = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < E; t += stride) {
+    for (int64_t t = E0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t < E; t += stride) {
         const int64_t g = e_gid[t];
         lab[t] = __ldg(labels + g);
         for (int c = 0; c < f_e; ++c) __stcs(ye + t * f_e + c, __ldg(edge_feat + g * f_e + c));
@@ -797,17 +797,17 @@ void launch_pack(int grid, const PackParams& pp, cudaStream_t st) {
     HGS_CUDA(cudaGetLastError());
 }
 
-void launch_gather_packed(int sms, const PackParams& pp, const uint4* erec, const int32_t* V_ptr,
-                          const int32_t* E_ptr, cudaStream_t st) {
-    const dim3 grid(sms * 8), block(256);
+void launch_gather_packed(int blocks, const PackParams& pp, const uint4* erec, const int32_t* vb,
+                          const int32_t* ve, const int32_t* eb, const int32_t* ee, cudaStream_t st) {
+    const dim3 grid(blocks), block(256);
     if (pp.f_v > 0)
-        k_gather_nodes<<<grid, block, 0, st>>>(pp.node_feat, pp.f_v, pp.fv_magic, pp.l2g, V_ptr, pp.v_cap,
+        k_gather_nodes<<<grid, block, 0, st>>>(pp.node_feat, pp.f_v, pp.fv_magic, pp.l2g, vb, ve, pp.v_cap,
                                                pp.ticket, pp.xv);
     if (erec)
-        k_gather_edges_rec<<<grid, block, 0, st>>>(erec, pp.e_gid, E_ptr, pp.e_cap, pp.ticket,
+        k_gather_edges_rec<<<grid, block, 0, st>>>(erec, pp.e_gid, eb, ee, pp.e_cap, pp.ticket,
                                                    reinterpret_cast<uint4*>(pp.ye), pp.lab);
     else
-        k_gather_edges<<<grid, block, 0, st>>>(pp.edge_feat, pp.f_e, pp.labels, pp.e_gid, E_ptr, pp.e_cap,
+        k_gather_edges<<<grid, block, 0, st>>>(pp.edge_feat, pp.f_e, pp.labels, pp.e_gid, eb, ee, pp.e_cap,
                                                pp.ticket, pp.ye, pp.lab);
     HGS_CUDA(cudaGetLastError());
 }

@@ -120,10 +120,10 @@ void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, i
                  int32_t* eoff, int32_t* ticket, cudaStream_t st);
 int64_t scan_tmp_words(int64_t R);
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st);
-// node / edge feature gather over the packed call outputs; V and E are read
-// on the device (*V_ptr, *E_ptr = the call totals)
-void launch_gather_packed(int sms, const PackParams& pp, const uint4* erec, const int32_t* V_ptr,
-                          const int32_t* E_ptr, cudaStream_t st);
+// node / edge feature gather over the packed call outputs
+// over vertices [*vb, *ve) and edges [*eb, *ee) of the call (device pointers)
+void launch_gather_packed(int blocks, const PackParams& pp, const uint4* erec, const int32_t* vb,
+                          const int32_t* ve, const int32_t* eb, const int32_t* ee, cudaStream_t st);
 // DevGraph::erec from the attached edge features + labels (f_e == 2 only)
 void build_edge_records(DevGraph& g, cudaStream_t st);
 void launch_finalize(const int64_t* batch_off, int32_t k, int32_t R, const int32_t* voff,

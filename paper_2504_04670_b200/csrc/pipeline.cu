@@ -246,10 +246,13 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         const int64_t pgrid = split ? (Rc + 7) / 8 : std::min<int64_t>((int64_t)sm_count(g.device) * 8, (Rc + 7) / 8);
         launch_pack((int)std::max<int64_t>(pgrid, 1), pp, pst);
         ++s->launches;
-    }
-    if (R > 0 && cfg.gather) {
-        launch_gather_packed(sm_count(g.device), pp, g.erec.p, s->root_voff.p + R, s->root_eoff.p + R, pst);
-        s->launches += 2;
+        if (cfg.gather) {  // this chunk's vertices / edges
+            const int gblocks = split ? std::max<int64_t>(1, std::min<int64_t>(sm_count(g.device) * 8, Rc * 4))
+                                      : sm_count(g.device) * 8;
+            launch_gather_packed(gblocks, pp, g.erec.p, s->root_voff.p + r0, s->root_voff.p + r1,
+                                 s->root_eoff.p + r0, s->root_eoff.p + r1, pst);
+            s->launches += 2;
+        }
     }
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
     if (R == 0 && s->profiled)
