@@ -76,7 +76,7 @@ struct RootStream<true> {
 template <int KCAP, bool PHILOX>
 __device__ __forceinline__ void choose_small(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
                                              const uint64_t* recip, uint32_t (&out)[KCAP]) {
-    static_assert(KCAP == 8, "sorting network below is for 8 keys");
+    static_assert(KCAP == 4 || KCAP == 6 || KCAP == 8, "sorting networks exist for 4, 6, 8 keys");
     uint32_t jj[KCAP], pre[KCAP];
 #pragma unroll
     for (int i = 0; i < KCAP; ++i) {
@@ -101,9 +101,16 @@ __device__ __forceinline__ void choose_small(RootStream<PHILOX>& rs, uint32_t n,
         out[x] = lo;                                                   \
         out[y] = hi;                                                   \
     }
-    HGS_CX(0, 1) HGS_CX(2, 3) HGS_CX(4, 5) HGS_CX(6, 7) HGS_CX(0, 2) HGS_CX(1, 3) HGS_CX(4, 6)
-    HGS_CX(5, 7) HGS_CX(1, 2) HGS_CX(5, 6) HGS_CX(0, 4) HGS_CX(3, 7) HGS_CX(1, 5) HGS_CX(2, 6)
-    HGS_CX(1, 4) HGS_CX(3, 6) HGS_CX(2, 4) HGS_CX(3, 5) HGS_CX(3, 4)
+    if constexpr (KCAP == 8) {
+        HGS_CX(0, 1) HGS_CX(2, 3) HGS_CX(4, 5) HGS_CX(6, 7) HGS_CX(0, 2) HGS_CX(1, 3) HGS_CX(4, 6)
+        HGS_CX(5, 7) HGS_CX(1, 2) HGS_CX(5, 6) HGS_CX(0, 4) HGS_CX(3, 7) HGS_CX(1, 5) HGS_CX(2, 6)
+        HGS_CX(1, 4) HGS_CX(3, 6) HGS_CX(2, 4) HGS_CX(3, 5) HGS_CX(3, 4)
+    } else if constexpr (KCAP == 6) {  // 12 comparators (checked on all 0/1 inputs)
+        HGS_CX(1, 2) HGS_CX(4, 5) HGS_CX(0, 2) HGS_CX(3, 5) HGS_CX(0, 1) HGS_CX(3, 4)
+        HGS_CX(2, 5) HGS_CX(0, 3) HGS_CX(1, 4) HGS_CX(2, 4) HGS_CX(1, 3) HGS_CX(2, 3)
+    } else {
+        HGS_CX(0, 1) HGS_CX(2, 3) HGS_CX(0, 2) HGS_CX(1, 3) HGS_CX(1, 2)
+    }
 #undef HGS_CX
 }
 
@@ -369,13 +376,19 @@ static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cu
 
 void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
                    cudaStream_t st) {
-    const bool local = kmax > 8;  // register fast path covers fanouts up to 8
-    if (philox) {
-        if (local) launch_expand_t<8, true, true>(threads, smem, ep, st);
-        else launch_expand_t<8, true, false>(threads, smem, ep, st);
-    } else {
-        if (local) launch_expand_t<8, false, true>(threads, smem, ep, st);
+    // register fast path for k <= 8, sized to the call's largest choice
+    if (kmax > 8) {
+        if (philox) launch_expand_t<8, true, true>(threads, smem, ep, st);
+        else launch_expand_t<8, false, true>(threads, smem, ep, st);
+    } else if (kmax > 6) {
+        if (philox) launch_expand_t<8, true, false>(threads, smem, ep, st);
         else launch_expand_t<8, false, false>(threads, smem, ep, st);
+    } else if (kmax > 4) {
+        if (philox) launch_expand_t<6, true, false>(threads, smem, ep, st);
+        else launch_expand_t<6, false, false>(threads, smem, ep, st);
+    } else {
+        if (philox) launch_expand_t<4, true, false>(threads, smem, ep, st);
+        else launch_expand_t<4, false, false>(threads, smem, ep, st);
     }
 }
 
