@@ -172,6 +172,33 @@ def test_clustered_vertex_ids(n, w, outliers, depth, fanout):
         assert_same(dev, ref, True)
 
 
+@pytest.mark.parametrize("n,m", [(3_000_000, 24_000_000), (9_000_000, 30_000_000)])
+def test_large_graph_subset(n, m):
+    """Multi-million-vertex graphs: packed hash entries near the 32-bit limit
+    (3M) and the unpacked (vertex, rank) path (9M > 2^23), 64-bit CSR sizes
+    on the host side; 512 roots against the oracle."""
+    rs = np.random.default_rng(n)
+    # rows as random ascending progressions: canonical CSR in O(m), no sort
+    deg = rs.poisson(m / n, n).astype(np.int64)
+    step = rs.integers(1, 64, n)
+    start = rs.integers(0, np.maximum(1, n - deg * step))
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    j = np.arange(rp[-1], dtype=np.int64) - np.repeat(rp[:-1], deg)
+    v = np.repeat(start, deg) + j * np.repeat(step, deg)
+    g = O.Graph(n=n, rp=rp, ci=v)
+    g.node_feat = (np.arange(n * 6, dtype=np.float64) * 0.25).reshape(n, 6)
+    g.edge_feat = (np.arange(len(v) * 2, dtype=np.float64) * 0.125).reshape(len(v), 2)
+    g.labels = (v % 2).astype(np.uint8)
+    roots = np.concatenate([rs.choice(n, 256, replace=False) for _ in range(2)]).astype(np.int64)
+    boff = np.array([0, 256, 512], np.int64)
+    seeds = rs.integers(0, 2**63, 512, dtype=np.uint64)
+    for rng in (0, 1):
+        kw = dict(rng=rng, depth=3, fanout=6)
+        dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert_same(dev, ref, True)
+
+
 @pytest.mark.parametrize("rng", [0, 1])
 def test_resumed_streams(rng):
     """Non-fresh sources (rng_state): xoshiro states / Philox decision bases."""
