@@ -328,8 +328,13 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
                 *dst = make_int2(rowsh | j, HAS_GID ? __ldg(p.a_gid + kk) : kk);
             edc += __popc(hb);
         };
+// Windows per group and whether groups are double-buffered: swept on B200
+// at C2 (G = 2, 4 double-buffered, 5-8 single): 6 single-buffered is best.
 #ifndef HGS_K2_G
-#define HGS_K2_G 4
+#define HGS_K2_G 6
+#endif
+#ifndef HGS_K2_SINGLE
+#define HGS_K2_SINGLE 1
 #endif
         constexpr int G = HGS_K2_G;  // windows in flight per group
         auto fetch = [&](int w, int (&rs)[G], int (&kk)[G], uint32_t (&v)[G]) {
@@ -357,8 +362,8 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
         };
         int w = 0;
         if (direct) {
-            // full groups, software-pipelined: the column loads of group g+1
-            // are in flight while group g is probed and emitted
+            // full groups: G windows' column loads in flight together (or, with
+            // double buffering, group g+1's loads during group g's probes)
             const int nfg = (S >> 5) / G;
 #if HGS_K2_SINGLE
             for (int gi = 0; gi < nfg; ++gi) {
