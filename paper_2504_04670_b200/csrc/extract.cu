@@ -41,10 +41,11 @@ struct HashSet;
 template <>
 struct HashSet<true> {
     uint32_t* slot;
-    uint32_t bmask, rmask;
-    int bits, rb;
+    uint32_t nb, rmask;  // nb buckets of 4 slots (any count)
+    int rb;
     static constexpr int kBytesPerSlot = 4;
-    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
+    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return __umulhi(v * 0x9E3779B1u, nb); }
+    __device__ __forceinline__ uint32_t next(uint32_t b) const { return b + 1 == nb ? 0u : b + 1; }
     __device__ __forceinline__ void clear(int nslots) const {
         for (int i = lane_id(); i < nslots / 4; i += 32)
             reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
@@ -59,7 +60,7 @@ struct HashSet<true> {
                 if (prev == kEmpty) return true;
                 if ((prev ^ hi) <= rmask) return false;
             }
-            b = (b + 1) & bmask;
+            b = next(b);
         }
     }
     __device__ __forceinline__ int find_slot(uint32_t v) const {
@@ -72,7 +73,7 @@ struct HashSet<true> {
             if ((q.z ^ hi) <= rmask) return 4 * b + 2;
             if ((q.w ^ hi) <= rmask) return 4 * b + 3;
             if (q.w == kEmpty) return -1;
-            b = (b + 1) & bmask;
+            b = next(b);
         }
     }
     __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)] = (v << rb) | r; }
@@ -86,7 +87,7 @@ struct HashSet<true> {
         uint32_t d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
         if (d > rmask && q.w != kEmpty) {  // full bucket without a match: rare
             do {
-                b = (b + 1) & bmask;
+                b = next(b);
                 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
                 d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
             } while (d > rmask && q.w != kEmpty);
@@ -98,10 +99,11 @@ struct HashSet<true> {
 template <>
 struct HashSet<false> {
     uint2* slot;  // (vertex, rank)
-    uint32_t bmask, rmask;
-    int bits, rb;
+    uint32_t nb, rmask;
+    int rb;
     static constexpr int kBytesPerSlot = 8;
-    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return (v * 0x9E3779B1u) >> (32 - bits); }
+    __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return __umulhi(v * 0x9E3779B1u, nb); }
+    __device__ __forceinline__ uint32_t next(uint32_t b) const { return b + 1 == nb ? 0u : b + 1; }
     __device__ __forceinline__ void clear(int nslots) const {
         for (int i = lane_id(); i < nslots; i += 32) slot[i] = make_uint2(kEmpty, 0);
     }
@@ -114,7 +116,7 @@ struct HashSet<false> {
                 if (prev == kEmpty) return true;
                 if (prev == v) return false;
             }
-            b = (b + 1) & bmask;
+            b = next(b);
         }
     }
     __device__ __forceinline__ int find_slot(uint32_t v) const {
@@ -127,7 +129,7 @@ struct HashSet<false> {
             if (q1.x == v) return 4 * b + 2;
             if (q1.z == v) return 4 * b + 3;
             if (q1.z == kEmpty) return -1;
-            b = (b + 1) & bmask;
+            b = next(b);
         }
     }
     __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)].y = r; }
@@ -142,7 +144,7 @@ struct HashSet<false> {
             r = (q0.z == v) ? (int)q0.w : r;
             r = (q0.x == v) ? (int)q0.y : r;
             if (r >= 0 || q1.z == kEmpty) return r;
-            b = (b + 1) & bmask;
+            b = next(b);
         }
     }
 };
@@ -160,12 +162,15 @@ struct HashSet<false> {
 //   tmp    row_cap+36 x i32  bucketed keys -> row starts (+ sentinels)
 //   aux    row_cap x int2  bucket counters -> per nonempty row (A pos - flat pos, rank<<16)
 template <bool PACKED, bool HAS_GID>
-__global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
+#ifndef HGS_K2_MINB
+#define HGS_K2_MINB 6  // CTAs per SM the register budget is sized for (80 registers; 7 CTAs at 72 measured slower)
+#endif
+__global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
     unsigned char* q = smem_raw + (size_t)warp * p.warp_bytes;
-    const int nslots = 4 << p.nb_bits;
+    const int nslots = 4 * p.n_buckets;
     HashSet<PACKED> hs;
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
     q += HashSet<PACKED>::kBytesPerSlot * nslots;
@@ -176,8 +181,7 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
     int32_t* rstart = tmp;
     int32_t* cnt = (int32_t*)q;
     int2* rinfo = (int2*)q;
-    hs.bits = p.nb_bits;
-    hs.bmask = (1u << p.nb_bits) - 1u;
+    hs.nb = (uint32_t)p.n_buckets;
     hs.rb = p.rank_bits;
     hs.rmask = (1u << p.rank_bits) - 1u;
     const unsigned lt = (1u << lane) - 1u;
@@ -299,19 +303,8 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
         if (lane == 0) rstart[NR] = S;
         __syncwarp();
 
-        // ---- window cursors: row holding the first entry of each 32-window
         for (int i = NR + 1 + lane; i <= NR + 32; i += 32) rstart[i] = 0x7fffffff;  // sentinels
         const int nwin = (S + 31) >> 5;
-        const bool direct = nwin <= p.win_cap;
-        if (direct) {
-            for (int w = lane; w < nwin; w += 32) wmask[w] = 0u;
-            __syncwarp();
-            for (int qi = lane; qi < NR; qi += 32) {
-                const int s0 = rstart[qi], s1 = rstart[qi + 1];
-                if (s0 & 31) atomicOr(&wmask[s0 >> 5], 1u << (s0 & 31));
-                for (int w = (s0 + 31) >> 5; (w << 5) < s1; ++w) wcur[w] = (uint16_t)qi;
-            }
-        }
         __syncwarp();
 
         // ---- induced subgraph: scan the flattened rows in 32-entry windows
@@ -337,10 +330,11 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
 #define HGS_K2_SINGLE 1
 #endif
         constexpr int G = HGS_K2_G;  // windows in flight per group
+        int wb = 0;  // first window of the current pass (window info is pass-local)
         auto fetch = [&](int w, int (&rs)[G], int (&kk)[G], uint32_t (&v)[G]) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
-                const int own = (int)wcur[w + u] + __popc(wmask[w + u] & le);
+                const int own = (int)wcur[w + u - wb] + __popc(wmask[w + u - wb] & le);
                 const int2 ri = rinfo[own];
                 kk[u] = ((w + u) << 5) + lane + ri.x;
                 rs[u] = ri.y;
@@ -360,58 +354,58 @@ __global__ void __launch_bounds__(128, 6) k_extract(ExtractParams p) {
                 for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::true_type{});
             }
         };
-        int w = 0;
-        if (direct) {
+        // Windows go in passes of win_cap: per pass, the row cursor of each
+        // window and a bitmask of row starts inside it (one u32 + one u16 per
+        // window, in the dead key array), then the scan.
+        for (; wb < nwin; wb += p.win_cap) {
+            const int we = min(nwin, wb + p.win_cap);
+            for (int w = lane; w < we - wb; w += 32) wmask[w] = 0u;
+            __syncwarp();
+            for (int qi = lane; qi < NR; qi += 32) {
+                const int s0 = rstart[qi], s1 = rstart[qi + 1];
+                const int w0 = s0 >> 5;
+                if ((s0 & 31) && w0 >= wb && w0 < we) atomicOr(&wmask[w0 - wb], 1u << (s0 & 31));
+                for (int w = max((s0 + 31) >> 5, wb); w < we && (w << 5) < s1; ++w) wcur[w - wb] = (uint16_t)qi;
+            }
+            __syncwarp();
             // full groups: G windows' column loads in flight together (or, with
             // double buffering, group g+1's loads during group g's probes)
-            const int nfg = (S >> 5) / G;
+            const int wfull = min(we, S >> 5);  // windows of the pass with 32 entries
+            const int nfg = max(0, wfull - wb) / G;
+            int w = wb;
 #if HGS_K2_SINGLE
             for (int gi = 0; gi < nfg; ++gi) {
                 int rsA[G], kkA[G];
                 uint32_t vA[G];
-                fetch(gi * G, rsA, kkA, vA);
+                fetch(wb + gi * G, rsA, kkA, vA);
                 consume(rsA, kkA, vA);
             }
-            w = nfg * G;
+            w = wb + nfg * G;
 #else
             if (nfg > 0) {
                 int rsA[G], kkA[G], rsB[G], kkB[G];
                 uint32_t vA[G], vB[G];
-                fetch(0, rsA, kkA, vA);
+                fetch(wb, rsA, kkA, vA);
                 for (int gi = 0; gi < nfg; gi += 2) {
-                    if (gi + 1 < nfg) fetch((gi + 1) * G, rsB, kkB, vB);
+                    if (gi + 1 < nfg) fetch(wb + (gi + 1) * G, rsB, kkB, vB);
                     consume(rsA, kkA, vA);
                     if (gi + 1 < nfg) {
-                        if (gi + 2 < nfg) fetch((gi + 2) * G, rsA, kkA, vA);
+                        if (gi + 2 < nfg) fetch(wb + (gi + 2) * G, rsA, kkA, vA);
                         consume(rsB, kkB, vB);
                     }
                 }
-                w = nfg * G;
+                w = wb + nfg * G;
             }
 #endif
-            for (; w < nwin; ++w) {  // < G trailing windows, the last one partial
+            for (; w < we; ++w) {  // < G trailing windows, the last one possibly partial
                 const int base = w << 5;
-                const int own = min((int)wcur[w] + __popc(wmask[w] & le), NR - 1);
+                const int own = min((int)wcur[w - wb] + __popc(wmask[w - wb] & le), NR - 1);
                 const int2 ri = rinfo[own];
                 const int kk = base + lane < S ? base + lane + ri.x : -1;
                 const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
                 emit(j, ri.y, kk, std::true_type{});
             }
-        } else {
-            int cursor = 0;  // huge sets: serial window cursor
-            for (; w < nwin; ++w) {
-                const int base = w << 5;
-                const int c = cursor;
-                const int off = rstart[c + 1 + lane] - base;
-                const unsigned bit = ((unsigned)(off - 1) < 31u) ? (1u << off) : 0u;
-                const int own = min(c + __popc(__reduce_or_sync(kFull, bit) & le), NR - 1);
-                const int own31 = __shfl_sync(kFull, own, 31);
-                cursor = (rstart[own31 + 1] == base + 32) ? own31 + 1 : own31;
-                const int2 ri = rinfo[own];
-                const int kk = base + lane < S ? base + lane + ri.x : -1;
-                const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
-                emit(j, ri.y, kk, std::true_type{});
-            }
+            __syncwarp();
         }
         const int count = (int)(edc - ed);
         if (lane == 0) {

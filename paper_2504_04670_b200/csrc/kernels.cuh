@@ -77,7 +77,7 @@ struct ExtractParams {
     int2* __restrict__ escratch;        // per root: e_stride x (local i<<16 | j, edge id)
     int32_t e_stride;
     int32_t* __restrict__ ticket;
-    int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
+    int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
     int32_t cnt_lg;                     // log2 of the bucket-counter capacity (<= 2*row_cap)
     int32_t* __restrict__ work;         // root counter (zeroed before each launch)
 };

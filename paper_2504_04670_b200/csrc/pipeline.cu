@@ -32,7 +32,7 @@ struct CallPlan {
     int expand_threads;
     size_t expand_smem;
     int32_t recip_smem;
-    int32_t nb_bits, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
+    int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
 };
 
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
@@ -57,23 +57,25 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
             c.expand_threads = 128;
         }
     }
-    // K2 hash set: 4-slot buckets, HGS_HASH_SLOTS_PER_KEY (default 4) slots per
-    // possible key; entries pack (vertex << rank_bits | rank) into 32 bits when
-    // vertex ids leave room, else (vertex, rank) 64-bit pairs.
-    int spk = 3;
-    if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) spk = std::max(2, atoi(e));
+    // K2 per-warp shared memory: hash set + keys + row starts + row info.
+    // Entries pack (vertex << rank_bits | rank) into 32 bits when vertex ids
+    // leave room, else (vertex, rank) pairs. The hash (4-slot buckets, any
+    // count) takes what is left of a 6-CTA-per-SM budget when that still
+    // gives >= 2.5 slots per possible key; otherwise 3 slots per key.
     c.rank_bits = 1;
     while (((int64_t)1 << c.rank_bits) < c.max_t) ++c.rank_bits;
     c.packed = (n + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
-    int bits = 2;
-    while (((int64_t)4 << bits) < spk * c.max_t) ++bits;
-    c.nb_bits = bits;
-    c.set_cap = (int32_t)((c.max_t + 31) / 32 * 32);
-    c.row_cap = (int32_t)((c.max_t + 31) / 32 * 32);
-    c.win_cap = c.set_cap * 2 / 3;  // (u32 mask + u16 cursor) per window alias the set array
-    const size_t slots = (size_t)4 << c.nb_bits;
-    size_t bytes = (c.packed ? 4 : 8) * slots + 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) +
-                   8 * (size_t)c.row_cap;
+    c.set_cap = (int32_t)std::max<int64_t>(16, (c.max_t + 3) / 4 * 4);  // >= 16: bucket counters need 32 ints
+    c.row_cap = c.set_cap;
+    c.win_cap = 4 * c.set_cap / 6;  // windows per pass: (u32 mask + u16 cursor) each, in the set array
+    const size_t rest = 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) + 8 * (size_t)c.row_cap;
+    const size_t bucket_bytes = c.packed ? 16 : 32;
+    const size_t budget = (233472 / 6 - 1024) / 4 / 16 * 16;  // per warp, 6 CTAs of 4 warps
+    int64_t nb = budget > rest ? (int64_t)((budget - rest) / bucket_bytes) : 0;
+    if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) nb = (atoi(e) * c.max_t + 3) / 4;
+    if (4 * nb * 2 < 5 * c.max_t) nb = (3 * c.max_t + 3) / 4;
+    c.n_buckets = (int32_t)std::max<int64_t>(nb, 2);
+    size_t bytes = bucket_bytes * (size_t)c.n_buckets + rest;
     bytes = (bytes + 15) / 16 * 16;
     c.warp_bytes = (int32_t)bytes;
     if (4 * bytes > 200 * 1024) fail(HGS_ERANGE, "hgs: per-root working set too large for shared memory");
@@ -164,7 +166,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t;
     xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
     xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
-    xp.ticket = s->ticket.p; xp.nb_bits = c.nb_bits; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
+    xp.ticket = s->ticket.p; xp.n_buckets = c.n_buckets; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
     xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
     xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
     const size_t xsmem = (size_t)4 * c.warp_bytes;
