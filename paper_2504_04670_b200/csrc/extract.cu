@@ -38,12 +38,18 @@ constexpr uint32_t kEmpty = 0xffffffffu;
 template <bool PACKED>
 struct HashSet;
 
+#ifndef HGS_K2_BW
+#define HGS_K2_BW 4  // slots per bucket of the packed hash (2: one 8-byte LDS per probe)
+#endif
 template <>
 struct HashSet<true> {
+    static constexpr int BW = HGS_K2_BW;
+    using Vec = std::conditional_t<BW == 4, uint4, uint2>;
     uint32_t* slot;
-    uint32_t nb, rmask;  // nb buckets of 4 slots (any count)
+    uint32_t nb, rmask;  // nb buckets of BW slots (any count)
     int rb;
     static constexpr int kBytesPerSlot = 4;
+    __device__ __forceinline__ void set_buckets(uint32_t nb4) { nb = nb4 * (4 / BW); }
     __device__ __forceinline__ uint32_t bucket(uint32_t v) const { return __umulhi(v * 0x9E3779B1u, nb); }
     __device__ __forceinline__ uint32_t next(uint32_t b) const { return b + 1 == nb ? 0u : b + 1; }
     __device__ __forceinline__ void clear(int nslots) const {
@@ -55,8 +61,8 @@ struct HashSet<true> {
         uint32_t b = bucket(v);
         for (;;) {
 #pragma unroll
-            for (int s = 0; s < 4; ++s) {
-                const uint32_t prev = atomicCAS(slot + 4 * b + s, kEmpty, e);
+            for (int s = 0; s < BW; ++s) {
+                const uint32_t prev = atomicCAS(slot + BW * b + s, kEmpty, e);
                 if (prev == kEmpty) return true;
                 if ((prev ^ hi) <= rmask) return false;
             }
@@ -67,30 +73,34 @@ struct HashSet<true> {
         const uint32_t hi = v << rb;
         uint32_t b = bucket(v);
         for (;;) {
-            const uint4 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
-            if ((q.x ^ hi) <= rmask) return 4 * b;
-            if ((q.y ^ hi) <= rmask) return 4 * b + 1;
-            if ((q.z ^ hi) <= rmask) return 4 * b + 2;
-            if ((q.w ^ hi) <= rmask) return 4 * b + 3;
-            if (q.w == kEmpty) return -1;
+#pragma unroll
+            for (int s = 0; s < BW; ++s)
+                if ((slot[BW * b + s] ^ hi) <= rmask) return BW * b + s;
+            if (slot[BW * b + BW - 1] == kEmpty) return -1;
             b = next(b);
         }
     }
     __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)] = (v << rb) | r; }
+    __device__ __forceinline__ static uint32_t bmin(const uint4& q, uint32_t hi) {
+        return min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
+    }
+    __device__ __forceinline__ static uint32_t bmin(const uint2& q, uint32_t hi) { return min(q.x ^ hi, q.y ^ hi); }
+    __device__ __forceinline__ static uint32_t blast(const uint4& q) { return q.w; }
+    __device__ __forceinline__ static uint32_t blast(const uint2& q) { return q.y; }
     // (entry ^ (v << rb)) is the entry's rank for the matching entry and
     // exceeds rmask for every other entry (keys are distinct), so the
     // bucket's minimum decides a hit without per-slot branches.
     __device__ __forceinline__ int find_rank(uint32_t v) const {
         const uint32_t hi = v << rb;
         uint32_t b = bucket(v);
-        uint4 q = *reinterpret_cast<const uint4*>(slot + 4 * b);
-        uint32_t d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
-        if (d > rmask && q.w != kEmpty) {  // full bucket without a match: rare
+        Vec q = *reinterpret_cast<const Vec*>(slot + BW * b);
+        uint32_t d = bmin(q, hi);
+        if (d > rmask && blast(q) != kEmpty) {  // full bucket without a match: rare
             do {
                 b = next(b);
-                q = *reinterpret_cast<const uint4*>(slot + 4 * b);
-                d = min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
-            } while (d > rmask && q.w != kEmpty);
+                q = *reinterpret_cast<const Vec*>(slot + BW * b);
+                d = bmin(q, hi);
+            } while (d > rmask && blast(q) != kEmpty);
         }
         return d <= rmask ? (int)d : -1;
     }
@@ -181,7 +191,8 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
     int32_t* rstart = tmp;
     int32_t* cnt = (int32_t*)q;
     int2* rinfo = (int2*)q;
-    hs.nb = (uint32_t)p.n_buckets;
+    if constexpr (PACKED) hs.set_buckets((uint32_t)p.n_buckets);
+    else hs.nb = (uint32_t)p.n_buckets;
     hs.rb = p.rank_bits;
     hs.rmask = (1u << p.rank_bits) - 1u;
     const unsigned lt = (1u << lane) - 1u;
