@@ -249,8 +249,11 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         launch_pack((int)std::max<int64_t>(pgrid, 1), pp, pst);
         ++s->launches;
         if (cfg.gather) {  // this chunk's vertices / edges
-            const int gblocks = split ? std::max<int64_t>(1, std::min<int64_t>(sm_count(g.device) * 8, Rc * 4))
-                                      : sm_count(g.device) * 8;
+#ifndef HGS_GATHER_BPSM
+#define HGS_GATHER_BPSM 8
+#endif
+            const int gblocks = split ? std::max<int64_t>(1, std::min<int64_t>(sm_count(g.device) * HGS_GATHER_BPSM, Rc * 4))
+                                      : sm_count(g.device) * HGS_GATHER_BPSM;
             launch_gather_packed(gblocks, pp, g.erec.p, s->root_voff.p + r0, s->root_voff.p + r1,
                                  s->root_eoff.p + r0, s->root_eoff.p + r1, pst);
             s->launches += 2;
