@@ -168,7 +168,7 @@ struct HashSet<false> {
 // Per-warp shared memory of K2 (set_cap == row_cap == max tree size rounded
 // up to 32; the regions are reused phase by phase):
 //   hash   4<<nb_bits slots                   vertex -> rank
-//   keys   set_cap x i32   unsorted keys -> sorted keys -> window masks/cursors
+//   keys   set_cap x i32   unsorted keys -> sorted keys -> per-window (mask, cursor)
 //   tmp    row_cap+36 x i32  bucketed keys -> row starts (+ sentinels)
 //   aux    row_cap x int2  bucket counters -> per nonempty row (A pos - flat pos, rank<<16)
 template <bool PACKED, bool HAS_GID>
@@ -185,8 +185,7 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
     q += HashSet<PACKED>::kBytesPerSlot * nslots;
     int32_t* keys = (int32_t*)q; q += 4 * p.set_cap;
-    uint32_t* wmask = reinterpret_cast<uint32_t*>(keys);
-    uint16_t* wcur = reinterpret_cast<uint16_t*>(keys + p.win_cap);
+    uint2* winfo = reinterpret_cast<uint2*>(keys);  // per window: (row-start mask, cursor row)
     int32_t* tmp = (int32_t*)q; q += 4 * (p.row_cap + 36);
     int32_t* rstart = tmp;
     int32_t* cnt = (int32_t*)q;
@@ -345,7 +344,8 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         auto fetch = [&](int w, int (&rs)[G], int (&kk)[G], uint32_t (&v)[G]) {
 #pragma unroll
             for (int u = 0; u < G; ++u) {
-                const int own = (int)wcur[w + u - wb] + __popc(wmask[w + u - wb] & le);
+                const uint2 wi = winfo[w + u - wb];
+                const int own = (int)wi.y + __popc(wi.x & le);
                 const int2 ri = rinfo[own];
                 kk[u] = ((w + u) << 5) + lane + ri.x;
                 rs[u] = ri.y;
@@ -370,13 +370,13 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         // window, in the dead key array), then the scan.
         for (; wb < nwin; wb += p.win_cap) {
             const int we = min(nwin, wb + p.win_cap);
-            for (int w = lane; w < we - wb; w += 32) wmask[w] = 0u;
+            for (int w = lane; w < we - wb; w += 32) winfo[w].x = 0u;
             __syncwarp();
             for (int qi = lane; qi < NR; qi += 32) {
                 const int s0 = rstart[qi], s1 = rstart[qi + 1];
                 const int w0 = s0 >> 5;
-                if ((s0 & 31) && w0 >= wb && w0 < we) atomicOr(&wmask[w0 - wb], 1u << (s0 & 31));
-                for (int w = max((s0 + 31) >> 5, wb); w < we && (w << 5) < s1; ++w) wcur[w - wb] = (uint16_t)qi;
+                if ((s0 & 31) && w0 >= wb && w0 < we) atomicOr(&winfo[w0 - wb].x, 1u << (s0 & 31));
+                for (int w = max((s0 + 31) >> 5, wb); w < we && (w << 5) < s1; ++w) winfo[w - wb].y = (uint32_t)qi;
             }
             __syncwarp();
             // full groups: G windows' column loads in flight together (or, with
@@ -410,7 +410,8 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
 #endif
             for (; w < we; ++w) {  // < G trailing windows, the last one possibly partial
                 const int base = w << 5;
-                const int own = min((int)wcur[w - wb] + __popc(wmask[w - wb] & le), NR - 1);
+                const uint2 wi = winfo[w - wb];
+                const int own = min((int)wi.y + __popc(wi.x & le), NR - 1);
                 const int2 ri = rinfo[own];
                 const int kk = base + lane < S ? base + lane + ri.x : -1;
                 const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;

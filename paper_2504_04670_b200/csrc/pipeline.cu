@@ -67,7 +67,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     c.packed = (n + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
     c.set_cap = (int32_t)std::max<int64_t>(16, (c.max_t + 3) / 4 * 4);  // >= 16: bucket counters need 32 ints
     c.row_cap = c.set_cap;
-    c.win_cap = 4 * c.set_cap / 6;  // windows per pass: (u32 mask + u16 cursor) each, in the set array
+    c.win_cap = c.set_cap / 2;  // windows per pass: (u32 mask, u32 cursor) each, in the set array
     const size_t rest = 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) + 8 * (size_t)c.row_cap;
     const size_t bucket_bytes = c.packed ? 16 : 32;
     const size_t budget = (233472 / 6 - 1024) / 4 / 16 * 16;  // per warp, 6 CTAs of 4 warps
