@@ -330,7 +330,8 @@ def run_gpu(args, world, rank, local_rank):
     total_ms = float(sum(step_ms))
     e2e_total = float(sum(e2e_s))
     if world > 1:
-        t = torch.tensor([total_ms, e2e_total], device=dev, dtype=torch.float64)
+        t = torch.tensor([total_ms, e2e_total], device=dev if dist.get_backend() == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         total_ms, e2e_total = float(t[0]), float(t[1])
     if rank != 0:
@@ -439,7 +440,8 @@ def run_epoch(args, world, rank, local_rank):
     total_ms = float(sum(ms))
     mbs = sum(t["minibatches"] for t in tots)
     if world > 1:
-        t = torch.tensor([total_ms, float(mbs)], device=dev, dtype=torch.float64)
+        t = torch.tensor([total_ms, float(mbs)], device=dev if dist.get_backend() == "nccl" else "cpu",
+                         dtype=torch.float64)
         dist.all_reduce(t[0:1], op=dist.ReduceOp.MAX)
         dist.all_reduce(t[1:2], op=dist.ReduceOp.SUM)
         total_ms, mbs = float(t[0]), int(t[1])
@@ -479,6 +481,11 @@ def main():
     world = int(os.environ.get("WORLD_SIZE", "1"))
     rank = int(os.environ.get("RANK", "0"))
     local_rank = int(os.environ.get("LOCAL_RANK", "0"))
+    # test hook: run several ranks on one GPU over gloo (exercises the
+    # multi-rank timing / reduction path where only one GPU is available)
+    backend = os.environ.get("HGS_DIST_BACKEND", "nccl")
+    if os.environ.get("HGS_FORCE_DEVICE") is not None:
+        local_rank = int(os.environ["HGS_FORCE_DEVICE"])
     set_workload(args.workload, world)
     if args.e2e_steps is None:
         args.e2e_steps = args.warmup + args.steps if args.workload in ("C1", "C2") else 3
@@ -489,7 +496,10 @@ def main():
         import torch
         import torch.distributed as dist
         torch.cuda.set_device(local_rank)
-        dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        if backend == "nccl":
+            dist.init_process_group("nccl", device_id=torch.device("cuda", local_rank))
+        else:
+            dist.init_process_group(backend)
     try:
         if args.workload == "C5":
             run_epoch(args, world, rank, local_rank)
