@@ -199,6 +199,40 @@ def test_large_graph_subset(n, m):
         assert_same(dev, ref, True)
 
 
+@pytest.mark.parametrize("depth,fanout", [(2, 6), (3, 4), (2, 40)])
+def test_hub_rows_many_windows(depth, fanout):
+    """Hubs with out-degree in the thousands: a root's scanned entries span
+    many K2 window passes (more than one pass of win_cap windows), and wide
+    fanouts take the local-memory choose path."""
+    rs = np.random.default_rng(depth * 100 + fanout)
+    n = 3000
+    edges = set()
+    hubs = rs.choice(n, 12, replace=False)
+    for h in hubs:
+        for v in rs.choice(n, 2500, replace=False):
+            if v != h:
+                edges.add((int(h), int(v)))
+    for _ in range(20000):
+        u, v = rs.integers(0, n, 2)
+        if u != v:
+            edges.add((int(u), int(v)))
+    e = np.array(sorted(edges), np.int64)
+    rp = np.concatenate([[0], np.cumsum(np.bincount(e[:, 0], minlength=n))]).astype(np.int64)
+    g = O.Graph(n=n, rp=rp, ci=e[:, 1].copy())
+    g.node_feat = rs.standard_normal((n, 6))
+    g.edge_feat = rs.standard_normal((len(e), 2))
+    g.labels = rs.integers(0, 2, len(e)).astype(np.uint8)
+    roots = np.concatenate([hubs[:6], rs.choice(n, 90, replace=False)]).astype(np.int64)
+    roots = np.unique(roots)
+    boff = np.array([0, len(roots) // 2, len(roots)], np.int64)
+    seeds = rs.integers(0, 2**63, len(roots), dtype=np.uint64)
+    for rng in (0, 1):
+        kw = dict(rng=rng, depth=depth, fanout=fanout)
+        dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert_same(dev, ref, True)
+
+
 @pytest.mark.parametrize("rng", [0, 1])
 def test_resumed_streams(rng):
     """Non-fresh sources (rng_state): xoshiro states / Philox decision bases."""
