@@ -44,7 +44,7 @@ struct HashSet;
 template <>
 struct HashSet<true> {
     static constexpr int BW = HGS_K2_BW;
-    using Vec = std::conditional_t<BW == 4, uint4, uint2>;
+    using Vec = std::conditional_t<BW == 4, uint4, std::conditional_t<BW == 2, uint2, uint32_t>>;
     uint32_t* slot;
     uint32_t nb, rmask;  // nb buckets of BW slots (any count)
     int rb;
@@ -85,6 +85,8 @@ struct HashSet<true> {
         return min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
     }
     __device__ __forceinline__ static uint32_t bmin(const uint2& q, uint32_t hi) { return min(q.x ^ hi, q.y ^ hi); }
+    __device__ __forceinline__ static uint32_t bmin(const uint32_t& q, uint32_t hi) { return q ^ hi; }
+    __device__ __forceinline__ static uint32_t blast(const uint32_t& q) { return q; }
     __device__ __forceinline__ static uint32_t blast(const uint4& q) { return q.w; }
     __device__ __forceinline__ static uint32_t blast(const uint2& q) { return q.y; }
     // (entry ^ (v << rb)) is the entry's rank for the matching entry and
