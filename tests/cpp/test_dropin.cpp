@@ -3,7 +3,9 @@
 // (Trainer::epoch_minibatch, trainer.cpp:433-459; cmd_bench_sampling,
 // cli.cpp:393-430), checked against the C oracle (oracle/liboracle.so).
 // Prints "ALL OK" on success; needs a GPU.
+#include <algorithm>
 #include <cmath>
+#include <memory>
 #include <cstdio>
 #include <cstring>
 #include <stdexcept>
@@ -235,6 +237,64 @@ int main() {
         CHECK(expect_throw<std::invalid_argument>([&] { coo_to_csr(dups); }) != "<no exception>");
         const CsrMatrix round = coo_to_csr(csr_to_coo(adj));
         CHECK(round == adj);
+    }
+    {   // sample_rows (sampler.cpp:64-86) on the GPU vs the host choice sources,
+        // then both sources must continue identically (device draws replayed)
+        CsrMatrix p(6, 40);
+        p.row_ptr = {0, 5, 5, 17, 18, 30, 40};
+        for (Index i = 0; i < 40; ++i) p.col_idx.push_back(i % 40);
+        for (Index r = 0; r < 6; ++r) std::sort(p.col_idx.begin() + p.row_ptr[r], p.col_idx.begin() + p.row_ptr[r + 1]);
+        p.values.assign(40, 0.5);
+        const std::vector<Index> streams = {2, 0, 2, 1, 0, 2};
+        const std::vector<uint64_t> sd = {11, 22, 33};
+        for (int mode = 0; mode < 2; ++mode) {
+            std::unique_ptr<ChoiceSource> dev_src, host_src;
+            if (mode == 0) {
+                dev_src = std::make_unique<PerRootChoiceSource>(sd);
+                host_src = std::make_unique<PerRootChoiceSource>(sd);
+            } else {
+                dev_src = std::make_unique<PhiloxChoiceSource>(sd);
+                host_src = std::make_unique<PhiloxChoiceSource>(sd);
+            }
+            const auto got = sample_rows(p, 4, *dev_src, streams);
+            for (Index r = 0; r < 6; ++r) {
+                const auto sup = p.row_cols(r);
+                std::vector<Index> exp;
+                if (!sup.empty()) {
+                    host_src->begin_root((uint64_t)streams[r]);
+                    for (auto q : host_src->choose((uint32_t)sup.size(), std::min<uint32_t>(4, (uint32_t)sup.size())))
+                        exp.push_back(sup[q]);
+                }
+                CHECK(got[r] == exp);
+            }
+            for (uint64_t st = 0; st < 3; ++st) {
+                dev_src->begin_root(st);
+                host_src->begin_root(st);
+                CHECK(dev_src->choose(50, 5) == host_src->choose(50, 5));
+            }
+        }
+        PerRootChoiceSource src(sd);
+        CHECK(expect_throw<std::invalid_argument>([&] { sample_rows(p, 0, src, streams); }) ==
+              "sample_rows: s must be >= 1");
+    }
+    {   // FrontierObserver through the resident-event path: shapes of Q / F / P
+        gpu::DeviceEvent dev(event);
+        PerRootChoiceSource src(seeds);
+        Index levels = 0, prev_q = (Index)(k * b);
+        auto out = dev.bulk_shadow(batches, cfg, src, false, [&](Index level, const FrontierSet& fs) {
+            ++levels;
+            CHECK(level == levels);
+            CHECK(fs.f.n_rows == k * b && fs.q.n_cols == event.n);
+            CHECK(fs.p.n_rows == prev_q);  // P: one row per frontier row of the level before
+            for (Index r = 0; r < fs.p.n_rows; ++r) {
+                double sum = 0;
+                for (Index t = fs.p.row_ptr[r]; t < fs.p.row_ptr[r + 1]; ++t) sum += fs.p.values[t];
+                CHECK(fs.p.row_ptr[r + 1] == fs.p.row_ptr[r] || std::fabs(sum - 1.0) < 1e-12);
+            }
+            prev_q = fs.q.n_rows;
+        });
+        CHECK(levels == cfg.depth);
+        compare(out, oracle(adj, nullptr, batches, seeds, nullptr, 0, cfg), false, "bulk_shadow(observer)");
     }
     std::printf(failures ? "FAILURES: %d\n" : "ALL OK\n", failures);
     return failures ? 1 : 0;
