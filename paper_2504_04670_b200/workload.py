@@ -136,6 +136,18 @@ def dropin_frontiers(rp, ci, values, roots, batch_off, seeds, *, rng=0, depth=3,
     return out
 
 
+def save_event(path: str, ev: Event) -> None:
+    """Binary event file (numpy .npz: make_edge_id_matrix CSR, features,
+    labels) — the fast on-disk form of an EventGraph (§8f #2; the
+    reference's JSON write_event, data.cpp:270-302, is its slow twin)."""
+    np.savez(path, n=ev.n, rp=ev.rp, ci=ev.ci, nf=ev.node_feat, ef=ev.edge_feat, lab=ev.labels)
+
+
+def load_event(path: str) -> Event:
+    z = np.load(path)
+    return Event(n=int(z["n"]), rp=z["rp"], ci=z["ci"], node_feat=z["nf"], edge_feat=z["ef"], labels=z["lab"])
+
+
 def preset_event(name: str, event_id: int = 0) -> Event:
     """The preset's event. Large presets (C4: ~1-2 min to generate) are cached
     as .npz under $HGS_EVENT_CACHE (default /tmp/hgs_events): a convenience
@@ -147,13 +159,11 @@ def preset_event(name: str, event_id: int = 0) -> Event:
     key = "_".join(f"{k}{v}" for k, v in sorted(cfg.items())) + f"_e{event_id}"
     path = os.path.join(d, f"{name}_{hashlib.sha1(key.encode()).hexdigest()[:12]}.npz")
     if os.path.exists(path):
-        z = np.load(path)
-        return Event(n=int(z["n"]), rp=z["rp"], ci=z["ci"], node_feat=z["nf"], edge_feat=z["ef"],
-                     labels=z["lab"])
+        return load_event(path)
     ev = generate_event(**cfg, event_id=event_id)
     try:
         os.makedirs(d, exist_ok=True)
-        np.savez(path + ".tmp.npz", n=ev.n, rp=ev.rp, ci=ev.ci, nf=ev.node_feat, ef=ev.edge_feat, lab=ev.labels)
+        save_event(path + ".tmp.npz", ev)
         os.replace(path + ".tmp.npz", path)
     except OSError:
         pass

@@ -126,3 +126,14 @@ def test_generator_matches_reference_presets():
             assert np.array_equal(a.node_feat.view(np.uint64), r.node_feat.view(np.uint64))
             assert np.array_equal(a.edge_feat.view(np.uint64), r.edge_feat.view(np.uint64))
             assert np.array_equal(a.labels, r.labels)
+
+
+def test_event_save_load_roundtrip(tmp_path):
+    from paper_2504_04670_b200 import workload as W
+    ev = W.preset_event("C1")
+    f = str(tmp_path / "c1.npz")
+    W.save_event(f, ev)
+    ev2 = W.load_event(f)
+    assert ev2.n == ev.n and ev2.m == ev.m
+    for a in ("rp", "ci", "node_feat", "edge_feat", "labels"):
+        assert np.array_equal(getattr(ev, a), getattr(ev2, a)), a
