@@ -795,20 +795,33 @@ __global__ void k_stats(const int32_t* __restrict__ level_counts, int32_t depth,
 
 // ---- launchers -----------------------------------------------------------------
 
-void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st) {
+void launch_extract(int grid, int warps, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st) {
     auto kern = packed ? (xp.a_gid ? k_extract<true, true> : k_extract<true, false>)
                        : (xp.a_gid ? k_extract<false, true> : k_extract<false, false>);
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 128, smem, st>>>(xp);
+    kern<<<grid, 32 * warps, smem, st>>>(xp);
     HGS_CUDA(cudaGetLastError());
 }
 
-int extract_blocks_per_sm(size_t smem, bool packed) {
+int extract_blocks_per_sm(size_t smem, int warps, bool packed) {
     auto kern = packed ? k_extract<true, false> : k_extract<false, false>;
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
-    HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 128, smem));
+    HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
     return per_sm > 0 ? per_sm : 1;
+}
+
+__global__ void k_max_i32(const int32_t* __restrict__ x, int32_t n, int32_t* __restrict__ out) {
+    int32_t m = 0;
+    for (int i = blockIdx.x * blockDim.x + threadIdx.x; i < n; i += gridDim.x * blockDim.x) m = max(m, x[i]);
+    m = __reduce_max_sync(kFull, m);
+    if ((threadIdx.x & 31) == 0) atomicMax(out, m);
+}
+
+void launch_max_i32(const int32_t* x, int32_t n, int32_t* out, cudaStream_t st) {
+    HGS_CUDA(cudaMemsetAsync(out, 0, sizeof(int32_t), st));
+    k_max_i32<<<std::max(1, std::min(148 * 4, (n + 255) / 256)), 256, 0, st>>>(x, n, out);
+    HGS_CUDA(cudaGetLastError());
 }
 
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st) {

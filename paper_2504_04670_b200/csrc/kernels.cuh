@@ -112,8 +112,10 @@ struct PackParams {
     int32_t* __restrict__ ticket;
 };
 
-void launch_extract(int grid, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st);
-int extract_blocks_per_sm(size_t smem, bool packed);
+void launch_extract(int grid, int warps, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st);
+int extract_blocks_per_sm(size_t smem, int warps, bool packed);
+// *out = max(x[0..n)) (>= 0), on the device
+void launch_max_i32(const int32_t* x, int32_t n, int32_t* out, cudaStream_t st);
 // Exclusive scan of (V_r, E_r) over roots [r0, r1) into voff/eoff[r0..r1];
 // for r0 > 0 the carry-in is voff/eoff[r0] as written by the previous chunk.
 void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, int64_t* tmp, int32_t* voff,

@@ -33,7 +33,43 @@ struct CallPlan {
     size_t expand_smem;
     int32_t recip_smem;
     int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
+    int32_t k2_warps;  // warps per K2 CTA (0: not planned yet)
 };
+
+// K2 per-warp shared memory for sets of up to `bound` vertices: hash set +
+// keys + row starts + row info. Entries pack (vertex << rank_bits | rank)
+// into 32 bits when vertex ids leave room, else (vertex, rank) pairs. The
+// hash (4-slot buckets, any count) takes what is left of a 6-CTA-per-SM
+// budget when that still gives >= 2.5 slots per possible key; otherwise 3
+// slots per key. Big sets run with 2 or 1 warps per CTA (up to ~227 KB of
+// shared memory per warp). False when even one warp cannot hold a set.
+bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
+    c.rank_bits = 1;
+    while (((int64_t)1 << c.rank_bits) < bound) ++c.rank_bits;
+    c.packed = (n + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
+    c.set_cap = (int32_t)std::max<int64_t>(16, (bound + 3) / 4 * 4);  // >= 16: bucket counters need 32 ints
+    c.row_cap = c.set_cap;
+    c.win_cap = c.set_cap / 2;  // windows per pass: (u32 mask, u32 cursor) each, in the set array
+    const size_t rest = 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) + 8 * (size_t)c.row_cap;
+    const size_t bucket_bytes = c.packed ? 16 : 32;
+    const size_t budget = (233472 / 6 - 1024) / 4 / 16 * 16;  // per warp, 6 CTAs of 4 warps
+    int64_t nb = budget > rest ? (int64_t)((budget - rest) / bucket_bytes) : 0;
+    if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) nb = (atoi(e) * bound + 3) / 4;
+    if (4 * nb * 2 < 5 * bound) nb = (3 * bound + 3) / 4;
+    const size_t max_block = 232448;  // opt-in dynamic shared memory per CTA (227 KB)
+    c.k2_warps = 0;
+    for (int spk_min : {3, 2}) {  // very large sets: fall back to 2 slots per key
+        if (spk_min == 2) nb = (2 * bound + 3) / 4;
+        c.n_buckets = (int32_t)std::max<int64_t>(nb, 2);
+        size_t bytes = bucket_bytes * (size_t)c.n_buckets + rest;
+        bytes = (bytes + 15) / 16 * 16;
+        c.warp_bytes = (int32_t)bytes;
+        for (int w : {4, 2, 1})
+            if ((size_t)w * bytes <= max_block) { c.k2_warps = w; break; }
+        if (c.k2_warps > 0) break;
+    }
+    return c.k2_warps > 0;
+}
 
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
     CallPlan c{};
@@ -57,28 +93,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
             c.expand_threads = 128;
         }
     }
-    // K2 per-warp shared memory: hash set + keys + row starts + row info.
-    // Entries pack (vertex << rank_bits | rank) into 32 bits when vertex ids
-    // leave room, else (vertex, rank) pairs. The hash (4-slot buckets, any
-    // count) takes what is left of a 6-CTA-per-SM budget when that still
-    // gives >= 2.5 slots per possible key; otherwise 3 slots per key.
-    c.rank_bits = 1;
-    while (((int64_t)1 << c.rank_bits) < c.max_t) ++c.rank_bits;
-    c.packed = (n + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
-    c.set_cap = (int32_t)std::max<int64_t>(16, (c.max_t + 3) / 4 * 4);  // >= 16: bucket counters need 32 ints
-    c.row_cap = c.set_cap;
-    c.win_cap = c.set_cap / 2;  // windows per pass: (u32 mask, u32 cursor) each, in the set array
-    const size_t rest = 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) + 8 * (size_t)c.row_cap;
-    const size_t bucket_bytes = c.packed ? 16 : 32;
-    const size_t budget = (233472 / 6 - 1024) / 4 / 16 * 16;  // per warp, 6 CTAs of 4 warps
-    int64_t nb = budget > rest ? (int64_t)((budget - rest) / bucket_bytes) : 0;
-    if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) nb = (atoi(e) * c.max_t + 3) / 4;
-    if (4 * nb * 2 < 5 * c.max_t) nb = (3 * c.max_t + 3) / 4;
-    c.n_buckets = (int32_t)std::max<int64_t>(nb, 2);
-    size_t bytes = bucket_bytes * (size_t)c.n_buckets + rest;
-    bytes = (bytes + 15) / 16 * 16;
-    c.warp_bytes = (int32_t)bytes;
-    if (4 * bytes > 200 * 1024) fail(HGS_ERANGE, "hgs: per-root working set too large for shared memory");
+    if (!plan_extract(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
     (void)a;
     return c;
 }
@@ -99,7 +114,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     const DevCsr& walk = cfg.symmetrize ? g.walk_sym : (seq_walk ? g.full_pattern() : g.a);
     graph_ensure_recip(g, walk.max_deg);
     if (cfg.gather && !g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
-    const CallPlan c = plan_call(walk, g.a, g.n_rows, cfg.depth, cfg.fanout);
+    CallPlan c = plan_call(walk, g.a, g.n_rows, cfg.depth, cfg.fanout);
     const int64_t R = in.R, k = in.k;
     if (R * c.max_t >= ((int64_t)1 << 40)) fail(HGS_ERANGE, "hgs: too many roots for one call");
     cudaStream_t st = s->stream;
@@ -166,10 +181,12 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t;
     xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
     xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
-    xp.ticket = s->ticket.p; xp.n_buckets = c.n_buckets; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
-    xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
-    xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
-    const size_t xsmem = (size_t)4 * c.warp_bytes;
+    xp.ticket = s->ticket.p;
+    auto set_layout = [&]() {
+        xp.n_buckets = c.n_buckets; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
+        xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
+        xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
+    };
 
     PackParams pp{};
     pp.touched = s->touched.p; pp.stride = c.max_t; pp.root_voff = s->root_voff.p;
@@ -213,12 +230,26 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         HGS_CUDA(cudaEventRecord(s->chunk_ev[nchunks], st));  // aux waits for this call's inputs
         HGS_CUDA(cudaStreamWaitEvent(pst, s->chunk_ev[nchunks], 0));
     }
-    const int xper_sm = extract_blocks_per_sm(xsmem, c.packed != 0);
     if (R > 0) {  // K1 over all roots at once: one lane per root, its length is one root's chain
         ep.r0 = 0; ep.R = (int32_t)R;
         launch_expand(c.expand_threads, c.expand_smem, c.kmax, ep, cfg.rng == HGS_RNG_PHILOX, st);
         ++s->launches;
     }
+    if (c.k2_warps == 0 && R > 0) {
+        // the tree bound is too loose for K2's shared memory: size K2 for the
+        // largest touched list K1 actually produced (one host round trip)
+        launch_max_i32(s->tcount.p, (int32_t)R, s->ticket.p + 6, st);
+        int32_t tmax = 0;
+        HGS_CUDA(cudaMemcpyAsync(&tmax, s->ticket.p + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+        HGS_CUDA(cudaStreamSynchronize(st));
+        if (!plan_extract(c, std::max<int32_t>(tmax, 1), g.n_rows))
+            fail(HGS_ERANGE, "hgs: a root's touched set (" + std::to_string(tmax) +
+                                 " vertices) exceeds K2's shared memory; reduce depth/fanout");
+    }
+    if (c.k2_warps == 0) plan_extract(c, 1, g.n_rows);  // R == 0: nothing to extract
+    set_layout();
+    const size_t xsmem = (size_t)c.k2_warps * c.warp_bytes;
+    const int xper_sm = extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
     s->frontier_kept = (cfg.flags & HGS_FLAG_KEEP_FRONTIERS) != 0;
     if (s->frontier_kept && R > 0) {  // K2 sorts the touched lists in place
         s->frontier.reserve((size_t)R * c.max_t);
@@ -230,10 +261,12 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         const int32_t r0 = (int32_t)(ci * chunk), r1 = (int32_t)std::min<int64_t>(R, r0 + chunk);
         const int64_t Rc = r1 - r0;
         xp.r0 = r0; xp.R = r1;
-        const int64_t xgrid = split ? (Rc + 3) / 4 : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + 3) / 4);
+        const int64_t per_cta = c.k2_warps;
+        const int64_t xgrid = split ? (Rc + per_cta - 1) / per_cta
+                                    : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + per_cta - 1) / per_cta);
         xp.work = s->ticket.p + 5;
         HGS_CUDA(cudaMemsetAsync(xp.work, 0, sizeof(int32_t), st));
-        launch_extract((int)std::max<int64_t>(xgrid, 1), xsmem, xp, c.packed != 0, st);
+        launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);
         ++s->launches;
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
         launch_scan(s->root_nv.p, s->root_ne.p, r0, r1, s->scan_tmp.p, s->root_voff.p, s->root_eoff.p,

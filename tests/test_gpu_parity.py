@@ -233,6 +233,34 @@ def test_hub_rows_many_windows(depth, fanout):
         assert_same(dev, ref, True)
 
 
+@pytest.mark.parametrize("n,m,depth,fanout", [(4000, 120000, 3, 20), (20000, 300000, 4, 8), (3000, 60000, 5, 5)])
+def test_big_trees(n, m, depth, fanout):
+    """Tree bounds of 8k-20k vertices per root: K2 runs with 2 or 1 warps per
+    CTA, or is sized after K1 from the largest touched list it produced."""
+    g = random_graph(n, m, n + depth)
+    rs = np.random.default_rng(depth * fanout)
+    roots = rs.choice(n, 96, replace=False).astype(np.int64)
+    boff = np.array([0, 40, 96], np.int64)
+    seeds = rs.integers(0, 2**63, 96, dtype=np.uint64)
+    for rng in (0, 1):
+        kw = dict(rng=rng, depth=depth, fanout=fanout)
+        dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert_same(dev, ref, True)
+
+
+def test_oversize_sets_fail_loudly():
+    """A root whose touched list cannot fit one warp's shared memory (> ~9k
+    vertices) is a clear HGS_ERANGE, not a wrong answer."""
+    H = hgs()
+    g = random_graph(30000, 1500000, 3)
+    roots = np.arange(8, dtype=np.int64)
+    boff = np.array([0, 8], np.int64)
+    seeds = np.arange(8, dtype=np.uint64)
+    with pytest.raises(H.HgsRuntimeError, match="exceeds K2's shared memory"):
+        device_run(g, roots, boff, seeds, depth=3, fanout=30)
+
+
 @pytest.mark.parametrize("rng", [0, 1])
 def test_resumed_streams(rng):
     """Non-fresh sources (rng_state): xoshiro states / Philox decision bases."""
