@@ -173,15 +173,18 @@ struct HashSet<false> {
 //   keys   set_cap x i32   unsorted keys -> sorted keys -> per-window (mask, cursor)
 //   tmp    row_cap+36 x i32  bucketed keys -> row starts (+ sentinels)
 //   aux    row_cap x int2  bucket counters -> per nonempty row (A pos - flat pos, rank<<16)
-template <bool PACKED, bool HAS_GID>
 #ifndef HGS_K2_MINB
 #define HGS_K2_MINB 6  // CTAs per SM the register budget is sized for (80 registers; 7 CTAs at 72 measured slower)
 #endif
+// GMEM: the per-warp working set lives in a global scratch slot instead of
+// shared memory (sets too large for one warp's shared memory; slow, rare).
+template <bool PACKED, bool HAS_GID, bool GMEM>
 __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
     extern __shared__ __align__(16) unsigned char smem_raw[];
     const int lane = lane_id();
     const int warp = threadIdx.x >> 5;
-    unsigned char* q = smem_raw + (size_t)warp * p.warp_bytes;
+    unsigned char* q = GMEM ? p.gscratch + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * p.warp_bytes
+                            : smem_raw + (size_t)warp * p.warp_bytes;
     const int nslots = 4 * p.n_buckets;
     HashSet<PACKED> hs;
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
@@ -796,15 +799,22 @@ __global__ void k_stats(const int32_t* __restrict__ level_counts, int32_t depth,
 // ---- launchers -----------------------------------------------------------------
 
 void launch_extract(int grid, int warps, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st) {
-    auto kern = packed ? (xp.a_gid ? k_extract<true, true> : k_extract<true, false>)
-                       : (xp.a_gid ? k_extract<false, true> : k_extract<false, false>);
+    if (xp.gscratch) {  // working sets in global scratch: grid * warps slots of warp_bytes
+        auto kern = packed ? (xp.a_gid ? k_extract<true, true, true> : k_extract<true, false, true>)
+                           : (xp.a_gid ? k_extract<false, true, true> : k_extract<false, false, true>);
+        kern<<<grid, 32 * warps, 0, st>>>(xp);
+        HGS_CUDA(cudaGetLastError());
+        return;
+    }
+    auto kern = packed ? (xp.a_gid ? k_extract<true, true, false> : k_extract<true, false, false>)
+                       : (xp.a_gid ? k_extract<false, true, false> : k_extract<false, false, false>);
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     kern<<<grid, 32 * warps, smem, st>>>(xp);
     HGS_CUDA(cudaGetLastError());
 }
 
 int extract_blocks_per_sm(size_t smem, int warps, bool packed) {
-    auto kern = packed ? k_extract<true, false> : k_extract<false, false>;
+    auto kern = packed ? k_extract<true, false, false> : k_extract<false, false, false>;
     HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     int per_sm = 0;
     HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));

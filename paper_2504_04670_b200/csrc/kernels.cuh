@@ -80,6 +80,7 @@ struct ExtractParams {
     int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits;
     int32_t cnt_lg;                     // log2 of the bucket-counter capacity (<= 2*row_cap)
     int32_t* __restrict__ work;         // root counter (zeroed before each launch)
+    unsigned char* gscratch;            // nullable: per-warp working sets in global memory
 };
 
 // K3: packing + gather.

@@ -34,6 +34,7 @@ struct CallPlan {
     int32_t recip_smem;
     int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
     int32_t k2_warps;  // warps per K2 CTA (0: not planned yet)
+    bool k2_gmem;      // K2 working sets in global scratch (sets beyond shared memory)
 };
 
 // K2 per-warp shared memory for sets of up to `bound` vertices: hash set +
@@ -68,6 +69,7 @@ bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
             if ((size_t)w * bytes <= max_block) { c.k2_warps = w; break; }
         if (c.k2_warps > 0) break;
     }
+    c.k2_gmem = false;
     return c.k2_warps > 0;
 }
 
@@ -242,14 +244,34 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         int32_t tmax = 0;
         HGS_CUDA(cudaMemcpyAsync(&tmax, s->ticket.p + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         HGS_CUDA(cudaStreamSynchronize(st));
-        if (!plan_extract(c, std::max<int32_t>(tmax, 1), g.n_rows))
-            fail(HGS_ERANGE, "hgs: a root's touched set (" + std::to_string(tmax) +
-                                 " vertices) exceeds K2's shared memory; reduce depth/fanout");
+        if (!plan_extract(c, std::max<int32_t>(tmax, 1), g.n_rows)) {
+            // beyond one warp's shared memory: K2 keeps its working sets in
+            // a global scratch slot per warp (3 hash slots per key)
+            plan_extract(c, 1, g.n_rows);  // rank bits / packing for the real bound below
+            c.rank_bits = 1;
+            while (((int64_t)1 << c.rank_bits) < tmax) ++c.rank_bits;
+            c.packed = (g.n_rows + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
+            c.set_cap = (tmax + 3) / 4 * 4;
+            c.row_cap = c.set_cap;
+            c.win_cap = c.set_cap / 2;
+            c.n_buckets = (3 * tmax + 3) / 4;
+            const size_t bytes = (c.packed ? 16 : 32) * (size_t)c.n_buckets + 4 * (size_t)c.set_cap +
+                                 4 * (size_t)(c.row_cap + 36) + 8 * (size_t)c.row_cap;
+            c.warp_bytes = (int32_t)((bytes + 15) / 16 * 16);
+            c.k2_warps = 4;
+            c.k2_gmem = true;
+        }
     }
     if (c.k2_warps == 0) plan_extract(c, 1, g.n_rows);  // R == 0: nothing to extract
     set_layout();
-    const size_t xsmem = (size_t)c.k2_warps * c.warp_bytes;
-    const int xper_sm = extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
+    const size_t xsmem = c.k2_gmem ? 0 : (size_t)c.k2_warps * c.warp_bytes;
+    const int xper_sm = c.k2_gmem ? 2 : extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
+    xp.gscratch = nullptr;
+    if (c.k2_gmem) {
+        const size_t slots = (size_t)xper_sm * sm_count(g.device) * c.k2_warps;
+        s->k2g.reserve(slots * (size_t)c.warp_bytes);
+        xp.gscratch = s->k2g.p;
+    }
     s->frontier_kept = (cfg.flags & HGS_FLAG_KEEP_FRONTIERS) != 0;
     if (s->frontier_kept && R > 0) {  // K2 sorts the touched lists in place
         s->frontier.reserve((size_t)R * c.max_t);
@@ -262,8 +284,9 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         const int64_t Rc = r1 - r0;
         xp.r0 = r0; xp.R = r1;
         const int64_t per_cta = c.k2_warps;
-        const int64_t xgrid = split ? (Rc + per_cta - 1) / per_cta
-                                    : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + per_cta - 1) / per_cta);
+        const int64_t xgrid = (split && !c.k2_gmem)
+                                  ? (Rc + per_cta - 1) / per_cta
+                                  : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + per_cta - 1) / per_cta);
         xp.work = s->ticket.p + 5;
         HGS_CUDA(cudaMemsetAsync(xp.work, 0, sizeof(int32_t), st));
         launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);

@@ -249,16 +249,19 @@ def test_big_trees(n, m, depth, fanout):
         assert_same(dev, ref, True)
 
 
-def test_oversize_sets_fail_loudly():
-    """A root whose touched list cannot fit one warp's shared memory (> ~9k
-    vertices) is a clear HGS_ERANGE, not a wrong answer."""
-    H = hgs()
+def test_oversize_sets_global_scratch():
+    """Touched sets beyond one warp's shared memory (~9k vertices): K2 runs
+    with its working sets in global scratch; same results as the oracle."""
     g = random_graph(30000, 1500000, 3)
     roots = np.arange(8, dtype=np.int64)
-    boff = np.array([0, 8], np.int64)
+    boff = np.array([0, 3, 8], np.int64)
     seeds = np.arange(8, dtype=np.uint64)
-    with pytest.raises(H.HgsRuntimeError, match="exceeds K2's shared memory"):
-        device_run(g, roots, boff, seeds, depth=3, fanout=30)
+    for rng in (0, 1):
+        kw = dict(rng=rng, depth=3, fanout=30)
+        dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert ref.V > 8 * 9000 / 2  # really oversize
+        assert_same(dev, ref, True)
 
 
 @pytest.mark.parametrize("rng", [0, 1])
