@@ -236,6 +236,14 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             }
             U += __popc(fb);
         }
+        if (U > kMaxSet) {  // local ids would not fit the edge slots: report, skip the root
+            if (lane == 0) {
+                report(p.ticket, kErrSetRange, r, U);
+                p.root_nv[r] = 0; p.root_ne[r] = 0; p.root_rloc[r] = -1; p.root_scan[r] = 0;
+            }
+            __syncwarp();
+            continue;
+        }
         lo = __reduce_min_sync(kFull, lo);
         hi = __reduce_max_sync(kFull, hi);
         // ---- order-preserving buckets b = (v - lo) >> shift, ~2U of them

@@ -6,7 +6,9 @@
 
 namespace hgs {
 
-enum : int32_t { kErrNone = 0, kErrRootRange = 1, kErrNegative = 2, kErrOverflow = 3, kErrCapacity = 4 };
+enum : int32_t { kErrNone = 0, kErrRootRange = 1, kErrNegative = 2, kErrOverflow = 3, kErrCapacity = 4, kErrSetRange = 5 };
+// largest distinct vertex set of one root (16-bit local ids in K2's edge slots)
+constexpr int32_t kMaxSet = 32767;
 
 __device__ __forceinline__ void report(int32_t* t, int32_t code, int32_t a, int32_t b) {
     if (atomicCAS(&t[1], 0, code) == 0) {

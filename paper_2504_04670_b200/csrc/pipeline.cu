@@ -78,9 +78,11 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     c.kmax = std::min<int64_t>(fanout, walk.max_deg);
     if (c.kmax > 256) fail(HGS_ERANGE, "hgs: min(fanout, max degree) > 256 is not supported by this build");
     c.max_t = tree_bound(c.kmax, depth);
-    if (c.max_t > 32767)
-        fail(HGS_ERANGE, "hgs: per-root tree bound " + std::to_string(c.max_t) +
-                             " exceeds this build's limit (32767); reduce depth/fanout");
+    // The tree bound only sizes K1's touched slots; the limit that matters is
+    // a root's distinct vertex count (16-bit local ids in K2's edge slots),
+    // checked by K2 itself (kErrSetRange).
+    if (c.max_t > ((int64_t)1 << 30))
+        fail(HGS_ERANGE, "hgs: per-root tree bound " + std::to_string(c.max_t) + " is too large; reduce depth/fanout");
     c.cache_entries = tree_bound(c.kmax, depth - 1);
     c.recip_smem = walk.max_deg + 1 <= 4096 ? walk.max_deg + 1 : 0;
     const size_t rbytes = (size_t)c.recip_smem * sizeof(uint64_t);
@@ -95,7 +97,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
             c.expand_threads = 128;
         }
     }
-    if (!plan_extract(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
+    if (c.max_t > kMaxSet || !plan_extract(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
     (void)a;
     return c;
 }
@@ -144,7 +146,10 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     s->comp_off.reserve((size_t)(R + k) + 1);
     s->batch_voff.reserve((size_t)k + 1);
     s->batch_eoff.reserve((size_t)k + 1);
-    const size_t vneed = (size_t)std::max<int64_t>(1, R * c.max_t);
+    // initial output capacity: the tree bound, capped per root (a loose bound
+    // would reserve far more than any call produces; a call that needs more
+    // grows the capacity once and re-runs, see sample_finish)
+    const size_t vneed = (size_t)std::max<int64_t>(1, R * std::min<int64_t>(c.max_t, 4096));
     if (s->v_cap < vneed) s->v_cap = vneed;
     if (s->e_cap == 0) s->e_cap = s->v_cap * 2;
     s->l2g.reserve(s->v_cap);
@@ -343,6 +348,10 @@ void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) {
     if (code == kErrNegative)
         fail(HGS_EINVAL, "row_normalize: negative value in a visited walk row (root ordinal " +
                              std::to_string(s->h_state[2]) + ", level " + std::to_string(s->h_state[3]) + ")");
+    if (code == kErrSetRange)
+        fail(HGS_ERANGE, "hgs: root ordinal " + std::to_string(s->h_state[2]) + " induces a subgraph of " +
+                             std::to_string(s->h_state[3]) + " vertices; this build's per-root limit is " +
+                             std::to_string(kMaxSet) + " (reduce depth/fanout)");
     if (code == kErrOverflow)
         fail(HGS_ERANGE, "hgs: more than 2^31-1 sampled vertices/edges in one call; split the call");
     s->V = s->h_state[8];

@@ -54,7 +54,7 @@ def main():
         depth = int(rs.integers(1, 5))
         fanout = int(rs.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 20]))
         # keep the per-root tree bound sane for deep/wide draws
-        while sum(fanout ** l for l in range(depth + 1)) > 20000:
+        while sum(fanout ** l for l in range(depth + 1)) > 80000:
             depth -= 1
         sym = bool(rs.random() < 0.7)
         rng = int(rs.integers(0, 2))

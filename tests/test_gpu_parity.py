@@ -264,6 +264,40 @@ def test_oversize_sets_global_scratch():
         assert_same(dev, ref, True)
 
 
+@pytest.mark.parametrize("depth,fanout", [(4, 16), (3, 40), (6, 6)])
+def test_tree_bound_beyond_local_ids(depth, fanout):
+    """Tree bounds beyond 32,767 (d=4 s=16: 69,905; d=3 s=40: 65,641; d=6
+    s=6: 55,987) with actual sets well below it: K1's slots take the bound,
+    K2 is sized from the touched lists; same results as the oracle."""
+    g = random_graph(40000, 1000000, depth * fanout)
+    rs = np.random.default_rng(fanout)
+    roots = rs.choice(g.n, 24, replace=False).astype(np.int64)
+    boff = np.array([0, 10, 24], np.int64)
+    seeds = rs.integers(0, 2**63, 24, dtype=np.uint64)
+    for rng in (0, 1):
+        kw = dict(rng=rng, depth=depth, fanout=fanout)
+        dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+        ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+        assert_same(dev, ref, True)
+
+
+def test_set_beyond_local_ids_is_erange():
+    """A root whose induced subgraph has more than 32,767 vertices is
+    reported (HGS_ERANGE naming the root), not silently wrapped."""
+    H = hgs()
+    g = random_graph(60000, 3000000, 5)
+    G = H.Graph(g.rp, g.ci)
+    S = H.Sampler(G)
+    roots = np.array([5, 7], np.int64)
+    with pytest.raises(H.HgsRuntimeError, match="per-root limit is 32767"):
+        S.bulk_shadow(roots, np.array([0, 2], np.int64), np.arange(2, dtype=np.uint64),
+                      rng=0, depth=3, fanout=60)
+    # the handle stays usable
+    S.bulk_shadow(roots, np.array([0, 2], np.int64), np.arange(2, dtype=np.uint64), rng=0, depth=2, fanout=4)
+    S.close()
+    G.close()
+
+
 @pytest.mark.parametrize("rng", [0, 1])
 def test_resumed_streams(rng):
     """Non-fresh sources (rng_state): xoshiro states / Philox decision bases."""
