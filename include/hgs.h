@@ -223,8 +223,8 @@ int hgs_sample_launches(hgs_sample* s, int64_t* n);
  * columns. Rows on one stream are decided in row order; streams run in
  * parallel. seeds[n_streams]; rng_state as in hgs_sample_run (nullable).
  * Outputs: out_off[n_rows+1] (offsets of each row's choices), out_cols[...],
- * and per stream the RNG draws / choose calls consumed (nullable). Rows wider
- * than 256 with s > 256 are HGS_ERANGE. */
+ * and per stream the RNG draws / choose calls consumed (nullable). More than
+ * 2^24 choices per row is HGS_ERANGE. */
 int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
                     const double* values, int64_t s, int32_t rng, const uint64_t* seeds, int64_t n_streams,
                     const uint64_t* rng_state, const int64_t* row_streams, int64_t* out_off, int64_t* out_cols,

@@ -495,8 +495,9 @@ int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* r
             if (st < 0 || st >= n_streams) fail(HGS_EINVAL, std::string(src) + ": root ordinal out of range");
             ++cnt[st + 1];
         }
-        if (std::min<int64_t>(s, maxdeg) > 256)
-            fail(HGS_ERANGE, "hgs_sample_rows: more than 256 choices per row is not supported by this build");
+        const int64_t kmax = std::min<int64_t>(s, maxdeg);
+        if (kmax > ((int64_t)1 << 24))
+            fail(HGS_ERANGE, "hgs_sample_rows: more than 2^24 choices per row is not supported by this build");
         if (maxdeg >= ((int64_t)1 << 31)) fail(HGS_ERANGE, "hgs_sample_rows: row too wide");
         std::vector<int64_t> sptr{0}, sid, srows;
         std::vector<int64_t> start(cnt.size(), 0);
@@ -515,7 +516,7 @@ int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* r
             HGS_CUDA(cudaStreamCreateWithFlags(&st, cudaStreamNonBlocking));
             DevBuf<int64_t> d_rp, d_ci, d_srows, d_sptr, d_sid, d_off, d_out;
             DevBuf<uint64_t> d_seeds, d_state, d_recip;
-            DevBuf<uint32_t> d_draws, d_dec;
+            DevBuf<uint32_t> d_draws, d_dec, d_big;
             std::vector<uint64_t> recip((size_t)maxdeg + 1, 0);
             for (int64_t m = 1; m <= maxdeg; ++m) recip[m] = recip_of((uint64_t)m);
             auto up = [&](auto& buf, const auto* src_, size_t n) {
@@ -540,6 +541,11 @@ int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* r
             p.state = rng_state ? d_state.p : nullptr; p.recip = d_recip.p;
             p.fanout = (int32_t)std::min<int64_t>(s, 1 << 30); p.groups = (int32_t)groups;
             p.draws = d_draws.p; p.decisions = d_dec.p;
+            if (kmax > (int64_t)kLocalK) {
+                d_big.reserve((size_t)groups * 3 * (size_t)kmax);
+                p.big = d_big.p;
+                p.big_k = (int32_t)kmax;
+            }
             launch_sample_rows(p, rng == HGS_RNG_PHILOX, st);
             if (out_off[n_rows] > 0)
                 HGS_CUDA(cudaMemcpyAsync(out_cols, d_out.p, sizeof(int64_t) * out_off[n_rows], cudaMemcpyDeviceToHost, st));

@@ -114,11 +114,12 @@ __device__ __forceinline__ void choose_small(RootStream<PHILOX>& rs, uint32_t n,
 #undef HGS_CX
 }
 
-// Generic variant for large fanouts (local-memory arrays, k <= 256).
+// Generic variant for large fanouts: val holds slots [0, k), (dpos, dval)
+// the displaced slots >= k (at most k of them). Local-memory arrays for
+// k <= kLocalK, else a per-lane slot of global scratch (ChoiceScratch).
 template <bool PHILOX>
 __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
-                             const uint64_t* __restrict__ recip, uint32_t* val) {
-    uint32_t dpos[256], dval[256];
+                             const uint64_t* __restrict__ recip, uint32_t* val, uint32_t* dpos, uint32_t* dval) {
     int nd = 0;
     for (uint32_t q = 0; q < k; ++q) val[q] = q;
     for (uint32_t i = 0; i < k; ++i) {
@@ -237,8 +238,14 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
                 const uint32_t k = min((uint32_t)p.fanout, deg);
                 rs.begin_decision(ndec);
                 ++ndec;
-                uint32_t pos[256];
-                choose_local<PHILOX>(rs, deg, k, recip, pos);
+                uint32_t lpos[kLocalK], ldp[kLocalK], ldv[kLocalK];
+                uint32_t *pos = lpos, *dp = ldp, *dv = ldv;
+                if (k > kLocalK) {
+                    pos = p.big + (size_t)(r - p.r0) * 3 * p.big_k;
+                    dp = pos + p.big_k;
+                    dv = dp + p.big_k;
+                }
+                choose_local<PHILOX>(rs, deg, k, recip, pos, dp, dv);
                 for (uint32_t q = 0; q < k; ++q, ++T) {
                     if (in_cache) cache[(size_t)T * bd + ti].x = row.x + (int32_t)pos[q];
                     else out[T] = row.x + (int32_t)pos[q];
@@ -347,8 +354,14 @@ __global__ void __launch_bounds__(128) k_sample_rows(RowsParams p) {
             choose_small<8, PHILOX>(rs, deg, k, p.recip, pos);
             for (uint32_t q = 0; q < k; ++q) dst[q] = p.col[b + pos[q]];
         } else {
-            uint32_t pos[256];
-            choose_local<PHILOX>(rs, deg, k, p.recip, pos);
+            uint32_t lpos[kLocalK], ldp[kLocalK], ldv[kLocalK];
+            uint32_t *pos = lpos, *dp = ldp, *dv = ldv;
+            if (k > kLocalK) {
+                pos = p.big + (size_t)g * 3 * p.big_k;
+                dp = pos + p.big_k;
+                dv = dp + p.big_k;
+            }
+            choose_local<PHILOX>(rs, deg, k, p.recip, pos, dp, dv);
             for (uint32_t q = 0; q < k; ++q) dst[q] = p.col[b + pos[q]];
         }
     }

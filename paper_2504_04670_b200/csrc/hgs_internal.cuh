@@ -224,6 +224,7 @@ struct hgs_sample {
     // extract scratch + offsets
     hgs::DevBuf<int32_t> root_nv, root_ne, root_rloc;
     hgs::DevBuf<int2> escratch;
+    hgs::DevBuf<uint32_t> kbig;       // K1 choose() scratch for choices > kLocalK (wide rows only)
     hgs::DevBuf<unsigned char> k2g;  // K2 working sets in global memory (oversized sets only)
     int32_t e_stride = 512;
     hgs::DevBuf<int64_t> scan_tmp;

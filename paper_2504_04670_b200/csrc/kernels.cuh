@@ -9,6 +9,9 @@ namespace hgs {
 enum : int32_t { kErrNone = 0, kErrRootRange = 1, kErrNegative = 2, kErrOverflow = 3, kErrCapacity = 4, kErrSetRange = 5 };
 // largest distinct vertex set of one root (16-bit local ids in K2's edge slots)
 constexpr int32_t kMaxSet = 32767;
+// choose() keeps up to this many slots in local memory; larger choices use
+// a global scratch slot per lane (ExpandParams/RowsParams::big)
+constexpr uint32_t kLocalK = 256;
 
 __device__ __forceinline__ void report(int32_t* t, int32_t code, int32_t a, int32_t b) {
     if (atomicCAS(&t[1], 0, code) == 0) {
@@ -39,6 +42,8 @@ struct ExpandParams {
     uint32_t* __restrict__ draws;
     uint32_t* __restrict__ decisions;
     int32_t* __restrict__ ticket;         // [0] ticket, [1] error code, [2] root, [3] aux
+    uint32_t* __restrict__ big;           // choices > kLocalK: 3 x big_k words per root of the launch
+    int32_t big_k;
 };
 
 void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
@@ -59,6 +64,8 @@ struct RowsParams {
     int32_t fanout, groups;
     uint32_t* __restrict__ draws;         // per group
     uint32_t* __restrict__ decisions;
+    uint32_t* __restrict__ big;           // choices > kLocalK: 3 x big_k words per group
+    int32_t big_k;
 };
 void launch_sample_rows(const RowsParams& p, bool philox, cudaStream_t st);
 

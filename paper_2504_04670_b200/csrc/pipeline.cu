@@ -76,7 +76,8 @@ bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
     CallPlan c{};
     c.kmax = std::min<int64_t>(fanout, walk.max_deg);
-    if (c.kmax > 256) fail(HGS_ERANGE, "hgs: min(fanout, max degree) > 256 is not supported by this build");
+    if (c.kmax > ((int64_t)1 << 24))
+        fail(HGS_ERANGE, "hgs: min(fanout, max degree) > 2^24 is not supported by this build");
     c.max_t = tree_bound(c.kmax, depth);
     // The tree bound only sizes K1's touched slots; the limit that matters is
     // a root's distinct vertex count (16-bit local ids in K2's edge slots),
@@ -236,6 +237,12 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         pst = s->aux;
         HGS_CUDA(cudaEventRecord(s->chunk_ev[nchunks], st));  // aux waits for this call's inputs
         HGS_CUDA(cudaStreamWaitEvent(pst, s->chunk_ev[nchunks], 0));
+    }
+    ep.big = nullptr; ep.big_k = 0;
+    if (c.kmax > (int64_t)kLocalK && R > 0) {  // wide choices: a global scratch slot per root
+        ep.big_k = (int32_t)c.kmax;
+        s->kbig.reserve((size_t)R * 3 * (size_t)c.kmax);
+        ep.big = s->kbig.p;
     }
     if (R > 0) {  // K1 over all roots at once: one lane per root, its length is one root's chain
         ep.r0 = 0; ep.R = (int32_t)R;

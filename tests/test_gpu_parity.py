@@ -199,11 +199,12 @@ def test_large_graph_subset(n, m):
         assert_same(dev, ref, True)
 
 
-@pytest.mark.parametrize("depth,fanout", [(2, 6), (3, 4), (2, 40)])
+@pytest.mark.parametrize("depth,fanout", [(2, 6), (3, 4), (2, 40), (2, 600)])
 def test_hub_rows_many_windows(depth, fanout):
     """Hubs with out-degree in the thousands: a root's scanned entries span
     many K2 window passes (more than one pass of win_cap windows), and wide
-    fanouts take the local-memory choose path."""
+    fanouts take the local-memory choose path (s=40) or, beyond 256 choices,
+    the global-scratch one (s=600)."""
     rs = np.random.default_rng(depth * 100 + fanout)
     n = 3000
     edges = set()
@@ -503,6 +504,24 @@ def test_sample_rows(rng, s):
         H.sample_rows(rp, ci, 0, seeds, streams)
     with pytest.raises(H.SamplerError, match="root ordinal out of range"):
         H.sample_rows(rp, ci, 2, seeds[:3], streams)
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_sample_rows_wide(rng):
+    """Rows of up to 2,000 entries with s=700: choices beyond 256 per row take
+    the global-scratch choose path; equals the oracle restatement."""
+    H = hgs()
+    rs = np.random.default_rng(7 + rng)
+    n = 60
+    deg = rs.integers(0, 2000, n)
+    rp = np.concatenate([[0], np.cumsum(deg)]).astype(np.int64)
+    ci = np.concatenate([np.sort(rs.choice(50000, d, replace=False)) for d in deg]).astype(np.int64)
+    seeds = rs.integers(0, 2**63, 9, dtype=np.uint64)
+    streams = rs.integers(0, 9, n).astype(np.int64)
+    off, cols, draws, decs = H.sample_rows(rp, ci, 700, seeds, streams, rng=rng, n_cols=50000)
+    ref, _, ndec, _ = O.sample_rows(rp, ci, 700, seeds, streams, rng=rng)
+    assert [cols[off[r]:off[r + 1]].tolist() for r in range(n)] == ref
+    assert np.array_equal(decs.astype(np.int64), ndec)
 
 
 def test_multi_handle_sharding_matches_single_call():
