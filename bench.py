@@ -415,9 +415,10 @@ def run_epoch(args, world, rank, local_rank):
               for e in evs]
     n_v = sum(e.n for e in evs)
     del evs
-    es = EP.EpochSampler(graphs, batch_size=BATCH, bulk_batches=K_BATCHES, depth=DEPTH, fanout=FANOUT, seed=1)
+    es = EP.EpochSampler(graphs, batch_size=BATCH, bulk_batches=args.bulk_batches, depth=DEPTH, fanout=FANOUT,
+                         seed=1)
     for i in range(args.warmup):
-        es.epoch(1000 + i, max_batches_per_event=K_BATCHES)
+        es.epoch(1000 + i, max_batches_per_event=es.k)
     torch.cuda.synchronize()
     if world > 1:
         dist.barrier()
@@ -452,7 +453,8 @@ def run_epoch(args, world, rank, local_rank):
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
             "config": {"workload": WORKLOAD_TEXT["C5"] + f": {args.events} events (generate_event C2 preset,"
-                                   f" event_id 0..{args.events - 1}), b={BATCH}, bulk_batches={K_BATCHES},"
+                                   f" event_id 0..{args.events - 1}), b={BATCH}, bulk_batches="
+                                   f"{args.bulk_batches or 'all batches of the event'},"
                                    f" {DEPTH}-hop, fanout {FANOUT}, with gather",
                        "events": args.events, "events_per_gpu": len(graphs), "vertices_per_gpu": n_v,
                        "minibatches_per_epoch": mbs // args.steps, "parallelism": f"events split over {world} GPU(s)",
@@ -472,6 +474,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--events", type=int, default=100, help="C5: events in the epoch (split over ranks)")
+    ap.add_argument("--bulk-batches", type=int, default=0,
+                    help="C5: minibatches per sampling call (0 = all batches of an event in one call)")
     ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"],
                     help="BASELINE.json config (C2 = the headline line)")
     ap.add_argument("--e2e-steps", type=int, default=None,

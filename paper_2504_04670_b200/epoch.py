@@ -41,9 +41,13 @@ class EpochSampler:
                  symmetrize: bool = True, rng: int = hgs.RNG_XOSHIRO, n_slots: int = 2):
         import torch
 
-        if batch_size < 1 or bulk_batches < 1:
-            raise hgs.SamplerError("SamplerConfig: batch_size and bulk_batches must be >= 1")
+        if batch_size < 1 or bulk_batches < 0:
+            raise hgs.SamplerError("SamplerConfig: batch_size must be >= 1 and bulk_batches >= 0")
         self.graphs = graphs
+        # bulk_batches=0: every batch of an event in one call (the epoch's
+        # minibatches bulk-sampled per event, BASELINE C5)
+        if bulk_batches == 0:
+            bulk_batches = max(g.n // batch_size + 1 for g in graphs)
         self.b, self.k = batch_size, bulk_batches
         self.seed = seed
         self.cfg = dict(depth=depth, fanout=fanout, symmetrize=symmetrize, rng=rng, gather=gather,
@@ -58,7 +62,9 @@ class EpochSampler:
         self.d_boff = [torch.empty(bulk_batches + 1, dtype=torch.int64, device="cuda") for _ in range(n_slots)]
         self.h_roots = [torch.empty(cap, dtype=torch.int32).pin_memory() for _ in range(n_slots)]
         self.h_boff = [torch.empty(bulk_batches + 1, dtype=torch.int64).pin_memory() for _ in range(n_slots)]
-        self._pool = cf.ThreadPoolExecutor(max_workers=1)
+        # host shuffles of upcoming events run ahead on a few worker threads
+        self.lookahead = 8
+        self._pool = cf.ThreadPoolExecutor(max_workers=4)
 
     def _sampler_for(self, slot: int, ev: int) -> hgs.Sampler:
         if self._slot_graph[slot] != ev:  # keep the workspace, switch the event
@@ -71,9 +77,8 @@ class EpochSampler:
         once a chunk's results are ready (device views valid until the slot is
         reused). Returns totals."""
         events = list(range(len(self.graphs))) if events is None else list(events)
-        nb_of = lambda e: self.graphs[e].n  # noqa: E731
-        fut = self._pool.submit(W.trainer_epoch_batches, nb_of(events[0]), self.b, self.seed, epoch, events[0]) \
-            if events else None
+        shuffle = lambda e: W.trainer_epoch_perm(self.graphs[e].n, self.b, self.seed, epoch, e)  # noqa: E731
+        futs = [self._pool.submit(shuffle, e) for e in events[:self.lookahead]]
         pending: list[Chunk | None] = [None] * len(self.slots)
         tot = dict(minibatches=0, roots=0, V=0, E=0, calls=0)
         slot = 0
@@ -90,31 +95,29 @@ class EpochSampler:
             pending[s] = None
 
         for i, ev in enumerate(events):
-            batches = fut.result()
-            if i + 1 < len(events):
-                fut = self._pool.submit(W.trainer_epoch_batches, nb_of(events[i + 1]), self.b, self.seed, epoch,
-                                        events[i + 1])
+            perm, nb, size = futs[i].result()
+            futs[i] = None
+            if i + self.lookahead < len(events):
+                futs.append(self._pool.submit(shuffle, events[i + self.lookahead]))
             if max_batches_per_event > 0:
-                batches = batches[:max_batches_per_event]
-            for b0 in range(0, len(batches), self.k):
-                chunk = batches[b0:b0 + self.k]
+                nb = min(nb, max_batches_per_event)
+            for b0 in range(0, nb, self.k):
+                kc = min(self.k, nb - b0)
+                R = kc * size
                 finish(slot)
                 S = self._sampler_for(slot, ev)
-                sizes = [len(x) for x in chunk]
-                R = int(sum(sizes))
                 hr, hb = self.h_roots[slot].numpy(), self.h_boff[slot].numpy()
-                hr[:R] = np.concatenate(chunk)
-                hb[0] = 0
-                hb[1:len(chunk) + 1] = np.cumsum(sizes)
+                hr[:R] = perm[b0 * size:b0 * size + R]
+                hb[:kc + 1] = np.arange(kc + 1, dtype=np.int64) * size
                 st = self.streams[slot]
                 with self._torch.cuda.stream(st):
                     self.d_roots[slot][:R].copy_(self.h_roots[slot][:R], non_blocking=True)
-                    self.d_boff[slot][:len(chunk) + 1].copy_(self.h_boff[slot][:len(chunk) + 1], non_blocking=True)
+                    self.d_boff[slot][:kc + 1].copy_(self.h_boff[slot][:kc + 1], non_blocking=True)
                 spec = hgs.trainer_seed_spec(self.seed, epoch, ev, batch_base=b0)
-                S.run_device_spec(self.d_roots[slot].data_ptr(), self.d_boff[slot].data_ptr(), R, len(chunk),
+                S.run_device_spec(self.d_roots[slot].data_ptr(), self.d_boff[slot].data_ptr(), R, kc,
                                   spec, **self.cfg)
-                pending[slot] = Chunk(ev, b0, len(chunk), S, hgs.SampleCounts(R, len(chunk), 0, 0))
-                tot["minibatches"] += len(chunk)
+                pending[slot] = Chunk(ev, b0, kc, S, hgs.SampleCounts(R, kc, 0, 0))
+                tot["minibatches"] += kc
                 tot["roots"] += R
                 tot["calls"] += 1
                 slot = (slot + 1) % len(self.slots)

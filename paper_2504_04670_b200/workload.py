@@ -178,6 +178,16 @@ def epoch_root_batches(n: int, b: int, rng_seed: int) -> list[np.ndarray]:
     return [perm[i * size:(i + 1) * size] for i in range(nb)]
 
 
+def epoch_root_perm(n: int, b: int, rng_seed: int) -> tuple[np.ndarray, int, int]:
+    """epoch_root_batches as one contiguous int32 array: (perm, n_batches,
+    batch size); batch i is perm[i*size:(i+1)*size]. The C shuffle runs
+    without the GIL, so several events can be shuffled in parallel."""
+    perm = np.zeros(n, np.int64)
+    nb = int(tools().hgs_epoch_root_batches(n, b, rng_seed, perm.ctypes.data))
+    size = n if n < b else b
+    return perm[:nb * size].astype(np.int32), nb, size
+
+
 def derive_grid(seed: int, prefix, k: int, b: int) -> np.ndarray:
     pre = np.ascontiguousarray(prefix, np.uint64)
     out = np.zeros(k * b, np.uint64)
@@ -192,6 +202,11 @@ def trainer_epoch_batches(n: int, b: int, seed: int, epoch: int, event: int = 0)
     """Trainer::epoch_minibatch's roots for one (epoch, event) (trainer.cpp:433-437):
     epoch_root_batches(n, b, roots_rng(seed, epoch, event))."""
     return epoch_root_batches(n, b, hgs.derive(seed, [STREAM_ROOTS, epoch, event]))
+
+
+def trainer_epoch_perm(n: int, b: int, seed: int, epoch: int, event: int = 0):
+    """trainer_epoch_batches as (contiguous int32 perm, n_batches, size)."""
+    return epoch_root_perm(n, b, hgs.derive(seed, [STREAM_ROOTS, epoch, event]))
 
 
 def trainer_roots(n: int, b: int, k: int, seed: int = 1, epoch0: int = 0, event: int = 0):
