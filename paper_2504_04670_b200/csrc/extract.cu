@@ -660,10 +660,10 @@ __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__
         const int q2 = f_v >> 1;
         const int64_t n2 = V * q2;
         const bool magic = n2 < ((int64_t)1 << 32);
-        const double2* src = reinterpret_cast<const double2*>(node_feat);
-        double2* dst = reinterpret_cast<double2*>(xv);
+        const uint4* src = reinterpret_cast<const uint4*>(node_feat);
+        uint4* dst = reinterpret_cast<uint4*>(xv);
         for (int64_t e0 = V0 * q2 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += stride * U) {
-            double2 x[U];
+            uint4 x[U];
 #pragma unroll
             for (int u = 0; u < U; ++u) {
                 const int64_t e = e0 + stride * u;
@@ -695,17 +695,18 @@ __global__ void __launch_bounds__(256) k_gather_edges_rec(const uint4* __restric
     const int64_t E0 = min((int64_t)*eb_, e_cap), E = min((int64_t)*ee, e_cap);
     const int64_t stride = (int64_t)gridDim.x * blockDim.x;
     constexpr int U = HGS_GATHER_U;
+    const uint64_t pol = l2_keep_policy();
     for (int64_t t0 = E0 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; t0 < E; t0 += stride * U) {
         int32_t g[U];
 #pragma unroll
-        for (int u = 0; u < U; ++u) g[u] = t0 + stride * u < E ? __ldg(e_gid + t0 + stride * u) : 0;
+        for (int u = 0; u < U; ++u) g[u] = t0 + stride * u < E ? __ldcs(e_gid + t0 + stride * u) : 0;
         uint4 f[U];
         uint32_t lb[U];
 #pragma unroll
         for (int u = 0; u < U; ++u) {
             if (t0 + stride * u < E) {
-                f[u] = __ldg(erec + 2 * (int64_t)g[u]);
-                lb[u] = __ldg(&erec[2 * (int64_t)g[u] + 1].x);
+                f[u] = ldg_keep(erec + 2 * (int64_t)g[u], pol);
+                lb[u] = ldg_keep(&erec[2 * (int64_t)g[u] + 1].x, pol);
             }
         }
 #pragma unroll
@@ -713,7 +714,7 @@ __global__ void __launch_bounds__(256) k_gather_edges_rec(const uint4* __restric
             const int64_t t = t0 + stride * u;
             if (t < E) {
                 __stcs(ye + t, f[u]);
-                lab[t] = (uint8_t)lb[u];
+                __stcs(lab + t, (uint8_t)lb[u]);
             }
         }
     }

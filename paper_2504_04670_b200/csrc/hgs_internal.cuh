@@ -27,6 +27,44 @@ struct Failure : std::runtime_error {
     } while (0)
 
 // Grow-only device buffer.
+// L2 residency hints for the gathers: the feature tables are re-read ~10x
+// per call by random rows while the outputs stream past them, so table loads
+// carry an evict_last policy and output stores are evict-first (.cs).
+#ifndef HGS_GATHER_HINT
+#define HGS_GATHER_HINT 1
+#endif
+#ifndef HGS_KEEP_FRAC
+#define HGS_KEEP_FRAC 1.0
+#endif
+__device__ __forceinline__ uint64_t l2_keep_policy() {
+    uint64_t p = 0;
+#if HGS_GATHER_HINT
+    asm("createpolicy.fractional.L2::evict_last.b64 %0, %1;" : "=l"(p) : "f"((float)HGS_KEEP_FRAC));
+#endif
+    return p;
+}
+__device__ __forceinline__ uint4 ldg_keep(const uint4* a, uint64_t pol) {
+#if HGS_GATHER_HINT
+    uint4 r;
+    asm volatile("ld.global.nc.L2::cache_hint.v4.u32 {%0, %1, %2, %3}, [%4], %5;"
+                 : "=r"(r.x), "=r"(r.y), "=r"(r.z), "=r"(r.w) : "l"(a), "l"(pol));
+    return r;
+#else
+    (void)pol;
+    return __ldg(a);
+#endif
+}
+__device__ __forceinline__ uint32_t ldg_keep(const uint32_t* a, uint64_t pol) {
+#if HGS_GATHER_HINT
+    uint32_t r;
+    asm volatile("ld.global.nc.L2::cache_hint.u32 %0, [%1], %2;" : "=r"(r) : "l"(a), "l"(pol));
+    return r;
+#else
+    (void)pol;
+    return __ldg(a);
+#endif
+}
+
 template <class T>
 struct DevBuf {
     T* p = nullptr;
