@@ -52,7 +52,7 @@ def main():
     while time.time() - t0 < secs:
         g = make_graph(rs)
         depth = int(rs.integers(1, 5))
-        fanout = int(rs.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 20]))
+        fanout = int(rs.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 20, 40, 300]))
         # keep the per-root tree bound sane for deep/wide draws
         while sum(fanout ** l for l in range(depth + 1)) > 80000:
             depth -= 1
