@@ -564,6 +564,59 @@ void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, i
 
 int64_t scan_tmp_words(int64_t R) { return 2 * ((R + kPairTile - 1) / kPairTile) + 4; }
 
+// Small calls (R <= kSmallScan, one chunk): the offset scan and the batch
+// offsets (k_finalize's work) in one CTA, replacing four launches that each
+// cost more than their work at this size.
+constexpr int kSmallScanPer = 16;
+constexpr int kSmallScan = 1024 * kSmallScanPer;
+__global__ void __launch_bounds__(1024) k_scan_small(const int32_t* __restrict__ nv, const int32_t* __restrict__ ne,
+                                                     int32_t R, int32_t* __restrict__ voff, int32_t* __restrict__ eoff,
+                                                     int32_t* __restrict__ ticket, const int64_t* __restrict__ batch_off,
+                                                     int32_t k, int32_t* __restrict__ batch_voff,
+                                                     int32_t* __restrict__ batch_eoff, int32_t* __restrict__ comp_off) {
+    __shared__ int64_t sh[66];
+    constexpr int P = kSmallScanPer;
+    const int base = threadIdx.x * P;
+    int32_t x[P], y[P];
+    int64_t a = 0, b = 0;
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        x[i] = base + i < R ? nv[base + i] : 0;
+        y[i] = base + i < R ? ne[base + i] : 0;
+        a += x[i];
+        b += y[i];
+    }
+    int64_t ta, tb;
+    block_scan_pair(a, b, sh, ta, tb);
+#pragma unroll
+    for (int i = 0; i < P; ++i) {
+        if (base + i < R) { voff[base + i] = (int32_t)a; eoff[base + i] = (int32_t)b; }
+        a += x[i];
+        b += y[i];
+    }
+    if (threadIdx.x == 0) {
+        voff[R] = (int32_t)ta;
+        eoff[R] = (int32_t)tb;
+        if (ta > 0x7fffffff || tb > 0x7fffffff) report(ticket, kErrOverflow, 0, 0);
+    }
+    __syncthreads();  // the offsets above are visible to the whole CTA
+    for (int bi = threadIdx.x; bi <= k; bi += blockDim.x) {
+        const int64_t f = batch_off[bi];
+        batch_voff[bi] = voff[f];
+        batch_eoff[bi] = eoff[f];
+        if (bi < k && batch_off[bi + 1] == f) comp_off[f + bi] = 0;  // empty batch
+    }
+}
+
+bool launch_scan_small(const int32_t* nv, const int32_t* ne, int32_t R, int32_t* voff, int32_t* eoff, int32_t* ticket,
+                       const int64_t* batch_off, int32_t k, int32_t* bvoff, int32_t* beoff, int32_t* comp_off,
+                       cudaStream_t st) {
+    if (R > kSmallScan) return false;
+    k_scan_small<<<1, 1024, 0, st>>>(nv, ne, R, voff, eoff, ticket, batch_off, k, bvoff, beoff, comp_off);
+    HGS_CUDA(cudaGetLastError());
+    return true;
+}
+
 // ===========================================================================
 // K3
 // ===========================================================================

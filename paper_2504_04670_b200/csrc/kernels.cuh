@@ -128,6 +128,10 @@ int extract_blocks_per_sm(size_t smem, int warps, bool packed);
 void launch_max_i32(const int32_t* x, int32_t n, int32_t* out, cudaStream_t st);
 // Exclusive scan of (V_r, E_r) over roots [r0, r1) into voff/eoff[r0..r1];
 // for r0 > 0 the carry-in is voff/eoff[r0] as written by the previous chunk.
+// scan + batch offsets in one launch for R <= 16384 (false: use launch_scan + launch_finalize)
+bool launch_scan_small(const int32_t* nv, const int32_t* ne, int32_t R, int32_t* voff, int32_t* eoff, int32_t* ticket,
+                       const int64_t* batch_off, int32_t k, int32_t* bvoff, int32_t* beoff, int32_t* comp_off,
+                       cudaStream_t st);
 void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, int64_t* tmp, int32_t* voff,
                  int32_t* eoff, int32_t* ticket, cudaStream_t st);
 int64_t scan_tmp_words(int64_t R);

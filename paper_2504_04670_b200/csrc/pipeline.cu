@@ -291,6 +291,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
                                  cudaMemcpyDeviceToDevice, st));
     }
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[1], st));
+    bool small_scan = false;  // scan + batch offsets done by one small launch
     for (int64_t ci = 0; ci < nchunks; ++ci) {
         const int32_t r0 = (int32_t)(ci * chunk), r1 = (int32_t)std::min<int64_t>(R, r0 + chunk);
         const int64_t Rc = r1 - r0;
@@ -304,9 +305,16 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
         launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);
         ++s->launches;
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
-        launch_scan(s->root_nv.p, s->root_ne.p, r0, r1, s->scan_tmp.p, s->root_voff.p, s->root_eoff.p,
-                    s->ticket.p, st);
-        s->launches += 3;
+        if (!split && launch_scan_small(s->root_nv.p, s->root_ne.p, (int32_t)R, s->root_voff.p, s->root_eoff.p,
+                                        s->ticket.p, in.batch_off, (int32_t)k, s->batch_voff.p, s->batch_eoff.p,
+                                        s->comp_off.p, st)) {
+            small_scan = true;
+            s->launches += 1;
+        } else {
+            launch_scan(s->root_nv.p, s->root_ne.p, r0, r1, s->scan_tmp.p, s->root_voff.p, s->root_eoff.p,
+                        s->ticket.p, st);
+            s->launches += 3;
+        }
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[3], st));
         if (split) {
             HGS_CUDA(cudaEventRecord(s->chunk_ev[ci], st));
@@ -330,9 +338,11 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[4], st));
     if (R == 0 && s->profiled)
         for (int i = 2; i <= 3; ++i) HGS_CUDA(cudaEventRecord(s->ev[i], st));
-    launch_finalize(in.batch_off, (int32_t)k, (int32_t)R, s->root_voff.p, s->root_eoff.p, s->batch_voff.p,
-                    s->batch_eoff.p, s->comp_off.p, pst);
-    ++s->launches;
+    if (!small_scan) {
+        launch_finalize(in.batch_off, (int32_t)k, (int32_t)R, s->root_voff.p, s->root_eoff.p, s->batch_voff.p,
+                        s->batch_eoff.p, s->comp_off.p, pst);
+        ++s->launches;
+    }
     if (split) {  // join: the handle's stream sees the whole call
         HGS_CUDA(cudaEventRecord(s->chunk_ev[nchunks], pst));
         HGS_CUDA(cudaStreamWaitEvent(st, s->chunk_ev[nchunks], 0));
