@@ -344,13 +344,10 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 *dst = make_int2(rowsh | j, HAS_GID ? __ldg(p.a_gid + kk) : kk);
             edc += __popc(hb);
         };
-// Windows per group and whether groups are double-buffered: swept on B200
-// at C2 (G = 2, 4 double-buffered, 5-8 single): 6 single-buffered is best.
+// Windows per group: swept on B200 at C2 (G = 2 and 4 double-buffered,
+// 5-8 single-buffered): 6 single-buffered groups are best.
 #ifndef HGS_K2_G
 #define HGS_K2_G 6
-#endif
-#ifndef HGS_K2_SINGLE
-#define HGS_K2_SINGLE 1
 #endif
         constexpr int G = HGS_K2_G;  // windows in flight per group
         int wb = 0;  // first window of the current pass (window info is pass-local)
@@ -392,12 +389,10 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 for (int w = max((s0 + 31) >> 5, wb); w < we && (w << 5) < s1; ++w) winfo[w - wb].y = (uint32_t)qi;
             }
             __syncwarp();
-            // full groups: G windows' column loads in flight together (or, with
-            // double buffering, group g+1's loads during group g's probes)
+            // full groups: G windows' column loads in flight together
             const int wfull = min(we, S >> 5);  // windows of the pass with 32 entries
             const int nfg = max(0, wfull - wb) / G;
             int w = wb;
-#if HGS_K2_SINGLE
             for (int gi = 0; gi < nfg; ++gi) {
                 int rsA[G], kkA[G];
                 uint32_t vA[G];
@@ -405,22 +400,6 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 consume(rsA, kkA, vA);
             }
             w = wb + nfg * G;
-#else
-            if (nfg > 0) {
-                int rsA[G], kkA[G], rsB[G], kkB[G];
-                uint32_t vA[G], vB[G];
-                fetch(wb, rsA, kkA, vA);
-                for (int gi = 0; gi < nfg; gi += 2) {
-                    if (gi + 1 < nfg) fetch(wb + (gi + 1) * G, rsB, kkB, vB);
-                    consume(rsA, kkA, vA);
-                    if (gi + 1 < nfg) {
-                        if (gi + 2 < nfg) fetch(wb + (gi + 2) * G, rsA, kkA, vA);
-                        consume(rsB, kkB, vB);
-                    }
-                }
-                w = wb + nfg * G;
-            }
-#endif
             for (; w < we; ++w) {  // < G trailing windows, the last one possibly partial
                 const int base = w << 5;
                 const uint2 wi = winfo[w - wb];
