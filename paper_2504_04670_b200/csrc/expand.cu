@@ -1,4 +1,6 @@
-// expand.cu — K1: stacked-Q frontier expansion, one lane per root.
+// expand.cu — K1: stacked-Q frontier expansion, one lane per root
+// (k_expand; Philox mode with fanouts <= 8: k_expand_group, a few lanes per
+// root deciding a level's rows in parallel).
 //
 // Restates sample_rows + the expansion loop of bulk_shadow
 // (sampler.cpp:64-86, 160-184) per root: level by level, every frontier row v
@@ -329,6 +331,128 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
     p.decisions[r] = ndec - dec0;
 }
 
+// Philox mode, decision-parallel: decisions are numbered per root
+// (PhiloxChoiceSource), so the rows of one level are
+// independent once each knows its decision number (= the count of nonempty
+// rows before it in the root's level) and its children's offset (= the sum
+// of the earlier rows' choice counts). A group of kGroupLanes lanes takes a
+// root and walks each level kGroupLanes rows at a time; segmented scans over
+// the group give both numbers. Same outputs as k_expand<., true, .>.
+#ifndef HGS_K1_GL
+#define HGS_K1_GL 4
+#endif
+constexpr int kGroupLanes = HGS_K1_GL;
+template <int KCAP>
+__global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
+    extern __shared__ uint64_t srecip_g[];
+    const uint64_t* recip = p.recip;
+    if (p.recip_smem > 0) {
+        for (int i = threadIdx.x; i < p.recip_smem; i += blockDim.x) srecip_g[i] = p.recip[i];
+        __syncthreads();
+        recip = srecip_g;
+    }
+    constexpr int GL = kGroupLanes;
+    const int gl = threadIdx.x & (GL - 1);
+    const unsigned gmask = ((1u << GL) - 1u) << (threadIdx.x & 31 & ~(GL - 1));
+    const int r = p.r0 + (int)((blockIdx.x * blockDim.x + threadIdx.x) / GL);
+    if (r >= p.R) return;  // whole groups leave together
+    const int32_t root = p.roots32 ? p.roots32[r] : (int32_t)p.roots64[r];
+    if (root < 0 || root >= p.n) {
+        if (gl == 0) {
+            report(p.ticket, kErrRootRange, r, root);
+            p.tcount[r] = 0;
+        }
+        return;
+    }
+    uint64_t seed;
+    if (p.seeds) seed = p.seeds[r];
+    else {
+        int lo = 0, hi = p.k - 1;
+        while (lo < hi) {
+            const int mid = (lo + hi + 1) >> 1;
+            if (__ldg(p.batch_off + mid) <= r) lo = mid; else hi = mid - 1;
+        }
+        uint64_t path[8];
+        for (int i = 0; i < 6; ++i) path[i] = p.spec.path[i];
+        const int len = p.spec.path_len;
+        path[len] = (uint64_t)(p.spec.batch_base + lo);
+        path[len + 1] = (uint64_t)(r - __ldg(p.batch_off + lo));
+        seed = derive_seed(p.spec.seed, path, len + 2);
+    }
+    RootStream<true> rs;
+    rs.init(seed, nullptr);
+    const uint32_t dec0 = p.state ? (uint32_t)p.state[r] : 0u;
+    uint32_t dec = dec0;
+    int32_t* out = p.touched + (size_t)r * p.stride;
+    int32_t* lc = p.level_counts + (size_t)r * (p.depth + 1);
+    if (gl == 0) {
+        out[0] = root;
+        lc[0] = 1;
+    }
+    __syncwarp(gmask);
+    int T = 1, lvl_begin = 0, lvl_end = 1;
+    bool bad = false;
+    for (int level = 0; level < p.depth && !bad; ++level) {
+        const int next_begin = T;
+        // rows of the level's next chunk are loaded one chunk ahead
+        auto load_row = [&](int i, int32_t& v, int32_t& b, int32_t& deg) {
+            v = 0; b = 0; deg = 0;
+            if (i < lvl_end) {
+                v = out[i];
+                b = __ldg(p.w_rp + v);
+                deg = __ldg(p.w_rp + v + 1) - b;
+            }
+        };
+        int32_t nv_, nb_, nd_;
+        load_row(lvl_begin + gl, nv_, nb_, nd_);
+        for (int i0 = lvl_begin; i0 < lvl_end; i0 += GL) {
+            const int i = i0 + gl;
+            const int32_t v = nv_, b = nb_, deg = nd_;
+            if (i0 + GL < lvl_end) load_row(i0 + GL + gl, nv_, nb_, nd_);
+            if (i < lvl_end && deg > 0 && p.neg_row && p.neg_row[v]) {
+                report(p.ticket, kErrNegative, r, level);
+                bad = true;
+            }
+            if (__any_sync(gmask, bad)) { bad = true; break; }
+            const uint32_t k = deg > 0 ? min((uint32_t)p.fanout, (uint32_t)deg) : 0u;
+            // group-exclusive prefix of (nonempty rows, choices)
+            uint32_t pn = deg > 0 ? 1u : 0u, pk = k;
+#pragma unroll
+            for (int o = 1; o < GL; o <<= 1) {
+                const uint32_t xn = __shfl_up_sync(gmask, pn, o, GL), xk = __shfl_up_sync(gmask, pk, o, GL);
+                if (gl >= o) { pn += xn; pk += xk; }
+            }
+            const uint32_t tn = __shfl_sync(gmask, pn, GL - 1, GL), tk = __shfl_sync(gmask, pk, GL - 1, GL);
+            if (k > 0) {
+                rs.begin_decision(dec + pn - 1);
+                uint32_t pos[KCAP];
+                choose_small<KCAP, true>(rs, (uint32_t)deg, k, recip, pos);
+                int32_t c[KCAP];
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q) c[q] = q < (int)k ? __ldg(p.w_ci + b + pos[q]) : 0;
+                int32_t* dst = out + T + (pk - k);
+#pragma unroll
+                for (int q = 0; q < KCAP; ++q)
+                    if (q < (int)k) dst[q] = c[q];
+            }
+            T += (int)tk;
+            dec += tn;
+        }
+        __syncwarp(gmask);  // this level's children are visible to the whole group
+        if (gl == 0 && !bad) lc[level + 1] = T - next_begin;
+        lvl_begin = next_begin;
+        lvl_end = T;
+    }
+    uint32_t dr = rs.draws;
+#pragma unroll
+    for (int o = GL / 2; o > 0; o >>= 1) dr += __shfl_down_sync(gmask, dr, o, GL);
+    if (gl == 0) {
+        p.tcount[r] = T;
+        p.draws[r] = dr;
+        p.decisions[r] = dec - dec0;
+    }
+}
+
 // sample_rows (sampler.cpp:64-86): one lane per choice stream, deciding that
 // stream's nonempty rows in row order (begin_root(row_streams[r]) then
 // choose(|support|, min(s, |support|)), positions -> the row's columns).
@@ -387,8 +511,29 @@ static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cu
     HGS_CUDA(cudaGetLastError());
 }
 
+template <int KCAP>
+static void launch_expand_group(const ExpandParams& ep, cudaStream_t st) {
+    const size_t smem = (size_t)ep.recip_smem * sizeof(uint64_t);
+    auto kern = k_expand_group<KCAP>;
+    if (smem > 48 * 1024)
+        HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
+    const int64_t threads = (int64_t)(ep.R - ep.r0) * kGroupLanes;
+    kern<<<(unsigned)((threads + 127) / 128), 128, smem, st>>>(ep);
+    HGS_CUDA(cudaGetLastError());
+}
+
+#ifndef HGS_K1_GROUP
+#define HGS_K1_GROUP 1
+#endif
+
 void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
                    cudaStream_t st) {
+    if (HGS_K1_GROUP && philox && kmax <= 8 && ep.R > ep.r0) {  // decision-parallel Philox path
+        if (kmax > 6) launch_expand_group<8>(ep, st);
+        else if (kmax > 4) launch_expand_group<6>(ep, st);
+        else launch_expand_group<4>(ep, st);
+        return;
+    }
     // register fast path for k <= 8, sized to the call's largest choice
     if (kmax > 8) {
         if (philox) launch_expand_t<8, true, true>(threads, smem, ep, st);
