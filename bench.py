@@ -43,6 +43,7 @@ sys.path.insert(0, ROOT)
 METRIC = "sampled minibatches/sec (and edges/sec) at 1/2/4/8 B200; % of HBM roofline"
 UNIT = "minibatches/s"
 K_BATCHES, BATCH, DEPTH, FANOUT = 64, 1024, 3, 6
+RNG = 0  # 0: per-root xoshiro streams (the reference's PerRootChoiceSource), 1: Philox
 WORKLOAD = "C2"
 
 
@@ -84,11 +85,14 @@ def set_workload(name, world):
         K_BATCHES, BATCH, DEPTH, FANOUT = W.SHAPE["C2"]
 
 
+RNG_TEXT = {0: "per-root xoshiro streams", 1: "per-root Philox streams"}
+
+
 def config_dict(n_gpus, ev):
     return {"workload": "%s, n=%d hits / m=%d edges, %d minibatches"
-            " x %d seeds per GPU, %d-hop, fanout %d, symmetrized walk, per-root xoshiro streams,"
+            " x %d seeds per GPU, %d-hop, fanout %d, symmetrized walk, %s,"
             " bulk_shadow+gather_features" % (WORKLOAD_TEXT[WORKLOAD], ev.n, ev.m, K_BATCHES, BATCH, DEPTH,
-                                               FANOUT),
+                                               FANOUT, RNG_TEXT[RNG]),
             "minibatches_per_step_per_gpu": K_BATCHES, "roots_per_minibatch": BATCH,
             "depth": DEPTH, "fanout": FANOUT, "parallelism": f"shard{n_gpus} (replicated graph)",
             "l2": "flushed (512 MiB memset) before every timed step"}
@@ -161,10 +165,10 @@ def cpu_sample_time(ev, n_batches, threads, rep0=1000):
     g = O.Graph(n=ev.n, rp=ev.rp, ci=ev.ci, node_feat=ev.node_feat, edge_feat=ev.edge_feat,
                 labels=ev.labels)
     if O.ref_available():
-        t, V, E = O.ref_time_sample(g, roots, boff, seeds, depth=DEPTH, fanout=FANOUT,
+        t, V, E = O.ref_time_sample(g, roots, boff, seeds, rng=RNG, depth=DEPTH, fanout=FANOUT,
                                     threads=threads)
         return t, V, E, "reference"
-    t, V, E = O.port_time_sample(g, roots, boff, seeds, depth=DEPTH, fanout=FANOUT,
+    t, V, E = O.port_time_sample(g, roots, boff, seeds, rng=RNG, depth=DEPTH, fanout=FANOUT,
                                  threads=threads)
     return t, V, E, "port"
 
@@ -230,7 +234,7 @@ def run_gpu(args, world, rank, local_rank):
                                                                     ev.labels)
     stream = torch.cuda.Stream(dev)  # a real (non-default) stream shared with the C ABI
     S = hgs.Sampler(G, stream=stream.cuda_stream)
-    cfg = dict(depth=DEPTH, fanout=FANOUT, symmetrize=True, rng=hgs.RNG_XOSHIRO, gather=True,
+    cfg = dict(depth=DEPTH, fanout=FANOUT, symmetrize=True, rng=RNG, gather=True,
                batch_size=BATCH, bulk_batches=K_BATCHES)
     nsteps = args.warmup + args.steps
     host_in, dev_in = [], []
@@ -474,6 +478,8 @@ def main():
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--events", type=int, default=100, help="C5: events in the epoch (split over ranks)")
+    ap.add_argument("--rng", default="xoshiro", choices=["xoshiro", "philox"],
+                    help="choice streams: per-root xoshiro (reference default) or counter-based Philox")
     ap.add_argument("--bulk-batches", type=int, default=0,
                     help="C5: minibatches per sampling call (0 = all batches of an event in one call)")
     ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"],
@@ -491,6 +497,8 @@ def main():
     if os.environ.get("HGS_FORCE_DEVICE") is not None:
         local_rank = int(os.environ["HGS_FORCE_DEVICE"])
     set_workload(args.workload, world)
+    global RNG
+    RNG = 1 if args.rng == "philox" else 0
     if args.e2e_steps is None:
         args.e2e_steps = args.warmup + args.steps if args.workload in ("C1", "C2") else 3
     if args.impl == "reference":
