@@ -276,6 +276,7 @@ __global__ void k_recip(uint64_t* r, int32_t n) {
 }  // namespace
 
 void graph_build_walk_sym(DevGraph& g) {
+    std::lock_guard<std::recursive_mutex> lock(g.lazy_mu);
     if (g.sym_built) return;
     const DevCsr& a = g.full_pattern();
     const int32_t n = a.n;
@@ -320,6 +321,7 @@ void graph_build_walk_sym(DevGraph& g) {
 }
 
 void graph_ensure_recip(DevGraph& g, int32_t max_m) {
+    std::lock_guard<std::recursive_mutex> lock(g.lazy_mu);
     const int32_t need = max_m + 1;
     if (need <= g.recip_n) return;
     g.recip.release();

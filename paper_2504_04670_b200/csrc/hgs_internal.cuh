@@ -1,5 +1,6 @@
 // hgs_internal.cuh — device graph store, workspaces and shared device helpers.
 #pragma once
+#include <mutex>
 #include <cuda_runtime.h>
 #include <stdint.h>
 
@@ -121,6 +122,9 @@ struct DevGraph {
     int32_t f_v = 0, f_e = 0;
     bool has_features = false;
     cudaStream_t stream = nullptr;  // ingest stream
+    // guards the lazily built parts (walk_sym, recip): sample handles on
+    // different host threads may share one graph
+    std::recursive_mutex lazy_mu;
 
     const DevCsr& full_pattern() const { return has_full ? a_full : a; }
 };

@@ -524,6 +524,35 @@ def test_sample_rows_wide(rng):
     assert np.array_equal(decs.astype(np.int64), ndec)
 
 
+def test_threads_share_a_fresh_graph():
+    """Sample handles on several host threads, one fresh graph (its walk and
+    reciprocal table are built lazily by whichever call comes first): every
+    thread's results equal the oracle's."""
+    import concurrent.futures as cf
+    H = hgs()
+    g = random_graph(20000, 200000, 31)
+    rs = np.random.default_rng(31)
+    jobs = []
+    for t in range(4):
+        roots = rs.choice(g.n, 300, replace=False).astype(np.int64)
+        jobs.append((roots, np.array([0, 100, 300], np.int64), rs.integers(0, 2**63, 300, dtype=np.uint64), t % 2))
+    G = H.Graph(g.rp, g.ci)
+
+    def run(job):
+        roots, boff, seeds, rng = job
+        S = H.Sampler(G)
+        S.bulk_shadow(roots, boff, seeds, rng=rng, depth=3, fanout=6)
+        out = S.to_host()
+        S.close()
+        return out
+
+    with cf.ThreadPoolExecutor(4) as ex:
+        outs = list(ex.map(run, jobs))
+    for (roots, boff, seeds, rng), dev in zip(jobs, outs):
+        assert_same(dev, O.bulk_shadow(g, roots, boff, seeds, rng=rng, depth=3, fanout=6), False)
+    G.close()
+
+
 def test_multi_handle_sharding_matches_single_call():
     """Two sample handles on one graph (as two ranks would be): the shard union
     equals the single call, batch for batch."""
