@@ -87,16 +87,14 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     c.cache_entries = tree_bound(c.kmax, depth - 1);
     c.recip_smem = walk.max_deg + 1 <= 4096 ? walk.max_deg + 1 : 0;
     const size_t rbytes = (size_t)c.recip_smem * sizeof(uint64_t);
-    c.expand_threads = 128;
-    c.expand_smem = (size_t)c.cache_entries * 128 * sizeof(int2) + rbytes;
-    if (c.expand_smem > 96 * 1024) {
-        c.expand_threads = 64;
-        c.expand_smem = (size_t)c.cache_entries * 64 * sizeof(int2) + rbytes;
-        if (c.expand_smem > 96 * 1024) {
-            c.cache_entries = 0;
-            c.expand_smem = rbytes;
-            c.expand_threads = 128;
-        }
+    // 64-lane blocks: K1's time per SM is linear in its lanes, and finer
+    // blocks even out the SMs (C2: 1024 blocks = 6.9 per SM; 128-lane blocks
+    // leave 68 SMs with 4 and 80 with 3: 0.173 vs 0.164 ms)
+    c.expand_threads = 64;
+    c.expand_smem = (size_t)c.cache_entries * c.expand_threads * sizeof(int2) + rbytes;
+    if (c.expand_smem > 96 * 1024) {  // deep / wide trees: rows re-read from the walk CSR
+        c.cache_entries = 0;
+        c.expand_smem = rbytes;
     }
     if (c.max_t > kMaxSet || !plan_extract(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
     (void)a;
