@@ -156,7 +156,10 @@ int hgs_sample_bind(hgs_sample* s, hgs_graph* g);
  * (PerRootChoiceSource / PhiloxChoiceSource seeds, root ordinal = flat index).
  * rng_state (nullable): resumes non-fresh sources — xoshiro: 4 u64 state
  * words per root; philox: 1 u64 per root = decisions already consumed.
- * Blocks until the results are ready. */
+ * Blocks until the results are ready. Limits (HGS_ERANGE): a root whose
+ * induced subgraph has more than 32,767 vertices (the message names the
+ * root ordinal), min(fanout, walk degree) > 2^24, more than 2^31-1 sampled
+ * vertices or edges in one call. */
 int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
                    const int64_t* batch_off, int64_t n_batches, const uint64_t* seeds,
                    const uint64_t* rng_state);
