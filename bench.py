@@ -278,6 +278,8 @@ def run_gpu(args, world, rank, local_rank):
             step_device(i, False)
             ev1[j].record(stream)
             S.wait()
+            if S.reruns():  # a capacity re-run inside wait() would run outside ev0..ev1
+                raise RuntimeError("bench: a timed step needed a capacity re-run; warm-up did not size the buffers")
             step_ms.append(ev0[j].elapsed_time(ev1[j]))
             launches += S.launches()
             stats.append(S.stats())

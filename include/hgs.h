@@ -102,8 +102,8 @@ typedef struct {
     uint32_t* decisions;  /* R   */
 } hgs_host_out;
 
-/* Device pointers of the last call's outputs (valid until the next run or
- * destroy on the same sample handle). */
+/* Device pointers of the last call's outputs (valid after hgs_sample_wait,
+ * until the next run or destroy on the same sample handle). */
 typedef struct {
     const int32_t *batch_voff, *batch_eoff, *comp_off, *l2g, *roots_local;
     const int32_t *e_row, *e_col, *e_gid, *root_voff, *root_eoff;
@@ -199,7 +199,12 @@ int hgs_derive_seeds(const hgs_seed_spec* spec, const int64_t* batch_off, int64_
 int hgs_sample_copy_frontiers(hgs_sample* s, int32_t* touched, int32_t* tcount, int32_t* level_counts,
                               int64_t* stride);
 
-/* Wait for the last run; fills counts[0..3] = R, k, V, E (may be NULL). */
+/* Wait for the last run; fills counts[0..3] = R, k, V, E (may be NULL).
+ * A run whose edge slots or output buffers proved too small is re-run here
+ * with exact sizes (counted by hgs_sample_reruns). For the run_device entry
+ * points this means: the device inputs (roots, batch offsets, seeds) must stay
+ * unchanged until hgs_sample_wait returns, and the outputs (device views) are
+ * valid only after it returns. */
 int hgs_sample_wait(hgs_sample* s, int64_t* counts);
 int hgs_sample_copy_to_host(hgs_sample* s, const hgs_host_out* out);
 int hgs_sample_device_views(hgs_sample* s, hgs_device_views* out);
@@ -213,8 +218,12 @@ int hgs_sample_kernel_times(hgs_sample* s, float* ms6);
  * (levels 0..d-1) [6]=sum of chosen children (levels 1..d) [7]=decisions
  * [8]=draws [9..9+d] = frontier rows per level 0..d. n >= 10 + depth. */
 int hgs_sample_stats(hgs_sample* s, int64_t* stats, int32_t n);
-/* Number of kernels the last run launched (for gpu_launches accounting). */
+/* Number of kernels the last run launched, re-runs included (for
+ * gpu_launches accounting). */
 int hgs_sample_launches(hgs_sample* s, int64_t* n);
+/* Capacity re-runs the last run needed inside hgs_sample_wait (0 once the
+ * handle's buffers fit the workload; timed steps must see 0). */
+int hgs_sample_reruns(hgs_sample* s, int64_t* n);
 
 /* ---- sample_rows ------------------------------------------------------------
  * hitgnn::sample_rows (sampler.hpp:60-66, sampler.cpp:64-86) on the device,

@@ -384,6 +384,11 @@ int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d
                           const uint64_t* d_seeds) {
     return guarded([&] {
         if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        if (n_roots < 0 || n_batches < 0) fail(HGS_EINVAL, "hgs_sample_run_device: negative count");
+        if (n_roots > 0 && n_batches < 1) fail(HGS_EINVAL, "hgs_sample_run_device: roots without batches");
+        if (n_roots >= ((int64_t)1 << 31) - 1) fail(HGS_ERANGE, "hgs_sample_run_device: too many roots");
+        if (n_batches > 0 && !d_batch_off) fail(HGS_EINVAL, "hgs_sample_run_device: null batch offsets");
+        if (n_roots > 0 && (!d_roots || !d_seeds)) fail(HGS_EINVAL, "hgs_sample_run_device: null roots or seeds");
         validate_cfg(cfg);
         DevGraph& g = s->graph->g;
         check_square(g, cfg->symmetrize);
@@ -410,8 +415,12 @@ int hgs_sample_run_device_spec(hgs_sample* s, const hgs_config* cfg, const int32
         if (!spec) fail(HGS_EINVAL, "hgs_sample_run_device_spec: null seed spec");
         if (spec->path_len < 0 || spec->path_len > 6)
             fail(HGS_EINVAL, "hgs_sample_run_device_spec: path_len must be in [0, 6]");
+        if (n_roots < 0 || n_batches < 0) fail(HGS_EINVAL, "hgs_sample_run_device_spec: negative count");
         if (n_roots > 0 && n_batches < 1)
             fail(HGS_EINVAL, "hgs_sample_run_device_spec: roots without batches");
+        if (n_roots >= ((int64_t)1 << 31) - 1) fail(HGS_ERANGE, "hgs_sample_run_device_spec: too many roots");
+        if (n_batches > 0 && !d_batch_off) fail(HGS_EINVAL, "hgs_sample_run_device_spec: null batch offsets");
+        if (n_roots > 0 && !d_roots) fail(HGS_EINVAL, "hgs_sample_run_device_spec: null roots");
         validate_cfg(cfg);
         DevGraph& g = s->graph->g;
         check_square(g, cfg->symmetrize);
@@ -612,6 +621,9 @@ int hgs_sample_copy_to_host(hgs_sample* s, const hgs_host_out* o) {
 int hgs_sample_device_views(hgs_sample* s, hgs_device_views* v) {
     return guarded([&] {
         if (!s || !v) fail(HGS_EINVAL, "hgs: null argument");
+        // a pending run may still be re-run with larger buffers inside
+        // hgs_sample_wait (capacity overflow), which can move every output
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_device_views: run not waited for");
         v->batch_voff = s->batch_voff.p; v->batch_eoff = s->batch_eoff.p; v->comp_off = s->comp_off.p;
         v->l2g = s->l2g.p; v->roots_local = s->roots_local.p; v->e_row = s->e_row.p;
         v->e_col = s->e_col.p; v->e_gid = s->e_gid.p; v->root_voff = s->root_voff.p;
@@ -647,6 +659,14 @@ int hgs_sample_launches(hgs_sample* s, int64_t* n) {
     return guarded([&] {
         if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
         *n = s->launches;
+    });
+}
+
+int hgs_sample_reruns(hgs_sample* s, int64_t* n) {
+    return guarded([&] {
+        if (!s || !n) fail(HGS_EINVAL, "hgs: null argument");
+        if (s->pending) fail(HGS_EINVAL, "hgs_sample_reruns: run not waited for");
+        *n = s->reruns;
     });
 }
 

@@ -674,7 +674,8 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
 // and their shared sectors), and edge features + label come as one 32-byte
 // record per edge (DevGraph::erec) instead of two requests.
 __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__ node_feat, int32_t f_v,
-                                                      uint32_t fv_magic, const int32_t* __restrict__ l2g,
+                                                      uint32_t fv_magic, uint32_t fv_err,
+                                                      const int32_t* __restrict__ l2g,
                                                       const int32_t* __restrict__ vb, const int32_t* __restrict__ ve,
                                                       int64_t v_cap, const int32_t* __restrict__ ticket,
                                                       double* __restrict__ xv) {
@@ -691,7 +692,10 @@ __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__
     if ((f_v & 1) == 0) {  // rows as f_v/2 16-byte pieces
         const int q2 = f_v >> 1;
         const int64_t n2 = V * q2;
-        const bool magic = n2 < ((int64_t)1 << 32);
+        // i = floor(e * m / 2^32) with m = ceil(2^32 / q2) is exact while
+        // e * (q2 * m - 2^32) < 2^32 (fv_err = q2 * m - 2^32); q2 == 1 needs no
+        // division at all (m would be 2^32)
+        const bool magic = q2 > 1 && n2 < ((int64_t)1 << 32) && (uint64_t)n2 * fv_err < ((uint64_t)1 << 32);
         const uint4* src = reinterpret_cast<const uint4*>(node_feat);
         uint4* dst = reinterpret_cast<uint4*>(xv);
         for (int64_t e0 = V0 * q2 + (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e0 < n2; e0 += stride * U) {
@@ -700,7 +704,7 @@ __global__ void __launch_bounds__(256) k_gather_nodes(const double* __restrict__
             for (int u = 0; u < U; ++u) {
                 const int64_t e = e0 + stride * u;
                 if (e < n2) {
-                    const int64_t i = magic ? (int64_t)__umulhi((unsigned)e, fv_magic) : e / q2;
+                    const int64_t i = q2 == 1 ? e : magic ? (int64_t)__umulhi((unsigned)e, fv_magic) : e / q2;
                     x[u] = __ldg(src + (int64_t)__ldg(l2g + i) * q2 + (e - i * q2));
                 }
             }
@@ -884,7 +888,7 @@ void launch_gather_packed(int blocks, const PackParams& pp, const uint4* erec, c
                           const int32_t* ve, const int32_t* eb, const int32_t* ee, cudaStream_t st) {
     const dim3 grid(blocks), block(256);
     if (pp.f_v > 0)
-        k_gather_nodes<<<grid, block, 0, st>>>(pp.node_feat, pp.f_v, pp.fv_magic, pp.l2g, vb, ve, pp.v_cap,
+        k_gather_nodes<<<grid, block, 0, st>>>(pp.node_feat, pp.f_v, pp.fv_magic, pp.fv_err, pp.l2g, vb, ve, pp.v_cap,
                                                pp.ticket, pp.xv);
     if (erec)
         k_gather_edges_rec<<<grid, block, 0, st>>>(erec, pp.e_gid, eb, ee, pp.e_cap, pp.ticket,

@@ -287,14 +287,15 @@ struct hgs_sample {
     bool pending = false;
     bool profiled = false;
     cudaEvent_t ev[6] = {};
-    int64_t launches = 0;
+    int64_t launches = 0;     // kernels launched by the last run, re-runs included
+    int64_t reruns = 0;       // capacity re-runs of the last run (0 in a steady state)
     // chunked pipeline: packing runs on a higher-priority side stream
     cudaStream_t aux = nullptr;
     std::vector<cudaEvent_t> chunk_ev;
 };
 
 namespace hgs {
-void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in);
+void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, bool rerun = false);
 void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in);
 void sample_stats(hgs_sample* s, int64_t* out, int n);
 void gather_rows(DevGraph& g, const int64_t* d_l2g, int64_t V, const int64_t* d_eid, int64_t E,

@@ -116,7 +116,8 @@ struct PackParams {
     const double* __restrict__ edge_feat;
     const uint8_t* __restrict__ labels;
     int32_t f_v, f_e, gather;
-    uint32_t fv_magic;  // ceil(2^32 / (f_v/2)) for even f_v
+    uint32_t fv_magic;  // ceil(2^32 / (f_v/2)) for even f_v (0 when f_v/2 == 1)
+    uint32_t fv_err;    // (f_v/2) * fv_magic - 2^32: the magic quotient is exact for e * fv_err < 2^32
     int64_t v_cap, e_cap;
     int32_t set_cap;  // per-warp staging of the root's set (>= max set size)
     int32_t* __restrict__ ticket;

@@ -109,7 +109,7 @@ int sm_count(int device) {
 
 }  // namespace
 
-void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) {
+void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, bool rerun) {
     DevGraph& g = s->graph->g;
     HGS_CUDA(cudaSetDevice(g.device));
     if (cfg.symmetrize) graph_build_walk_sym(g);
@@ -124,7 +124,10 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
 
     s->R = R; s->k = k; s->depth = cfg.depth; s->fanout = cfg.fanout;
     s->gathered = cfg.gather; s->symmetrize = cfg.symmetrize; s->rng = cfg.rng;
-    s->launches = 0;
+    if (!rerun) {
+        s->launches = 0;
+        s->reruns = 0;
+    }
     s->touched_stride = c.max_t;
     const size_t R1 = (size_t)R + 1;
     s->touched.reserve((size_t)std::max<int64_t>(R, 1) * c.max_t);
@@ -204,7 +207,11 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) 
     pp.node_feat = g.node_feat.p; pp.edge_feat = g.edge_feat.p; pp.labels = g.labels.p;
     pp.f_v = g.f_v; pp.f_e = g.f_e; pp.gather = cfg.gather;
     const uint32_t q2 = (uint32_t)std::max(1, g.f_v / 2);
-    pp.fv_magic = (uint32_t)((((uint64_t)1 << 32) + q2 - 1) / q2);
+    {
+        const uint64_t m = ((((uint64_t)1 << 32) + q2 - 1) / q2);  // 2^32 for q2 == 1: unused then
+        pp.fv_magic = q2 > 1 ? (uint32_t)m : 0u;
+        pp.fv_err = q2 > 1 ? (uint32_t)(q2 * m - ((uint64_t)1 << 32)) : 0u;
+    }
     pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
     pp.set_cap = c.set_cap;
 
@@ -389,7 +396,8 @@ void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) {
             s->v_cap = (size_t)s->V;
             s->l2g.release(); s->xv.release();
         }
-        sample_enqueue(s, cfg, in);
+        ++s->reruns;
+        sample_enqueue(s, cfg, in, true);
         sample_finish(s, cfg, in);
     }
 }

@@ -33,7 +33,7 @@ EXPORTS = [
     "hgs_sample_wait", "hgs_sample_copy_to_host", "hgs_sample_device_views",
     "hgs_sample_kernel_times", "hgs_sample_stats", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
     "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind", "hgs_sample_copy_frontiers",
-    "hgs_sample_rows",
+    "hgs_sample_rows", "hgs_sample_reruns",
 ]
 
 
@@ -157,6 +157,7 @@ def lib() -> C.CDLL:
         L.hgs_sample_device_views.argtypes = [vp, C.POINTER(DeviceViews)]
         L.hgs_sample_kernel_times.argtypes = [vp, vp]
         L.hgs_sample_launches.argtypes = [vp, vp]
+        L.hgs_sample_reruns.argtypes = [vp, vp]
         L.hgs_sample_stats.argtypes = [vp, vp, i32]
         _lib_cache = L
     return _lib_cache
@@ -245,6 +246,12 @@ class Graph:
         ci = np.zeros(max(nnz, 1), np.int64)
         _check(lib().hgs_graph_walk(self._h, int(symmetrize), _p(rp), _p(ci)))
         return rp, ci[:int(rp[-1])]
+
+    def reruns(self) -> int:
+        """Capacity re-runs the last run needed (0 once buffers fit)."""
+        n = np.zeros(1, np.int64)
+        _check(lib().hgs_sample_reruns(self._h, _p(n)))
+        return int(n[0])
 
     def close(self):
         if self._h:
