@@ -331,8 +331,8 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         __syncwarp();
 
         // ---- induced subgraph: scan the flattened rows in 32-entry windows
-        int2* const ed = p.escratch + (size_t)r * p.e_stride;
-        int2* const ed_end = ed + p.e_stride;
+        int2* const ed = p.escratch + (p.e_off ? (size_t)p.e_off[r] : (size_t)r * p.e_stride);
+        int2* const ed_end = p.e_off ? p.escratch + p.e_off[r + 1] : ed + p.e_stride;
         int2* edc = ed;  // next free edge slot
         // Emit the hits of one window in scan order. CHK is set when the
         // slot might overflow: stores are then bounds-checked, overflow is
@@ -417,7 +417,7 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             p.root_ne[r] = count;
             p.root_rloc[r] = T > 0 ? hs.find_rank((uint32_t)root) : -1;
             p.root_scan[r] = S;
-            if (count > p.e_stride) {
+            if (count > (int)(ed_end - ed)) {
                 atomicMax(&p.ticket[4], count);
                 report(p.ticket, kErrCapacity, r, count);
             }
@@ -618,7 +618,8 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
         const int64_t vb = p.root_voff[r], eb = p.root_eoff[r];
         const int Vr = p.root_voff[r + 1] - (int32_t)vb;
         const int Er = p.root_eoff[r + 1] - (int32_t)eb;
-        if (Er > p.e_stride) continue;  // slot overflowed in K2 (reported there): the call is re-run
+        const int ecap = p.e_off ? p.e_off[r + 1] - p.e_off[r] : p.e_stride;
+        if (Er > ecap) continue;  // slot overflowed in K2 (reported there): the call is re-run
         if (vb + Vr > p.v_cap || eb + Er > p.e_cap) {
             if (lane == 0) report(p.ticket, kErrCapacity, r, -1);
             continue;
@@ -645,7 +646,7 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
             }
         }
         // COO edges (block_diag rebasing) and edge ids
-        const int2* ed = p.escratch + (size_t)r * p.e_stride;
+        const int2* ed = p.escratch + (p.e_off ? (size_t)p.e_off[r] : (size_t)r * p.e_stride);
         for (int t0 = 0; t0 < Er; t0 += 32 * U) {
             int2 e[U];
 #pragma unroll
@@ -853,17 +854,43 @@ void launch_extract(int grid, int warps, size_t smem, const ExtractParams& xp, b
     }
     auto kern = packed ? (xp.a_gid ? k_extract<true, true, false> : k_extract<true, false, false>)
                        : (xp.a_gid ? k_extract<false, true, false> : k_extract<false, false, false>);
-    HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    kern<<<grid, 32 * warps, smem, st>>>(xp);
+    kern<<<grid, 32 * warps, smem, st>>>(xp);  // shared-memory opt-in: extract_blocks_per_sm
     HGS_CUDA(cudaGetLastError());
 }
 
+int prepare_kernel(const void* const* kerns, int n, size_t smem, int warps) {
+    struct Entry {
+        int dev;
+        const void* k0;
+        size_t smem;
+        int warps, per_sm;
+    };
+    static std::mutex mu;
+    static std::vector<Entry> cache;
+    int dev = 0;
+    HGS_CUDA(cudaGetDevice(&dev));
+    std::lock_guard<std::mutex> lk(mu);
+    for (const Entry& e : cache)
+        if (e.dev == dev && e.k0 == kerns[0] && e.smem == smem && e.warps == warps) return e.per_sm;
+    int best = 1 << 30;
+    int optin = 0;
+    HGS_CUDA(cudaDeviceGetAttribute(&optin, cudaDevAttrMaxSharedMemoryPerBlockOptin, dev));
+    for (int i = 0; i < n; ++i) {
+        // the attribute is one value per kernel: opt in to the device maximum
+        // (a per-size value would break a later, larger launch served from the cache)
+        HGS_CUDA(cudaFuncSetAttribute(kerns[i], cudaFuncAttributeMaxDynamicSharedMemorySize, optin));
+        int per_sm = 0;
+        HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kerns[i], 32 * warps, smem));
+        best = std::min(best, std::max(per_sm, 1));
+    }
+    cache.push_back({dev, kerns[0], smem, warps, best});
+    return best;
+}
+
 int extract_blocks_per_sm(size_t smem, int warps, bool packed) {
-    auto kern = packed ? k_extract<true, false, false> : k_extract<false, false, false>;
-    HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    int per_sm = 0;
-    HGS_CUDA(cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, kern, 32 * warps, smem));
-    return per_sm > 0 ? per_sm : 1;
+    const void* kp[4] = {(const void*)k_extract<true, false, false>, (const void*)k_extract<true, true, false>,
+                         (const void*)k_extract<false, false, false>, (const void*)k_extract<false, true, false>};
+    return prepare_kernel(packed ? kp : kp + 2, 2, smem, warps);
 }
 
 __global__ void k_max_i32(const int32_t* __restrict__ x, int32_t n, int32_t* __restrict__ out) {

@@ -269,6 +269,8 @@ struct hgs_sample {
     hgs::DevBuf<uint32_t> kbig;       // K1 choose() scratch for choices > kLocalK (wide rows only)
     hgs::DevBuf<unsigned char> k2g;  // K2 working sets in global memory (oversized sets only)
     int32_t e_stride = 512;
+    hgs::DevBuf<int32_t> eoff_exact;  // exact per-root edge-slot offsets for an overflow re-run
+    bool exact_slots = false;
     hgs::DevBuf<int64_t> scan_tmp;
     hgs::DevBuf<unsigned long long> stats_tmp;
     hgs::DevBuf<int32_t> ticket;  // [1]=error code [2..3]=error detail [4]=max E_r seen

@@ -90,6 +90,8 @@ struct ExtractParams {
     int32_t cnt_lg;                     // log2 of the bucket-counter capacity (<= 2*row_cap)
     int32_t* __restrict__ work;         // root counter (zeroed before each launch)
     unsigned char* gscratch;            // nullable: per-warp working sets in global memory
+    int32_t lnb;                        // k_extract_dir: log2 of the rank-directory buckets
+    const int32_t* __restrict__ e_off;  // nullable: exact edge-slot offsets [R+1] (re-run after overflow)
 };
 
 // K3: packing + gather.
@@ -101,6 +103,7 @@ struct PackParams {
     const int32_t* __restrict__ root_rloc;
     const int2* __restrict__ escratch;
     int32_t e_stride;
+    const int32_t* __restrict__ e_off;  // nullable: exact edge-slot offsets (see ExtractParams)
     const int64_t* __restrict__ batch_off;
     int32_t k, r0, R;                   // roots [r0, R)
     int32_t* __restrict__ l2g;
@@ -125,6 +128,13 @@ struct PackParams {
 
 void launch_extract(int grid, int warps, size_t smem, const ExtractParams& xp, bool packed, cudaStream_t st);
 int extract_blocks_per_sm(size_t smem, int warps, bool packed);
+// K2, directory variant (extract_dir.cu): the default path
+void launch_extract_dir(int grid, int warps, size_t smem, const ExtractParams& xp, cudaStream_t st);
+int extract_dir_prepare(size_t smem, int warps);
+// Shared-memory opt-in + occupancy (CTAs per SM, min over the kernels) of
+// kernels launched with `smem` dynamic bytes and 32*warps threads, cached per
+// (device, kernels, smem, warps): no driver calls on the per-call path.
+int prepare_kernel(const void* const* kerns, int n, size_t smem, int warps);
 // *out = max(x[0..n)) (>= 0), on the device
 void launch_max_i32(const int32_t* x, int32_t n, int32_t* out, cudaStream_t st);
 // Exclusive scan of (V_r, E_r) over roots [r0, r1) into voff/eoff[r0..r1];

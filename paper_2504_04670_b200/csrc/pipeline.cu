@@ -35,7 +35,53 @@ struct CallPlan {
     int32_t n_buckets, set_cap, row_cap, win_cap, warp_bytes, rank_bits, packed;
     int32_t k2_warps;  // warps per K2 CTA (0: not planned yet)
     bool k2_gmem;      // K2 working sets in global scratch (sets beyond shared memory)
+    bool k2_dir;       // K2 = k_extract_dir (rank directory); else the hash-set k_extract
+    int32_t lnb;       // k_extract_dir: log2 of the directory buckets
 };
+
+int ceil_log2(int64_t x) {
+    int l = 0;
+    while (((int64_t)1 << l) < x) ++l;
+    return l;
+}
+
+// k_extract_dir per-warp shared memory for touched lists of up to `bound`
+// entries (duplicates included): directory of NB = 2^lnb buckets (~8 per
+// key, at least the sort's 2*set_cap counters, and fine enough that the low
+// bits of a key within its bucket fit 15 bits: n <= NB << 15), keys, bucketed
+// keys / row starts, sorted keys / row info, and one pass of window info.
+// False when the fast path does not apply (very large sets or id ranges):
+// the hash-set kernel then serves the call.
+// Opt-in (HGS_K2_DIR=1): measured on B200 at C2 it is no faster than the
+// hash-set kernel (0.774 vs 0.752 ms at 24 warps per SM; K2 is bound by its
+// per-warp latency chain and occupancy, not by the probe), see DESIGN.md.
+bool plan_extract_dir(CallPlan& c, int64_t bound, int64_t n) {
+    if (!getenv("HGS_K2_DIR")) return false;
+    if (bound > 2048) return false;
+    c.set_cap = (int32_t)std::max<int64_t>(16, (bound + 3) / 4 * 4);
+    c.row_cap = c.set_cap;
+    c.win_cap = std::max(16, c.set_cap / 2);  // windows per pass (larger rows: several passes)
+    const int cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
+    int lnb = std::max(cnt_lg, ceil_log2(6 * (int64_t)c.set_cap));
+#ifdef HGS_K2D_LNB
+    lnb = std::max(cnt_lg, HGS_K2D_LNB);
+#endif
+    if (const char* e = getenv("HGS_K2D_LNB")) lnb = std::max(cnt_lg, atoi(e));
+    lnb = std::max(lnb, ceil_log2(std::max<int64_t>(n, 1)) - 15);
+    if (lnb > 14) return false;
+    c.lnb = lnb;
+    const size_t bytes = 4 * ((size_t)1 << lnb) + 4 * (size_t)(c.set_cap + 4) + 4 * (size_t)(c.set_cap + 36) +
+                         8 * (size_t)c.set_cap + 8 * (size_t)c.win_cap;
+    c.warp_bytes = (int32_t)((bytes + 15) / 16 * 16);
+    const size_t max_block = 232448;
+    c.k2_warps = 0;
+    for (int w : {4, 2, 1})
+        if ((size_t)w * c.warp_bytes <= max_block) { c.k2_warps = w; break; }
+    if (c.k2_warps == 0) return false;
+    c.k2_dir = true;
+    c.k2_gmem = false;
+    return true;
+}
 
 // K2 per-warp shared memory for sets of up to `bound` vertices: hash set +
 // keys + row starts + row info. Entries pack (vertex << rank_bits | rank)
@@ -70,7 +116,12 @@ bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
         if (c.k2_warps > 0) break;
     }
     c.k2_gmem = false;
+    c.k2_dir = false;
     return c.k2_warps > 0;
+}
+
+bool plan_k2(CallPlan& c, int64_t bound, int64_t n) {
+    return plan_extract_dir(c, bound, n) || plan_extract(c, bound, n);
 }
 
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
@@ -96,7 +147,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
         c.cache_entries = 0;
         c.expand_smem = rbytes;
     }
-    if (c.max_t > kMaxSet || !plan_extract(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
+    if (c.max_t > kMaxSet || !plan_k2(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
     (void)a;
     return c;
 }
@@ -139,7 +190,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     s->root_ne.reserve(R1);
     s->root_rloc.reserve(R1);
     s->root_scan.reserve(R1);
-    s->escratch.reserve(R1 * s->e_stride);
+    if (!(rerun && s->exact_slots)) s->escratch.reserve(R1 * s->e_stride);
     s->scan_tmp.reserve(scan_tmp_words(R));
     s->ticket.reserve(8);
     s->root_voff.reserve(R1);
@@ -190,17 +241,19 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     xp.touched = s->touched.p; xp.tcount = s->tcount.p; xp.stride = c.max_t;
     xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
     xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
+    xp.e_off = rerun && s->exact_slots ? s->eoff_exact.p : nullptr;
     xp.ticket = s->ticket.p;
     auto set_layout = [&]() {
         xp.n_buckets = c.n_buckets; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;
         xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
         xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
+        xp.lnb = c.lnb;
     };
 
     PackParams pp{};
     pp.touched = s->touched.p; pp.stride = c.max_t; pp.root_voff = s->root_voff.p;
     pp.root_eoff = s->root_eoff.p; pp.root_rloc = s->root_rloc.p; pp.escratch = s->escratch.p;
-    pp.e_stride = s->e_stride; pp.batch_off = in.batch_off; pp.k = (int32_t)k;
+    pp.e_stride = s->e_stride; pp.e_off = xp.e_off; pp.batch_off = in.batch_off; pp.k = (int32_t)k;
     pp.l2g = s->l2g.p; pp.roots_local = s->roots_local.p; pp.comp_off = s->comp_off.p;
     pp.e_row = s->e_row.p; pp.e_col = s->e_col.p; pp.e_gid = s->e_gid.p;
     pp.xv = s->xv.p; pp.ye = s->ye.p; pp.lab = s->lab.p;
@@ -261,7 +314,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         int32_t tmax = 0;
         HGS_CUDA(cudaMemcpyAsync(&tmax, s->ticket.p + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         HGS_CUDA(cudaStreamSynchronize(st));
-        if (!plan_extract(c, std::max<int32_t>(tmax, 1), g.n_rows)) {
+        if (!plan_k2(c, std::max<int32_t>(tmax, 1), g.n_rows)) {
             // beyond one warp's shared memory: K2 keeps its working sets in
             // a global scratch slot per warp (3 hash slots per key)
             plan_extract(c, 1, g.n_rows);  // rank bits / packing for the real bound below
@@ -279,10 +332,12 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
             c.k2_gmem = true;
         }
     }
-    if (c.k2_warps == 0) plan_extract(c, 1, g.n_rows);  // R == 0: nothing to extract
+    if (c.k2_warps == 0) plan_k2(c, 1, g.n_rows);  // R == 0: nothing to extract
     set_layout();
     const size_t xsmem = c.k2_gmem ? 0 : (size_t)c.k2_warps * c.warp_bytes;
-    const int xper_sm = c.k2_gmem ? 2 : extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
+    const int xper_sm = c.k2_gmem ? 2
+                        : c.k2_dir ? extract_dir_prepare(xsmem, c.k2_warps)
+                                   : extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
     xp.gscratch = nullptr;
     if (c.k2_gmem) {
         const size_t slots = (size_t)xper_sm * sm_count(g.device) * c.k2_warps;
@@ -307,7 +362,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
                                   : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + per_cta - 1) / per_cta);
         xp.work = s->ticket.p + 5;
         HGS_CUDA(cudaMemsetAsync(xp.work, 0, sizeof(int32_t), st));
-        launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);
+        if (c.k2_dir) launch_extract_dir((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, st);
+        else launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);
         ++s->launches;
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
         if (!split && launch_scan_small(s->root_nv.p, s->root_ne.p, (int32_t)R, s->root_voff.p, s->root_eoff.p,
@@ -382,11 +438,25 @@ void sample_finish(hgs_sample* s, const hgs_config& cfg, const CallInputs& in) {
         // An edge slot or the output capacity was too small: grow to the
         // observed need and run the call again (inputs are still resident).
         const int32_t need = s->h_state[4];
+        s->exact_slots = false;
         if (need > s->e_stride) {
-            int32_t es = s->e_stride;
+            // Grow the uniform per-root slot while that stays within a few
+            // times the call's own edge count; a few heavy (hub) roots
+            // instead get exact slots for the re-run: offsets = the scan of
+            // the per-root counts the failed run already produced.
+            int64_t es = s->e_stride;
             while (es < need) es *= 2;
-            s->e_stride = es;
-            s->escratch.release();
+            const int64_t uniform = (s->R + 1) * es, budget = std::max<int64_t>(4 * (int64_t)s->E, 1 << 24);
+            if (uniform <= budget && es < (1 << 30)) {
+                s->e_stride = (int32_t)es;
+                s->escratch.release();
+            } else {
+                s->eoff_exact.reserve((size_t)s->R + 1);
+                HGS_CUDA(cudaMemcpyAsync(s->eoff_exact.p, s->root_eoff.p, sizeof(int32_t) * ((size_t)s->R + 1),
+                                         cudaMemcpyDeviceToDevice, s->stream));
+                s->escratch.reserve((size_t)s->E + 1);
+                s->exact_slots = true;
+            }
         }
         if ((size_t)s->E > s->e_cap) {
             s->e_cap = (size_t)s->E + (size_t)s->E / 8 + 1024;

@@ -247,12 +247,6 @@ class Graph:
         _check(lib().hgs_graph_walk(self._h, int(symmetrize), _p(rp), _p(ci)))
         return rp, ci[:int(rp[-1])]
 
-    def reruns(self) -> int:
-        """Capacity re-runs the last run needed (0 once buffers fit)."""
-        n = np.zeros(1, np.int64)
-        _check(lib().hgs_sample_reruns(self._h, _p(n)))
-        return int(n[0])
-
     def close(self):
         if self._h:
             lib().hgs_graph_destroy(self._h)
@@ -368,6 +362,12 @@ class Sampler:
         d = dict(zip(keys, (int(x) for x in a[:9])))
         d["F_levels"] = [int(x) for x in a[9:]]
         return d
+
+    def reruns(self) -> int:
+        """Capacity re-runs the last run needed (0 once buffers fit)."""
+        n = np.zeros(1, np.int64)
+        _check(lib().hgs_sample_reruns(self._h, _p(n)))
+        return int(n[0])
 
     def launches(self) -> int:
         n = np.zeros(1, np.int64)

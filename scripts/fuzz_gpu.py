@@ -45,11 +45,10 @@ def make_graph(rs):
     return g
 
 
-def main():
-    secs = float(sys.argv[1]) if len(sys.argv) > 1 else 300
-    rs = np.random.default_rng(int(sys.argv[2]) if len(sys.argv) > 2 else 12345)
+def run(rs, *, secs=None, max_cases=None, log=print):
+    """Fuzz until `secs` elapse or `max_cases` cases ran; returns (cases, mismatches)."""
     t0, cases, bad = time.time(), 0, 0
-    while time.time() - t0 < secs:
+    while (secs is None or time.time() - t0 < secs) and (max_cases is None or cases < max_cases):
         g = make_graph(rs)
         depth = int(rs.integers(1, 5))
         fanout = int(rs.choice([1, 2, 3, 4, 5, 6, 7, 8, 9, 12, 20, 40, 300]))
@@ -79,10 +78,19 @@ def main():
         cases += 1
         if diff:
             bad += 1
-            print(f"MISMATCH n={g.n} m={len(g.ci)} {kw} sizes={sizes} fields={diff}", flush=True)
+            log(f"MISMATCH n={g.n} m={len(g.ci)} {kw} sizes={sizes} fields={diff}")
         S.close()
         G.close()
-    print(f"fuzz: {cases} cases, {bad} mismatches in {time.time() - t0:.0f}s", flush=True)
+    log(f"fuzz: {cases} cases, {bad} mismatches in {time.time() - t0:.0f}s")
+    return cases, bad
+
+
+def main():
+    secs = float(sys.argv[1]) if len(sys.argv) > 1 else 300
+    seed = int(sys.argv[2]) if len(sys.argv) > 2 else 12345
+    print(f"fuzz_gpu: seed {seed}, {secs:.0f}s, K2 = {'directory' if os.environ.get('HGS_K2_DIR') else 'hash-set'}",
+          flush=True)
+    _, bad = run(np.random.default_rng(seed), secs=secs, log=lambda m: print(m, flush=True))
     sys.exit(1 if bad else 0)
 
 

@@ -6,7 +6,8 @@ available where /root/reference exists). The fixtures then travel with the
 repo, so the oracle restatement and the CUDA path are checked against the
 reference's own results on machines without it.
 
-    python tests/golden/make_golden.py
+    python tests/golden/make_golden.py          # KATs, small cases, C1, frontiers
+    python tests/golden/make_golden.py --c2     # C2 event + sampler digests (~3 min)
 """
 from __future__ import annotations
 
@@ -151,9 +152,38 @@ def write_frontiers():
     print("frontier fixtures written:", len(index))
 
 
+def write_c2():
+    """C2 (BASELINE configs[1]) digests from the reference generator and
+    sampler: the event arrays, and the full bench-protocol call (64 x 1024
+    roots, d=3, s=6, gather) under both choice streams."""
+    g = O.ref_generate_event(n_tracks=13000, noise=10000, false_factor=14.5)
+    c2 = {"graph": {"n": g.n, "m": g.m, "rp": digest(g.rp), "ci": digest(g.ci),
+                    "node_feat": digest(g.node_feat), "edge_feat": digest(g.edge_feat),
+                    "labels": digest(g.labels)}, "runs": []}
+    k, b = 64, 1024
+    rsd = O.derive(1, [0x62656E6368, k, 0])
+    batches = O.epoch_root_batches(g.n, b, rsd, impl="ref")[:k]
+    roots = np.concatenate(batches)
+    boff = np.arange(k + 1, dtype=np.int64) * b
+    seeds = np.array([O.derive(1, [0x7374726D, k, 0, bi, pos]) for bi in range(k) for pos in range(b)],
+                     np.uint64)
+    c2["roots"] = digest(roots)
+    c2["seeds"] = digest(seeds)
+    for rng in (0, 1):
+        s = O.bulk_shadow(g, roots, boff, seeds, rng=rng, depth=3, fanout=6, gather=True, impl="ref")
+        c2["runs"].append({"rng": rng, "depth": 3, "V": s.V, "E": s.E,
+                           "digests": {f: digest(getattr(s, f)) for f in OUT_FIELDS}})
+    with open(os.path.join(HERE, "c2.json"), "w") as f:
+        json.dump(c2, f, indent=1)
+    print("C2 reference digests written:", [(r["rng"], r["V"], r["E"]) for r in c2["runs"]])
+
+
 def main():
     if "--frontiers" in sys.argv:
         write_frontiers()
+        return
+    if "--c2" in sys.argv:
+        write_c2()
         return
     if not O.ref_available():
         raise SystemExit("oracle/_ref not built: run `make -f oracle/Makefile` where /root/reference exists")

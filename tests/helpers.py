@@ -108,3 +108,56 @@ def load_json(name):
 def sha(a) -> str:
     import hashlib
     return hashlib.sha256(np.ascontiguousarray(a).tobytes()).hexdigest()
+
+
+# ---------------------------------------------------------------------------
+# bench-size parity: slices of one device call against chunked oracle calls
+
+def batch_slice(dev: dict, boff, b0: int, b1: int, f_v: int = 0, f_e: int = 0) -> dict:
+    """Outputs of batches [b0, b1) of one device call, in the layout of a call
+    over just those batches (batch-local ids need no rebasing; only the call
+    offsets do). Per-root streams make that call's result identical."""
+    boff = np.asarray(boff, np.int64)
+    bv = np.asarray(dev["batch_voff"]).astype(np.int64)
+    be = np.asarray(dev["batch_eoff"]).astype(np.int64)
+    r0, r1 = int(boff[b0]), int(boff[b1])
+    v0, v1, e0, e1 = int(bv[b0]), int(bv[b1]), int(be[b0]), int(be[b1])
+    out = {"batch_voff": bv[b0:b1 + 1] - v0, "batch_eoff": be[b0:b1 + 1] - e0,
+           "comp_off": np.asarray(dev["comp_off"])[r0 + b0:r1 + b1],
+           "roots_local": np.asarray(dev["roots_local"])[r0:r1],
+           "l2g": np.asarray(dev["l2g"])[v0:v1],
+           "draws": np.asarray(dev["draws"])[r0:r1], "decisions": np.asarray(dev["decisions"])[r0:r1]}
+    for f in ("e_row", "e_col", "e_gid", "lab"):
+        if dev.get(f) is not None:
+            out[f] = np.asarray(dev[f])[e0:e1]
+    if dev.get("xv") is not None and f_v:
+        out["xv"] = np.asarray(dev["xv"])[v0 * f_v:v1 * f_v]
+    if dev.get("ye") is not None and f_e:
+        out["ye"] = np.asarray(dev["ye"])[e0 * f_e:e1 * f_e]
+    return out
+
+
+def check_against_oracle_chunks(dev: dict, g, roots, boff, seeds, chunks, *, gather, f_v=0, f_e=0,
+                                threads=None, **kw) -> list:
+    """Run the oracle on each batch range of `chunks` (host threads in
+    parallel; the C oracle releases the GIL) and compare the matching slice of
+    the device call bit for bit. Returns [(b0, b1, bad_fields)] for mismatches."""
+    import concurrent.futures as cf
+    roots = np.asarray(roots, np.int64)
+    seeds = np.asarray(seeds, np.uint64)
+    boff = np.asarray(boff, np.int64)
+
+    def one(ch):
+        b0, b1 = ch
+        r0, r1 = int(boff[b0]), int(boff[b1])
+        ref = O.bulk_shadow(g, roots[r0:r1], boff[b0:b1 + 1] - r0, seeds[r0:r1], gather=gather, **kw)
+        return b0, b1, compare(batch_slice(dev, boff, b0, b1, f_v, f_e), ref, gather=gather)
+
+    with cf.ThreadPoolExecutor(threads or min(len(chunks), os.cpu_count() or 4)) as ex:
+        res = list(ex.map(one, chunks))
+    return [r for r in res if r[2]]
+
+
+def even_chunks(k: int, parts: int):
+    parts = max(1, min(parts, k))
+    return [(k * i // parts, k * (i + 1) // parts) for i in range(parts) if k * i // parts < k * (i + 1) // parts]

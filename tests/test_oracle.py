@@ -284,3 +284,23 @@ def test_oracle_frontiers_match_reference_observer():
             assert dg(np.array(q, np.int64)) == exp["q_ci"], (c["name"], lvl)
             assert dg(np.array(f_rp, np.int64)) == exp["f_rp"], (c["name"], lvl)
             assert dg(np.array(f_ci, np.int64)) == exp["f_ci"], (c["name"], lvl)
+
+
+def test_c2_generator_and_oracle_match_reference_digests():
+    """C2 pinned to the reference itself (tests/golden/c2.json, generated by
+    oracle/_ref): the workload generator's event and the oracle's full
+    bench-protocol call (xoshiro streams, gather)."""
+    from paper_2504_04670_b200 import workload as W
+    from tests.helpers import load_json, sha
+    gold = load_json("c2.json")
+    ev = W.preset_event("C2")
+    assert sha(ev.rp.astype(np.int64)) == gold["graph"]["rp"] and sha(ev.ci.astype(np.int64)) == gold["graph"]["ci"]
+    assert sha(ev.node_feat) == gold["graph"]["node_feat"] and sha(ev.labels) == gold["graph"]["labels"]
+    roots, boff, seeds = W.bench_roots(ev.n, 1024, 64, seed=1, rep=0)
+    g = O.Graph(n=ev.n, rp=ev.rp, ci=ev.ci, node_feat=ev.node_feat, edge_feat=ev.edge_feat, labels=ev.labels)
+    s = O.bulk_shadow(g, roots, boff, seeds, rng=0, depth=3, fanout=6, gather=True)
+    run = gold["runs"][0]
+    assert (s.V, s.E) == (run["V"], run["E"])
+    for f in ("batch_voff", "batch_eoff", "comp_off", "l2g", "roots_local", "e_row", "e_col", "e_gid", "xv", "ye",
+              "lab"):
+        assert sha(getattr(s, f)) == run["digests"][f], f
