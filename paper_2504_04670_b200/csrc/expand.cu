@@ -19,6 +19,8 @@
 // dependent row_ptr loads.
 #include <cuda_runtime.h>
 
+#include <cstdlib>
+
 #include "kernels.cuh"
 
 namespace hgs {
@@ -68,6 +70,22 @@ struct RootStream<true> {
     }
 };
 
+// Draws of one decision taken from a buffer the group's lane 0 filled from
+// the root's xoshiro stream, in order: without rejections (Rng::bounded,
+// rng.cpp:43-50, rejects x < 2^64 mod m, probability < m / 2^64) the draw of
+// child t of a root is stream draw t - 1, so a decision's draws start at its
+// children's offset. A rejection flags the root for the exact serial path.
+struct BufStream {
+    const uint64_t* b;
+    bool rejected = false;
+    __device__ __forceinline__ void begin_decision(uint32_t) {}
+    __device__ __forceinline__ uint32_t draw(uint32_t i, uint64_t m, uint64_t rc) {
+        const uint64_t x = b[i];
+        rejected |= hgs::rejected(x, m, rc);
+        return mod_small(x, (uint32_t)m, rc);
+    }
+};
+
 // choose(n, k) of RandomChoiceSource (rng.cpp:105-119) for k <= KCAP without
 // materialising the array: step i swaps slots i and j_i = i + bounded(n - i)
 // (j_i >= i), so slot i ends holding the value that sat at j_i just before
@@ -75,8 +93,8 @@ struct RootStream<true> {
 // or j_i itself — and later steps never touch slot i again. The pre-step
 // value of slot i is likewise the pre-step value of the latest a with
 // j_a == i, or i. O(k^2) register compares, then a 19-comparator network.
-template <int KCAP, bool PHILOX>
-__device__ __forceinline__ void choose_small(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
+template <int KCAP, class Stream>
+__device__ __forceinline__ void choose_small(Stream& rs, uint32_t n, uint32_t k,
                                              const uint64_t* recip, uint32_t (&out)[KCAP]) {
     static_assert(KCAP == 4 || KCAP == 6 || KCAP == 8, "sorting networks exist for 4, 6, 8 keys");
     uint32_t jj[KCAP], pre[KCAP];
@@ -148,42 +166,35 @@ __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
     }
 }
 
-template <int KCAP, bool PHILOX, bool LOCAL>
-__global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
-    extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree), then the recip table
-    const int r = p.r0 + blockIdx.x * blockDim.x + threadIdx.x;
-    // bounded() reciprocals in shared memory when the table is small
-    uint64_t* srecip = reinterpret_cast<uint64_t*>(cache + (size_t)p.cache_entries * blockDim.x);
-    const uint64_t* recip = p.recip;
-    if (p.recip_smem > 0) {
-        for (int i = threadIdx.x; i < p.recip_smem; i += blockDim.x) srecip[i] = p.recip[i];
-        __syncthreads();
-        recip = srecip;
+// Root seed: the uploaded seed, or Rng::derive(seed, {path..., batch_base +
+// bi, pos}) (rng.cpp:76-85) from the call's seed spec.
+__device__ __forceinline__ uint64_t root_seed(const ExpandParams& p, int r) {
+    if (p.seeds) return p.seeds[r];
+    int lo = 0, hi = p.k - 1;  // batch of r: largest bi with batch_off[bi] <= r
+    while (lo < hi) {
+        const int mid = (lo + hi + 1) >> 1;
+        if (__ldg(p.batch_off + mid) <= r) lo = mid; else hi = mid - 1;
     }
-    if (r >= p.R) return;
-    const int bd = blockDim.x, ti = threadIdx.x;
+    uint64_t path[8];
+    for (int i = 0; i < 6; ++i) path[i] = p.spec.path[i];
+    const int len = p.spec.path_len;
+    path[len] = (uint64_t)(p.spec.batch_base + lo);
+    path[len + 1] = (uint64_t)(r - __ldg(p.batch_off + lo));
+    return derive_seed(p.spec.seed, path, len + 2);
+}
 
+// One root, one lane, in the reference's decision order. `cache` (nullable:
+// rows are then re-read from the walk CSR) holds (row start, degree) of the
+// rows still to expand, entry i of this lane at cache[i * bd + ti].
+template <int KCAP, bool PHILOX, bool LOCAL>
+__device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, int ti, const uint64_t* recip) {
     const int32_t root = p.roots32 ? p.roots32[r] : (int32_t)p.roots64[r];
     if (root < 0 || root >= p.n) {
         report(p.ticket, kErrRootRange, r, root);
         p.tcount[r] = 0;
         return;
     }
-    uint64_t seed;
-    if (p.seeds) seed = p.seeds[r];
-    else {  // Rng::derive(seed, {path..., batch_base + bi, pos}) (rng.cpp:76-85)
-        int lo = 0, hi = p.k - 1;  // batch of r: largest bi with batch_off[bi] <= r
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (__ldg(p.batch_off + mid) <= r) lo = mid; else hi = mid - 1;
-        }
-        uint64_t path[8];
-        for (int i = 0; i < 6; ++i) path[i] = p.spec.path[i];
-        const int len = p.spec.path_len;
-        path[len] = (uint64_t)(p.spec.batch_base + lo);
-        path[len + 1] = (uint64_t)(r - __ldg(p.batch_off + lo));
-        seed = derive_seed(p.spec.seed, path, len + 2);
-    }
+    const uint64_t seed = root_seed(p, r);
     RootStream<PHILOX> rs;
     rs.init(seed, (!PHILOX && p.state) ? p.state + 4 * (size_t)r : nullptr);
     uint32_t ndec = (PHILOX && p.state) ? (uint32_t)p.state[r] : 0u;
@@ -193,7 +204,7 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
     int32_t* lc = p.level_counts + (size_t)r * (p.depth + 1);
     out[0] = root;
     lc[0] = 1;
-    const bool cached = p.cache_entries > 0;
+    const bool cached = cache != nullptr;
     {
         const int32_t b = p.w_rp[root];
         if (cached) cache[ti] = make_int2(b, p.w_rp[root + 1] - b);
@@ -226,7 +237,7 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
         const uint32_t k = min((uint32_t)p.fanout, deg);
         rs.begin_decision(ndec);
         ++ndec;
-        choose_small<KCAP, PHILOX>(rs, deg, k, recip, pos);
+        choose_small<KCAP>(rs, deg, k, recip, pos);
         return k;
     };
     for (int level = 0; level < p.depth; ++level) {
@@ -331,31 +342,64 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
     p.decisions[r] = ndec - dec0;
 }
 
-// Philox mode, decision-parallel: decisions are numbered per root
-// (PhiloxChoiceSource), so the rows of one level are
-// independent once each knows its decision number (= the count of nonempty
-// rows before it in the root's level) and its children's offset (= the sum
-// of the earlier rows' choice counts). A group of kGroupLanes lanes takes a
-// root and walks each level kGroupLanes rows at a time; segmented scans over
-// the group give both numbers. Same outputs as k_expand<., true, .>.
+template <int KCAP, bool PHILOX, bool LOCAL>
+__global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
+    extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree), then the recip table
+    const int r = p.r0 + blockIdx.x * blockDim.x + threadIdx.x;
+    // bounded() reciprocals in shared memory when the table is small
+    uint64_t* srecip = reinterpret_cast<uint64_t*>(cache + (size_t)p.cache_entries * blockDim.x);
+    const uint64_t* recip = p.recip;
+    if (p.recip_smem > 0) {
+        for (int i = threadIdx.x; i < p.recip_smem; i += blockDim.x) srecip[i] = p.recip[i];
+        __syncthreads();
+        recip = srecip;
+    }
+    if (r >= p.R) return;
+    expand_root<KCAP, PHILOX, LOCAL>(p, r, p.cache_entries > 0 ? cache : nullptr, blockDim.x, threadIdx.x, recip);
+}
+
+// Decision-parallel K1: the rows of one level are independent once each knows
+// its decision number (= nonempty rows before it in the root's order) and its
+// children's offset (= the sum of the earlier rows' choice counts). A group of
+// GL lanes takes a root and walks each level GL rows at a time; segmented
+// scans over the group give both numbers.
+//   Philox (PhiloxChoiceSource): draws are counter-based, so
+//     every lane evaluates its own decisions.
+//   xoshiro (PerRootChoiceSource): the stream is sequential, but a decision's
+//     draws are the stream draws at its children's offset (one draw per child
+//     unless bounded() rejects, probability < 4e-18 per draw at C2): lane 0 of
+//     the group generates the chunk's draws into shared memory, each lane
+//     consumes its own. A rejection anywhere sends the root to the serial
+//     per-root path (expand_root), which reproduces the reference exactly.
+// Same outputs as k_expand.
 #ifndef HGS_K1_GL
 #define HGS_K1_GL 4
 #endif
-constexpr int kGroupLanes = HGS_K1_GL;
-template <int KCAP>
+#ifndef HGS_K1X_GL
+#define HGS_K1X_GL 4
+#endif
+template <bool PHILOX>
+constexpr int group_lanes() { return PHILOX ? HGS_K1_GL : HGS_K1X_GL; }
+
+template <int KCAP, bool PHILOX>
 __global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
-    extern __shared__ uint64_t srecip_g[];
+    extern __shared__ uint64_t smem_g[];  // recip table, then (xoshiro) per-group draw buffers
+    constexpr int GL = group_lanes<PHILOX>();
     const uint64_t* recip = p.recip;
     if (p.recip_smem > 0) {
-        for (int i = threadIdx.x; i < p.recip_smem; i += blockDim.x) srecip_g[i] = p.recip[i];
+        for (int i = threadIdx.x; i < p.recip_smem; i += blockDim.x) smem_g[i] = p.recip[i];
         __syncthreads();
-        recip = srecip_g;
+        recip = smem_g;
     }
-    constexpr int GL = kGroupLanes;
+    uint64_t* buf = smem_g + ((p.recip_smem + 1) & ~1) + (size_t)(threadIdx.x / GL) * (GL * KCAP);
     const int gl = threadIdx.x & (GL - 1);
     const unsigned gmask = ((1u << GL) - 1u) << (threadIdx.x & 31 & ~(GL - 1));
     const int r = p.r0 + (int)((blockIdx.x * blockDim.x + threadIdx.x) / GL);
     if (r >= p.R) return;  // whole groups leave together
+    if (!PHILOX && p.force_serial > 0 && r % p.force_serial == 0) {  // test hook: the exact fallback
+        if (gl == 0) expand_root<KCAP, false, false>(p, r, nullptr, 1, 0, recip);
+        return;
+    }
     const int32_t root = p.roots32 ? p.roots32[r] : (int32_t)p.roots64[r];
     if (root < 0 || root >= p.n) {
         if (gl == 0) {
@@ -364,24 +408,17 @@ __global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
         }
         return;
     }
-    uint64_t seed;
-    if (p.seeds) seed = p.seeds[r];
-    else {
-        int lo = 0, hi = p.k - 1;
-        while (lo < hi) {
-            const int mid = (lo + hi + 1) >> 1;
-            if (__ldg(p.batch_off + mid) <= r) lo = mid; else hi = mid - 1;
-        }
-        uint64_t path[8];
-        for (int i = 0; i < 6; ++i) path[i] = p.spec.path[i];
-        const int len = p.spec.path_len;
-        path[len] = (uint64_t)(p.spec.batch_base + lo);
-        path[len + 1] = (uint64_t)(r - __ldg(p.batch_off + lo));
-        seed = derive_seed(p.spec.seed, path, len + 2);
+    const uint64_t seed = root_seed(p, r);
+    RootStream<true> rs;  // Philox
+    Xoshiro256 xs{};      // xoshiro: lane 0's copy is the stream
+    if constexpr (PHILOX) rs.init(seed, nullptr);
+    else if (gl == 0) {
+        if (p.state) {
+            const uint64_t* st = p.state + 4 * (size_t)r;
+            xs.a = st[0]; xs.b = st[1]; xs.c = st[2]; xs.d = st[3];
+        } else xs.seed(seed);
     }
-    RootStream<true> rs;
-    rs.init(seed, nullptr);
-    const uint32_t dec0 = p.state ? (uint32_t)p.state[r] : 0u;
+    const uint32_t dec0 = (PHILOX && p.state) ? (uint32_t)p.state[r] : 0u;
     uint32_t dec = dec0;
     int32_t* out = p.touched + (size_t)r * p.stride;
     int32_t* lc = p.level_counts + (size_t)r * (p.depth + 1);
@@ -391,7 +428,7 @@ __global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
     }
     __syncwarp(gmask);
     int T = 1, lvl_begin = 0, lvl_end = 1;
-    bool bad = false;
+    bool bad = false, rej = false;
     for (int level = 0; level < p.depth && !bad; ++level) {
         const int next_begin = T;
         // rows of the level's next chunk are loaded one chunk ahead
@@ -423,10 +460,21 @@ __global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
                 if (gl >= o) { pn += xn; pk += xk; }
             }
             const uint32_t tn = __shfl_sync(gmask, pn, GL - 1, GL), tk = __shfl_sync(gmask, pk, GL - 1, GL);
+            if constexpr (!PHILOX) {
+                if (gl == 0)
+                    for (uint32_t t = 0; t < tk; ++t) buf[t] = xs.next();
+                __syncwarp(gmask);
+            }
             if (k > 0) {
-                rs.begin_decision(dec + pn - 1);
                 uint32_t pos[KCAP];
-                choose_small<KCAP, true>(rs, (uint32_t)deg, k, recip, pos);
+                if constexpr (PHILOX) {
+                    rs.begin_decision(dec + pn - 1);
+                    choose_small<KCAP>(rs, (uint32_t)deg, k, recip, pos);
+                } else {
+                    BufStream bs{buf + (pk - k)};
+                    choose_small<KCAP>(bs, (uint32_t)deg, k, recip, pos);
+                    rej |= bs.rejected;
+                }
                 int32_t c[KCAP];
 #pragma unroll
                 for (int q = 0; q < KCAP; ++q) c[q] = q < (int)k ? __ldg(p.w_ci + b + pos[q]) : 0;
@@ -435,20 +483,26 @@ __global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
                 for (int q = 0; q < KCAP; ++q)
                     if (q < (int)k) dst[q] = c[q];
             }
+            if constexpr (!PHILOX) __syncwarp(gmask);  // the buffer is refilled by the next chunk
             T += (int)tk;
             dec += tn;
         }
         __syncwarp(gmask);  // this level's children are visible to the whole group
+        if (!PHILOX && __any_sync(gmask, rej)) break;
         if (gl == 0 && !bad) lc[level + 1] = T - next_begin;
         lvl_begin = next_begin;
         lvl_end = T;
     }
-    uint32_t dr = rs.draws;
+    if (!PHILOX && __any_sync(gmask, rej)) {  // a rejected draw shifted the stream: redo exactly
+        if (gl == 0) expand_root<KCAP, false, false>(p, r, nullptr, 1, 0, recip);
+        return;
+    }
+    uint32_t dr = PHILOX ? rs.draws : 0u;
 #pragma unroll
     for (int o = GL / 2; o > 0; o >>= 1) dr += __shfl_down_sync(gmask, dr, o, GL);
     if (gl == 0) {
         p.tcount[r] = T;
-        p.draws[r] = dr;
+        p.draws[r] = PHILOX ? dr : (uint32_t)(T - 1);  // xoshiro: one draw per child
         p.decisions[r] = dec - dec0;
     }
 }
@@ -475,7 +529,7 @@ __global__ void __launch_bounds__(128) k_sample_rows(RowsParams p) {
         int64_t* dst = p.out_cols + p.out_off[r];
         if (k <= 8) {
             uint32_t pos[8];
-            choose_small<8, PHILOX>(rs, deg, k, p.recip, pos);
+            choose_small<8>(rs, deg, k, p.recip, pos);
             for (uint32_t q = 0; q < k; ++q) dst[q] = p.col[b + pos[q]];
         } else {
             uint32_t lpos[kLocalK], ldp[kLocalK], ldv[kLocalK];
@@ -501,6 +555,10 @@ void launch_sample_rows(const RowsParams& p, bool philox, cudaStream_t st) {
     HGS_CUDA(cudaGetLastError());
 }
 
+// HGS_K1_GROUPX=1: the decision-parallel kernel for xoshiro streams (see
+// HGS_K1X_GROUP); read per call.
+static bool getenv_flag_k1_groupx() { return getenv("HGS_K1_GROUPX") != nullptr; }
+
 template <int KCAP, bool PH, bool LOCAL>
 static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cudaStream_t st) {
     auto kern = k_expand<KCAP, PH, LOCAL>;
@@ -511,13 +569,15 @@ static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cu
     HGS_CUDA(cudaGetLastError());
 }
 
-template <int KCAP>
+template <int KCAP, bool PHILOX>
 static void launch_expand_group(const ExpandParams& ep, cudaStream_t st) {
-    const size_t smem = (size_t)ep.recip_smem * sizeof(uint64_t);
-    auto kern = k_expand_group<KCAP>;
+    constexpr int GL = group_lanes<PHILOX>();
+    const size_t smem = (size_t)((ep.recip_smem + 1) & ~1) * sizeof(uint64_t) +
+                        (PHILOX ? 0 : (size_t)128 * KCAP * sizeof(uint64_t));
+    auto kern = k_expand_group<KCAP, PHILOX>;
     if (smem > 48 * 1024)
         HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
-    const int64_t threads = (int64_t)(ep.R - ep.r0) * kGroupLanes;
+    const int64_t threads = (int64_t)(ep.R - ep.r0) * GL;
     kern<<<(unsigned)((threads + 127) / 128), 128, smem, st>>>(ep);
     HGS_CUDA(cudaGetLastError());
 }
@@ -525,13 +585,29 @@ static void launch_expand_group(const ExpandParams& ep, cudaStream_t st) {
 #ifndef HGS_K1_GROUP
 #define HGS_K1_GROUP 1
 #endif
+// The decision-parallel xoshiro path is opt-in (HGS_K1X_GROUP=1 at build
+// time or HGS_K1_GROUPX=1 at run time): measured on B200 at C2 it takes
+// 0.175 ms (4-lane groups; 2: 0.182, 8: 0.243) against 0.166 for one lane
+// per root — lane 0's serial stream generation idles the other lanes.
+#ifndef HGS_K1X_GROUP
+#define HGS_K1X_GROUP 0
+#endif
 
 void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,
                    cudaStream_t st) {
-    if (HGS_K1_GROUP && philox && kmax <= 8 && ep.R > ep.r0) {  // decision-parallel Philox path
-        if (kmax > 6) launch_expand_group<8>(ep, st);
-        else if (kmax > 4) launch_expand_group<6>(ep, st);
-        else launch_expand_group<4>(ep, st);
+    // decision-parallel paths for choices of <= 8 (the register network);
+    // the xoshiro one needs no uploaded resume state beyond the 4 words
+    const bool group = philox ? HGS_K1_GROUP : (HGS_K1X_GROUP || getenv_flag_k1_groupx());
+    if (group && kmax <= 8 && ep.R > ep.r0) {
+        if (philox) {
+            if (kmax > 6) launch_expand_group<8, true>(ep, st);
+            else if (kmax > 4) launch_expand_group<6, true>(ep, st);
+            else launch_expand_group<4, true>(ep, st);
+        } else {
+            if (kmax > 6) launch_expand_group<8, false>(ep, st);
+            else if (kmax > 4) launch_expand_group<6, false>(ep, st);
+            else launch_expand_group<4, false>(ep, st);
+        }
         return;
     }
     // register fast path for k <= 8, sized to the call's largest choice

@@ -44,6 +44,7 @@ struct ExpandParams {
     int32_t* __restrict__ ticket;         // [0] ticket, [1] error code, [2] root, [3] aux
     uint32_t* __restrict__ big;           // choices > kLocalK: 3 x big_k words per root of the launch
     int32_t big_k;
+    int32_t force_serial;                 // test hook: roots r % force_serial == 0 take the serial path
 };
 
 void launch_expand(int threads, size_t smem, int64_t kmax, const ExpandParams& ep, bool philox,

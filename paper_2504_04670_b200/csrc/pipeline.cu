@@ -235,6 +235,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     ep.recip_smem = c.recip_smem;
     ep.touched = s->touched.p; ep.tcount = s->tcount.p; ep.level_counts = s->level_counts.p;
     ep.draws = s->draws.p; ep.decisions = s->decisions.p; ep.ticket = s->ticket.p;
+    if (const char* e = getenv("HGS_K1_FORCE_SERIAL")) ep.force_serial = atoi(e);  // test hook
 
     ExtractParams xp{};
     xp.a_rp = g.a.rp.p; xp.a_ci = g.a.ci.p; xp.a_gid = g.has_gid ? g.a_gid.p : nullptr; xp.a_ri = g.a_ri.p;

@@ -623,3 +623,53 @@ def test_c2_full_workload():
     assert (S.counts.V, S.counts.E) == (ref.V, ref.E) == (14330269, 17161199)
     assert_same(dev, ref, True)
     del rows
+
+
+def test_hub_root_gets_exact_slots():
+    """One root whose induced subgraph has ~11k edges among 4,096 small ones:
+    growing every root's edge slot to fit it would take (R+1) x 16,384 slots,
+    so the re-run places edges at exact per-root offsets instead (ADVICE r1:
+    a hub no longer inflates every slot or fails with an allocation error)."""
+    H = hgs()
+    rs = np.random.default_rng(17)
+    n, clique = 40000, 150
+    u = rs.integers(0, n, 120000)
+    v = rs.integers(0, n, 120000)
+    cu, cv = np.meshgrid(np.arange(clique), np.arange(clique), indexing="ij")
+    u = np.concatenate([u, cu.ravel()])
+    v = np.concatenate([v, cv.ravel()])
+    keep = u != v
+    key = np.unique(u[keep].astype(np.int64) * n + v[keep])
+    rp = np.concatenate([[0], np.cumsum(np.bincount(key // n, minlength=n))]).astype(np.int64)
+    g = O.Graph(n=n, rp=rp, ci=(key % n).astype(np.int64))
+    g.node_feat, g.edge_feat = rs.standard_normal((n, 6)), rs.standard_normal((len(key), 2))
+    g.labels = rs.integers(0, 2, len(key)).astype(np.uint8)
+    roots = np.concatenate([[3], rs.choice(np.arange(clique, n), 4095, replace=False)]).astype(np.int64)
+    boff = np.array([0, 2048, 4096], np.int64)
+    seeds = rs.integers(0, 2**63, 4096, dtype=np.uint64)
+    kw = dict(depth=2, fanout=60, gather=True)
+    dev, S = device_run(g, roots, boff, seeds, **kw)
+    assert S.reruns() == 1
+    ref = O.bulk_shadow(g, roots, boff, seeds, **kw)
+    assert ref.batch_eoff[1] > 11000
+    assert_same(dev, ref, True)
+
+
+@pytest.mark.parametrize("every", [0, 1, 3])
+def test_k1_xoshiro_serial_fallback(monkeypatch, every):
+    """The decision-parallel xoshiro K1 (HGS_K1_GROUPX=1) hands a root whose
+    stream saw a rejected draw to the serial per-root path; HGS_K1_FORCE_SERIAL
+    forces that path for every `every`-th root (0: none). Mixed roots give the oracle's outputs and
+    per-root draw / decision counts."""
+    monkeypatch.setenv("HGS_K1_GROUPX", "1")
+    monkeypatch.setenv("HGS_K1_FORCE_SERIAL", str(every))
+    g = random_graph(6000, 60000, 23)
+    rs = np.random.default_rng(23)
+    roots = np.concatenate([rs.permutation(6000)[:500] for _ in range(3)]).astype(np.int64)
+    boff = np.array([0, 500, 1000, 1500], np.int64)
+    seeds = rs.integers(0, 2**63, 1500, dtype=np.uint64)
+    state = rs.integers(0, 2**63, 4 * 1500, dtype=np.uint64)
+    for st in (None, state):
+        dev, _ = device_run(g, roots, boff, seeds, depth=3, fanout=6, gather=True, state=st)
+        ref = O.bulk_shadow(g, roots, boff, seeds, depth=3, fanout=6, gather=True, state=st)
+        assert_same(dev, ref, True)
