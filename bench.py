@@ -155,6 +155,18 @@ class Clocks:
 # reference / CPU baseline
 
 
+def cpu_model() -> str:
+    try:
+        with open("/proc/cpuinfo") as f:
+            for line in f:
+                if line.startswith("model name"):
+                    return line.split(":", 1)[1].strip()
+    except OSError:
+        pass
+    import platform
+    return platform.processor() or "unknown"
+
+
 def cpu_sample_time(ev, n_batches, threads, rep0=1000):
     """Reference bulk_shadow + gather_features (oracle/_ref) on n_batches of the
     workload, batch-sharded over `threads`. Falls back to the C restatement
@@ -179,7 +191,11 @@ def run_reference(args, world, rank):
     from paper_2504_04670_b200 import workload as W
     ev = W.preset_event(WORKLOAD)
     threads = os.cpu_count() or 1
-    nb = max(threads, 8)
+    # one step = the GPU arm's own call (K_BATCHES minibatches of BATCH roots),
+    # as one bulk_shadow + gather_features over contiguous batch ranges on all
+    # host threads (each thread one reference call: one symmetrize_pattern per
+    # thread per step, sampler.cpp:129)
+    nb = K_BATCHES
     times = []
     kind = None
     for i in range(args.warmup + args.steps):
@@ -192,9 +208,9 @@ def run_reference(args, world, rank):
             "warmup": args.warmup, "ms_per_step": 1e3 * total / len(times), "higher_is_better": True,
             "scaling": "strong" if WORKLOAD == "C3" else "weak", "vs_baseline": None, "dtype": "int64", "data": "synthetic",
             "impl": "reference", "config": config_dict(world, ev),
-            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind,
-                             "sample": f"{nb} minibatches x {BATCH} roots of {WORKLOAD} per step, "
-                                       f"bulk_shadow+gather_features, batch-sharded over "
+            "cpu_baseline": {"value": value, "unit": UNIT, "cores": threads, "kind": kind, "cpu_model": cpu_model(),
+                             "sample": f"{nb} minibatches x {BATCH} roots of {WORKLOAD} per step (the GPU arm's "
+                                       f"call), bulk_shadow+gather_features over contiguous batch ranges on "
                                        f"{threads} threads"},
             "e2e": {"value": value, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
@@ -202,6 +218,24 @@ def run_reference(args, world, rank):
 
 # ----------------------------------------------------------------------------
 # the GPU arm
+
+
+def distinct_devices(world, dev) -> int:
+    """Number of distinct physical GPUs the ranks run on (device UUIDs). A
+    multi-rank line is only printed when every rank has its own GPU; the
+    HGS_FORCE_DEVICE test hook (several ranks on one GPU over gloo) reports
+    the true device count and marks the line."""
+    import torch
+    uuid = str(torch.cuda.get_device_properties(dev).uuid)
+    if world == 1:
+        return 1
+    import torch.distributed as dist
+    allu = [None] * world
+    dist.all_gather_object(allu, uuid)
+    n = len(set(allu))
+    if n < world and os.environ.get("HGS_FORCE_DEVICE") is None:
+        raise SystemExit(f"bench: {world} ranks share {n} GPU(s); refusing to report a multi-GPU number")
+    return n
 
 
 def byte_model(st, f_v, f_e, gather=True):
@@ -227,6 +261,7 @@ def run_gpu(args, world, rank, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    n_dev = distinct_devices(world, dev)
     t0 = time.time()
     ev = W.preset_event(WORKLOAD)
     log(f"[rank {rank}] event n={ev.n} m={ev.m} generated in {time.time() - t0:.1f}s")
@@ -268,16 +303,23 @@ def run_gpu(args, world, rank, local_rank):
     torch.cuda.synchronize()
     ev0 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
     ev1 = [torch.cuda.Event(enable_timing=True) for _ in range(args.steps)]
-    step_ms, kern, stats, launches = [], [], [], 0
+    step_ms, wall_ms, kern, stats, launches = [], [], [], [], 0
     with Clocks(local_rank) as clk:
         for j in range(args.steps):
             i = args.warmup + j
             with torch.cuda.stream(stream):
                 flush.zero_()
+            if world > 1:  # every rank starts the step together; the wall clock runs to the last rank's end
+                stream.synchronize()
+                dist.barrier()
+            tw = time.perf_counter()
             ev0[j].record(stream)
             step_device(i, False)
             ev1[j].record(stream)
             S.wait()
+            if world > 1:
+                dist.barrier()
+            wall_ms.append(1e3 * (time.perf_counter() - tw))
             if S.reruns():  # a capacity re-run inside wait() would run outside ev0..ev1
                 raise RuntimeError("bench: a timed step needed a capacity re-run; warm-up did not size the buffers")
             step_ms.append(ev0[j].elapsed_time(ev1[j]))
@@ -333,13 +375,27 @@ def run_gpu(args, world, rank, local_rank):
                 h2d = pr.nbytes + pb.nbytes + ps.nbytes
                 d2h = (4 * 2 * (c.k + 1) + 4 * (c.R + c.k) + 4 * c.V + 4 * c.R + 12 * c.E
                        + 8 * c.V * G.f_v + 8 * c.E * G.f_e + c.E + 8 * c.R)
-    total_ms = float(sum(step_ms))
     e2e_total = float(sum(e2e_s))
-    if world > 1:
-        t = torch.tensor([total_ms, e2e_total], device=dev if dist.get_backend() == "nccl" else "cpu",
+    if world > 1:  # per step: the slowest rank's device time; then the sum over steps
+        t = torch.tensor(step_ms + [e2e_total], device=dev if dist.get_backend() == "nccl" else "cpu",
                          dtype=torch.float64)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
-        total_ms, e2e_total = float(t[0]), float(t[1])
+        step_ms, e2e_total = [float(x) for x in t[:-1]], float(t[-1])
+    total_ms = float(sum(step_ms))
+    # C++ drop-in end to end (rank 0, one GPU): std::vector<SampledBatch> out
+    e2e_cpp = None
+    if rank == 0 and not args.no_dropin_e2e and WORKLOAD in ("C1", "C2"):
+        roots_h, boff_h, seeds_h = host_in[args.warmup]
+        e2e_cpp = {}
+        for mode, name in ((0, "device_event"), (1, "trainer_two_lines")):
+            sec, V, E = W.dropin_time(ev, roots_h, boff_h, seeds_h, depth=DEPTH, fanout=FANOUT, mode=mode,
+                                      warmup=1, reps=3)
+            e2e_cpp[name] = {"value": K_BATCHES / float(np.mean(sec)), "unit": UNIT, "s_per_call": float(np.mean(sec)),
+                             "V": V, "E": E}
+        e2e_cpp["path"] = ("C++ drop-in, host int64 vectors in, std::vector<SampledBatch> with gathered fp64 "
+                           "features out, wall clock: device_event = gpu::DeviceEvent::bulk_shadow(gather); "
+                           "trainer_two_lines = hitgnn::bulk_shadow(edge-id A) + gather_features per batch "
+                           "(trainer.cpp:457-458) through the resident-graph cache")
     if rank != 0:
         return
     mb = world * K_BATCHES * args.steps
@@ -365,7 +421,7 @@ def run_gpu(args, world, rank, local_rank):
         with open(prof) as f:
             traffic = json.load(f).get("dram_bytes_per_launch")
     line = {
-        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+        "metric": METRIC, "value": value, "unit": UNIT, "n_gpus": n_dev, "steps": args.steps,
         "warmup": args.warmup, "ms_per_step": total_ms / args.steps, "higher_is_better": True,
         "scaling": "strong" if WORKLOAD == "C3" else "weak", "vs_baseline": None, "dtype": "int32", "data": "synthetic",
         "config": config_dict(world, ev),
@@ -387,15 +443,31 @@ def run_gpu(args, world, rank, local_rank):
                 "path": "hgs_sample_run (host int64 inputs, pinned) + hgs_sample_copy_to_host "
                         "(all outputs, pinned), wall clock"},
         "counts_per_step": {k: int(np.mean([s[k] for s in stats])) for k in ("V", "E", "S")},
+        "timing": ("CUDA events on the sampling stream around each step, per step the max over ranks, summed"
+                   + ("; wall_ms_per_step = barrier -> all ranks done" if world > 1 else "")),
     }
+    if world > 1:
+        line["wall_ms_per_step"] = float(np.mean(wall_ms))
+        line["ranks"] = world
+    if e2e_cpp:
+        line["e2e_cpp"] = e2e_cpp
     if world == 1 and not args.no_cpu_baseline:
+        # (i) all host threads on the call's own shape (K_BATCHES minibatches,
+        # contiguous batch ranges per thread); (ii) one thread, the reference as
+        # shipped (trainer.cpp:457 samples on the caller thread), on a
+        # 2-minibatch sample
         threads = os.cpu_count() or 1
-        nb = 2 * threads
+        nb = K_BATCHES
         t, V, E, kind = cpu_sample_time(ev, nb, threads)
+        nb1 = 2
+        t1, _, _, _ = cpu_sample_time(ev, nb1, 1, rep0=1500)
         line["cpu_baseline"] = {"value": nb / t, "unit": UNIT, "cores": threads, "kind": kind,
-                                "sample": f"{nb} minibatches x {BATCH} roots of {WORKLOAD}, "
-                                          f"bulk_shadow+gather_features, batch-sharded over "
-                                          f"{threads} host threads ({t:.1f}s wall)"}
+                                "cpu_model": cpu_model(),
+                                "value_1thread": nb1 / t1,
+                                "sample": f"{nb} minibatches x {BATCH} roots of {WORKLOAD} (the GPU call), "
+                                          f"bulk_shadow+gather_features over contiguous batch ranges on "
+                                          f"{threads} host threads ({t:.1f}s wall); 1-thread figure: {nb1} "
+                                          f"minibatches on one thread ({t1:.1f}s)"}
     print(json.dumps(line), flush=True)
 
 
@@ -412,6 +484,7 @@ def run_epoch(args, world, rank, local_rank):
 
     dev = torch.device("cuda", local_rank)
     torch.cuda.set_device(dev)
+    n_dev = distinct_devices(world, dev)
     mine = list(range(rank, args.events, world))
     t0 = time.time()
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
@@ -454,7 +527,7 @@ def run_epoch(args, world, rank, local_rank):
         total_ms, mbs = float(t[0]), int(t[1])
     if rank != 0:
         return
-    line = {"metric": METRIC, "value": mbs / (total_ms / 1e3), "unit": UNIT, "n_gpus": world,
+    line = {"metric": METRIC, "value": mbs / (total_ms / 1e3), "unit": UNIT, "n_gpus": n_dev,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": total_ms / args.steps,
             "higher_is_better": True, "scaling": "strong", "vs_baseline": None, "dtype": "int32",
             "data": "synthetic",
@@ -486,6 +559,7 @@ def main():
                     help="C5: minibatches per sampling call (0 = all batches of an event in one call)")
     ap.add_argument("--workload", default="C2", choices=["C1", "C2", "C3", "C4", "C5"],
                     help="BASELINE.json config (C2 = the headline line)")
+    ap.add_argument("--no-dropin-e2e", action="store_true", help="skip the C++ drop-in e2e legs")
     ap.add_argument("--e2e-steps", type=int, default=None,
                     help="steps of the host-buffer e2e leg (default: all; fewer for C3/C4)")
     args = ap.parse_args()

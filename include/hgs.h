@@ -37,6 +37,7 @@
 #ifndef HGS_H
 #define HGS_H
 
+#include <stddef.h>
 #include <stdint.h>
 
 #ifdef __cplusplus
@@ -118,6 +119,13 @@ typedef struct {
 const char* hgs_last_error(void);
 int hgs_abi_version(void);
 int hgs_device_count(int* count);
+/* Page-locked host memory (cudaMallocHost / cudaFreeHost) for staging
+ * buffers of host callers that do not link the CUDA runtime themselves. */
+int hgs_host_alloc(size_t bytes, void** out);
+int hgs_host_free(void* p);
+/* The calling thread's current CUDA device (cudaGetDevice): the device the
+ * C++ drop-in's reference-signature entry points use. */
+int hgs_current_device(int* device);
 
 /* ---- graph store ---------------------------------------------------------
  * A in the reference's CsrMatrix layout (int64 row_ptr[n_rows+1],

@@ -34,6 +34,16 @@ void hgs_event_copy(const hgs_event* ev, int64_t* row_ptr, int64_t* col_idx, dou
 void hgs_event_free(hgs_event* ev);
 const char* hgs_tools_last_error(void);
 
+/* End-to-end timing of the C++ drop-in (host arrays in, std::vector<SampledBatch>
+ * with gathered features out): mode 0 = gpu::DeviceEvent::bulk_shadow(gather),
+ * mode 1 = the reference trainer's bulk_shadow + per-batch gather_features
+ * (trainer.cpp:457-458). seconds[reps] wall clock per rep; ve = {V, E}. */
+int hgs_dropin_time(int64_t n, const int64_t* row_ptr, const int64_t* col_idx, const double* node_feat,
+                    int64_t f_v, const double* edge_feat, int64_t f_e, const uint8_t* labels,
+                    const int64_t* roots, const int64_t* batch_off, int64_t n_batches, const uint64_t* seeds,
+                    int64_t depth, int64_t fanout, int32_t mode, int32_t warmup, int32_t reps, double* seconds,
+                    int64_t* ve);
+
 /* epoch_root_batches (sampler.cpp:245-263) with Rng(rng_seed): writes the
  * shuffled permutation of [0, n) to perm; returns the number of batches. */
 int64_t hgs_epoch_root_batches(int64_t n, int64_t batch_size, uint64_t rng_seed, int64_t* perm);

@@ -282,6 +282,22 @@ std::vector<std::vector<Index>> epoch_root_batches(Index n_vertices, Index batch
 
 namespace gpu {
 
+// Resident-graph cache behind the reference-signature entry points.
+// bulk_shadow / shadow_reference (A) and gather_features (the event's
+// features) keep what they upload on the calling thread's current CUDA
+// device, so the reference's call pattern (trainer.cpp:457-458: the same
+// edge-id matrix and EventGraph every chunk) uploads each event once.
+//   A: keyed by device, object address, array pointers, sizes and a full
+//      content hash of row_ptr / col_idx / values (checked on every call).
+//   event: keyed by device, address, array pointers, sizes and a sampled
+//      content fingerprint (4,096 strided elements + both ends of every
+//      array); an EventGraph mutated in place at other positions must be
+//      released (release_cached) or HGS_DROPIN_VERIFY=full set (full hash).
+// Up to 16 entries, least recently used evicted; HGS_DROPIN_CACHE=0 disables
+// the cache (upload per call, the pre-cache behaviour).
+void release_cached();
+std::size_t cached_entries();
+
 // An event resident on one GPU: A (edge ids), walk, features. Create once per
 // event (next to make_edge_id_matrix in Trainer's constructor) and sample
 // from it repeatedly; bulk_shadow(..., gather = true) returns batches with

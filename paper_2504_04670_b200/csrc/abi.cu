@@ -89,6 +89,27 @@ int hgs_device_count(int* count) {
     });
 }
 
+int hgs_host_alloc(size_t bytes, void** out) {
+    return guarded([&] {
+        if (!out) fail(HGS_EINVAL, "hgs_host_alloc: null argument");
+        *out = nullptr;
+        if (bytes) HGS_CUDA(cudaMallocHost(out, bytes));
+    });
+}
+
+int hgs_host_free(void* p) {
+    return guarded([&] {
+        if (p) HGS_CUDA(cudaFreeHost(p));
+    });
+}
+
+int hgs_current_device(int* device) {
+    return guarded([&] {
+        if (!device) fail(HGS_EINVAL, "hgs_current_device: null argument");
+        HGS_CUDA(cudaGetDevice(device));
+    });
+}
+
 uint64_t hgs_derive(uint64_t seed, const uint64_t* path, int32_t len) { return derive_seed(seed, path, len); }
 
 void hgs_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]) {
@@ -258,10 +279,14 @@ int hgs_graph_gather(hgs_graph* h, const int64_t* l2g, int64_t V, const int64_t*
                 fail(HGS_EINVAL, "gather_features: adjacency values do not carry edge ids; "
                                  "sample from make_edge_id_matrix(event)");
         HGS_CUDA(cudaSetDevice(g.device));
+        // per-graph grow-only scratch (no cudaMalloc per batch); one gather at a time per graph
+        std::lock_guard<std::mutex> lk(g.gather_mu);
         cudaStream_t st = g.stream;
-        DevBuf<int64_t> dl, de;
-        DevBuf<double> dx, dy;
-        DevBuf<uint8_t> db;
+        DevBuf<int64_t>& dl = g.g_l2g;
+        DevBuf<int64_t>& de = g.g_eid;
+        DevBuf<double>& dx = g.g_xv;
+        DevBuf<double>& dy = g.g_ye;
+        DevBuf<uint8_t>& db = g.g_lab;
         dl.reserve((size_t)V + 1); de.reserve((size_t)E + 1);
         dx.reserve((size_t)(V * g.f_v) + 1); dy.reserve((size_t)(E * g.f_e) + 1); db.reserve((size_t)E + 1);
         upload(dl.p, l2g, sizeof(int64_t) * V, st);

@@ -5,6 +5,11 @@
 // reference's SampledBatch values.
 #include <algorithm>
 #include <cmath>
+#include <cstdlib>
+#include <cstring>
+#include <memory>
+#include <mutex>
+#include <thread>
 #include <numeric>
 #include <string>
 
@@ -42,6 +47,203 @@ bool values_are_ids(const CsrMatrix& a) {
     for (std::size_t k = 0; k < a.values.size(); ++k)
         if (a.values[k] != static_cast<double>(k) + 1.0) return false;
     return true;
+}
+
+int current_device() {
+    int d = 0;
+    check(hgs_current_device(&d));
+    return d;
+}
+
+// ---- resident-graph cache (see include/hitgnn/core.hpp, gpu::release_cached)
+
+std::uint64_t rotl64(std::uint64_t x, int r) { return (x << r) | (x >> (64 - r)); }
+
+// Content hash for change detection: four independent multiply-rotate lanes.
+std::uint64_t hash_bytes(const void* p, std::size_t bytes, std::uint64_t h) {
+    constexpr std::uint64_t K = 0x9E3779B97F4A7C15ULL;
+    const auto* c = static_cast<const unsigned char*>(p);
+    std::uint64_t a = h ^ 0x243F6A8885A308D3ULL, b = h ^ 0x13198A2E03707344ULL, d = h ^ 0xA4093822299F31D0ULL,
+                  e = h ^ 0x082EFA98EC4E6C89ULL;
+    std::size_t i = 0;
+    for (; i + 32 <= bytes; i += 32) {
+        std::uint64_t w[4];
+        std::memcpy(w, c + i, 32);
+        a = rotl64(a ^ w[0], 29) * K;
+        b = rotl64(b ^ w[1], 29) * K;
+        d = rotl64(d ^ w[2], 29) * K;
+        e = rotl64(e ^ w[3], 29) * K;
+    }
+    for (; i < bytes; ++i) a = rotl64(a ^ c[i], 29) * K;
+    return rotl64(a, 1) ^ rotl64(b, 7) ^ rotl64(d, 13) ^ rotl64(e, 19) ^ (bytes * K);
+}
+
+// Sampled fingerprint: 4,096 strided elements plus the first and last 4 KB.
+std::uint64_t fingerprint_bytes(const void* p, std::size_t bytes, std::uint64_t h, bool full) {
+    if (full || bytes <= 65536) return hash_bytes(p, bytes, h);
+    const auto* c = static_cast<const unsigned char*>(p);
+    h = hash_bytes(c, 4096, h);
+    h = hash_bytes(c + bytes - 4096, 4096, h);
+    const std::size_t step = (bytes - 8) / 4096;
+    for (std::size_t i = 0; i < 4096; ++i) h = hash_bytes(c + i * step, 8, h);
+    return h;
+}
+
+struct CacheKey {
+    int device = 0;
+    int kind = 0;  // 0: A (sampling), 1: event (features)
+    const void* obj = nullptr;
+    const void* ptr[4] = {};
+    std::int64_t size[4] = {};
+    std::uint64_t hash = 0;
+    bool operator==(const CacheKey& o) const {
+        return device == o.device && kind == o.kind && obj == o.obj && hash == o.hash &&
+               std::equal(ptr, ptr + 4, o.ptr) && std::equal(size, size + 4, o.size);
+    }
+};
+
+struct CacheEntry {
+    CacheKey key;
+    hgs_graph* g = nullptr;
+    std::vector<hgs_sample*> idle;  // sample handles not in use
+    int in_use = 0;
+    std::uint64_t tick = 0;
+    bool ids = true;  // A: values are make_edge_id_matrix ids
+    ~CacheEntry() {
+        for (hgs_sample* s : idle) hgs_sample_destroy(s);
+        if (g) hgs_graph_destroy(g);
+    }
+};
+
+struct Cache {
+    std::mutex mu;
+    std::vector<std::unique_ptr<CacheEntry>> entries;
+    std::uint64_t tick = 0;
+};
+Cache& cache() {
+    static Cache* c = new Cache;  // never destroyed: handles may outlive static teardown order
+    return *c;
+}
+
+bool cache_enabled() {
+    const char* e = std::getenv("HGS_DROPIN_CACHE");
+    return !(e && std::string(e) == "0");
+}
+bool verify_full() {
+    const char* e = std::getenv("HGS_DROPIN_VERIFY");
+    return e && std::string(e) == "full";
+}
+
+// A borrowed (graph, sample handle) pair; returned to the cache on scope exit
+// (or destroyed with the graph when the cache is off).
+struct Lease {
+    CacheEntry* entry = nullptr;
+    std::unique_ptr<CacheEntry> owned;  // cache disabled: private entry
+    hgs_sample* s = nullptr;
+    Lease() = default;
+    Lease(const Lease&) = delete;
+    ~Lease() {
+        if (owned) {
+            if (s) hgs_sample_destroy(s);
+            return;
+        }
+        if (!entry) return;
+        std::lock_guard<std::mutex> lk(cache().mu);
+        if (s) entry->idle.push_back(s);
+        --entry->in_use;
+    }
+    hgs_graph* graph() const { return owned ? owned->g : entry->g; }
+};
+
+// Find or build the entry for `key`, then borrow a sample handle of it.
+template <class Build>
+void lease(Lease& out, const CacheKey& key, Build&& build) {
+    if (!cache_enabled()) {
+        out.owned = std::make_unique<CacheEntry>();
+        out.owned->key = key;
+        build(*out.owned);
+        check(hgs_sample_create(out.owned->g, nullptr, &out.s));
+        return;
+    }
+    Cache& c = cache();
+    std::unique_lock<std::mutex> lk(c.mu);
+    CacheEntry* e = nullptr;
+    for (auto& p : c.entries)
+        if (p->key == key) e = p.get();
+    if (!e) {
+        lk.unlock();  // build (uploads) outside the lock
+        auto fresh = std::make_unique<CacheEntry>();
+        fresh->key = key;
+        build(*fresh);
+        lk.lock();
+        for (auto& p : c.entries)  // another thread may have built it meanwhile
+            if (p->key == key) e = p.get();
+        if (!e) {
+            constexpr std::size_t kMax = 16;
+            while (c.entries.size() >= kMax) {  // evict the least recently used idle entry
+                auto victim = c.entries.end();
+                for (auto it = c.entries.begin(); it != c.entries.end(); ++it)
+                    if ((*it)->in_use == 0 && (victim == c.entries.end() || (*it)->tick < (*victim)->tick))
+                        victim = it;
+                if (victim == c.entries.end()) break;
+                c.entries.erase(victim);
+            }
+            c.entries.push_back(std::move(fresh));
+            e = c.entries.back().get();
+        }
+    }
+    e->tick = ++c.tick;
+    ++e->in_use;
+    out.entry = e;
+    if (!e->idle.empty()) {
+        out.s = e->idle.back();
+        e->idle.pop_back();
+    }
+    lk.unlock();
+    if (!out.s) check(hgs_sample_create(e->g, nullptr, &out.s));
+}
+
+// A (sampling matrix): full content hash, values checked for the id pattern
+void lease_csr(Lease& out, const CsrMatrix& a) {
+    CacheKey key;
+    key.device = current_device();
+    key.kind = 0;
+    key.obj = &a;
+    key.ptr[0] = a.row_ptr.data(); key.ptr[1] = a.col_idx.data(); key.ptr[2] = a.values.data();
+    key.size[0] = a.n_rows; key.size[1] = a.n_cols; key.size[2] = static_cast<std::int64_t>(a.col_idx.size());
+    key.size[3] = static_cast<std::int64_t>(a.values.size());
+    std::uint64_t h = hash_bytes(a.row_ptr.data(), a.row_ptr.size() * sizeof(Index), 1);
+    h = hash_bytes(a.col_idx.data(), a.col_idx.size() * sizeof(Index), h);
+    h = hash_bytes(a.values.data(), a.values.size() * sizeof(double), h);
+    key.hash = h;
+    lease(out, key, [&](CacheEntry& e) {
+        e.ids = values_are_ids(a);
+        e.g = upload_csr(a, key.device, !e.ids);
+    });
+}
+
+void lease_event(Lease& out, const EventGraph& event) {
+    CacheKey key;
+    key.device = current_device();
+    key.kind = 1;
+    key.obj = &event;
+    key.ptr[0] = event.edges.entries.data(); key.ptr[1] = event.node_features.data.data();
+    key.ptr[2] = event.edge_features.data.data(); key.ptr[3] = event.labels.data();
+    key.size[0] = event.n; key.size[1] = event.m();
+    key.size[2] = event.node_features.cols; key.size[3] = event.edge_features.cols;
+    const bool full = verify_full();
+    std::uint64_t h = fingerprint_bytes(event.edges.entries.data(), event.edges.entries.size() * sizeof(CooEntry), 2, full);
+    h = fingerprint_bytes(event.node_features.data.data(), event.node_features.data.size() * sizeof(double), h, full);
+    h = fingerprint_bytes(event.edge_features.data.data(), event.edge_features.data.size() * sizeof(double), h, full);
+    h = fingerprint_bytes(event.labels.data(), event.labels.size(), h, full);
+    key.hash = h;
+    lease(out, key, [&](CacheEntry& e) {
+        const CsrMatrix a = make_edge_id_matrix(event);
+        e.g = upload_csr(a, key.device, false);
+        check(hgs_graph_attach_features(e.g, event.node_features.data.data(), event.node_features.cols,
+                                        event.edge_features.data.data(), event.edge_features.cols,
+                                        event.labels.data()));
+    });
 }
 
 // Run one bulk call on a resident graph and materialise SampledBatch values.
@@ -129,6 +331,58 @@ void emit_frontiers(hgs_graph* g, hgs_sample* s, const CsrMatrix& a, const std::
     }
 }
 
+// Page-locked host staging for one thread's calls (grow-only slots).
+struct Staging {
+    void* p[13] = {};
+    std::size_t cap[13] = {};
+    template <class T>
+    T* get(int slot, std::size_t n) {
+        const std::size_t bytes = std::max<std::size_t>(n, 1) * sizeof(T);
+        if (cap[slot] < bytes) {
+            if (p[slot]) hgs_host_free(p[slot]);
+            p[slot] = nullptr;
+            cap[slot] = 0;
+            const std::size_t want = bytes + bytes / 8;
+            check(hgs_host_alloc(want, &p[slot]));
+            cap[slot] = want;
+        }
+        return static_cast<T*>(p[slot]);
+    }
+    ~Staging() {
+        for (void* q : p)
+            if (q) hgs_host_free(q);
+    }
+};
+Staging& staging() {
+    thread_local Staging st;
+    return st;
+}
+
+// f(i) for i in [0, n) on up to hardware_concurrency host threads (the
+// per-batch SampledBatch values are independent).
+template <class F>
+void parallel_for(Index n, F&& f) {
+    const Index T = std::min<Index>(n, std::max<Index>(1, std::thread::hardware_concurrency()));
+    if (T <= 1) {
+        for (Index i = 0; i < n; ++i) f(i);
+        return;
+    }
+    std::vector<std::thread> pool;
+    std::exception_ptr err;
+    std::mutex emu;
+    for (Index t = 0; t < T; ++t)
+        pool.emplace_back([&, t] {
+            try {
+                for (Index i = t; i < n; i += T) f(i);
+            } catch (...) {
+                std::lock_guard<std::mutex> lk(emu);
+                if (!err) err = std::current_exception();
+            }
+        });
+    for (auto& th : pool) th.join();
+    if (err) std::rethrow_exception(err);
+}
+
 std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
                                    const std::vector<std::vector<Index>>& batches,
                                    const SamplerConfig& cfg, ChoiceSource& choice, bool gather,
@@ -179,27 +433,39 @@ std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
     check(hgs_sample_wait(s, counts));
     const Index V = counts[2], E = counts[3], k = static_cast<Index>(batches.size());
 
-    std::vector<int32_t> bvoff(k + 1), beoff(k + 1), comp(R + k), l2g(V), rl(R), er(E), ec(E), eg(E);
-    std::vector<std::uint32_t> draws(R), decisions(R);
-    std::vector<double> xv, ye;
-    std::vector<std::uint8_t> lab;
+    // D2H into page-locked staging owned by this thread (grow-only), then the
+    // reference's SampledBatch layout built batch-parallel on host threads
+    Staging& st = staging();
+    auto* bvoff = st.get<int32_t>(0, static_cast<std::size_t>(k + 1));
+    auto* beoff = st.get<int32_t>(1, static_cast<std::size_t>(k + 1));
+    auto* comp = st.get<int32_t>(2, R + static_cast<std::size_t>(k));
+    auto* l2g = st.get<int32_t>(3, static_cast<std::size_t>(V));
+    auto* rl = st.get<int32_t>(4, R);
+    auto* er = st.get<int32_t>(5, static_cast<std::size_t>(E));
+    auto* ec = st.get<int32_t>(6, static_cast<std::size_t>(E));
+    auto* eg = st.get<int32_t>(7, static_cast<std::size_t>(E));
+    auto* draws_p = st.get<std::uint32_t>(8, R);
+    auto* decs_p = st.get<std::uint32_t>(9, R);
+    double *xv = nullptr, *ye = nullptr;
+    std::uint8_t* lab = nullptr;
     hgs_host_out o{};
-    o.batch_voff = bvoff.data(); o.batch_eoff = beoff.data(); o.comp_off = comp.data();
-    o.l2g = l2g.data(); o.roots_local = rl.data(); o.e_row = er.data(); o.e_col = ec.data();
-    o.e_gid = eg.data(); o.draws = draws.data(); o.decisions = decisions.data();
+    o.batch_voff = bvoff; o.batch_eoff = beoff; o.comp_off = comp;
+    o.l2g = l2g; o.roots_local = rl; o.e_row = er; o.e_col = ec;
+    o.e_gid = eg; o.draws = draws_p; o.decisions = decs_p;
     if (gather) {
-        xv.resize(static_cast<std::size_t>(V * f_v));
-        ye.resize(static_cast<std::size_t>(E * f_e));
-        lab.resize(static_cast<std::size_t>(E));
-        o.xv = xv.data(); o.ye = ye.data(); o.lab = lab.data();
+        xv = st.get<double>(10, static_cast<std::size_t>(V * f_v));
+        ye = st.get<double>(11, static_cast<std::size_t>(E * f_e));
+        lab = st.get<std::uint8_t>(12, static_cast<std::size_t>(E));
+        o.xv = xv; o.ye = ye; o.lab = lab;
     }
     check(hgs_sample_copy_to_host(s, &o));
+    const std::vector<std::uint32_t> draws(draws_p, draws_p + R), decisions(decs_p, decs_p + R);
     if (per_root) per_root->advance(draws);
     else philox->advance(decisions);
     if (observer) emit_frontiers(g, s, *a_host, roots, cfg, *observer);
 
     std::vector<SampledBatch> out(static_cast<std::size_t>(k));
-    for (Index b = 0; b < k; ++b) {
+    auto build = [&](Index b) {
         SampledBatch& sb = out[b];
         const Index v0 = bvoff[b], v1 = bvoff[b + 1], e0 = beoff[b], e1 = beoff[b + 1];
         const Index r0 = boff[b], r1 = boff[b + 1];
@@ -210,16 +476,17 @@ std::vector<SampledBatch> run_bulk(hgs_graph* g, hgs_sample* s,
             if (!gather) val = values ? (*values)[eg[e]] : static_cast<double>(eg[e]) + 1.0;
             sb.adjacency.entries[e - e0] = {er[e], ec[e], val};
         }
-        sb.component_offsets.assign(comp.begin() + (r0 + b), comp.begin() + (r1 + b + 1));
-        sb.local_to_global.assign(l2g.begin() + v0, l2g.begin() + v1);
-        sb.roots_local.assign(rl.begin() + r0, rl.begin() + r1);
+        sb.component_offsets.assign(comp + (r0 + b), comp + (r1 + b + 1));
+        sb.local_to_global.assign(l2g + v0, l2g + v1);
+        sb.roots_local.assign(rl + r0, rl + r1);
         if (gather) {
-            sb.node_features = DenseMatrix(v1 - v0, f_v, std::vector<double>(xv.begin() + v0 * f_v, xv.begin() + v1 * f_v));
-            sb.edge_features = DenseMatrix(e1 - e0, f_e, std::vector<double>(ye.begin() + e0 * f_e, ye.begin() + e1 * f_e));
-            sb.edge_labels.assign(lab.begin() + e0, lab.begin() + e1);
-            sb.edge_global_ids.assign(eg.begin() + e0, eg.begin() + e1);
+            sb.node_features = DenseMatrix(v1 - v0, f_v, std::vector<double>(xv + v0 * f_v, xv + v1 * f_v));
+            sb.edge_features = DenseMatrix(e1 - e0, f_e, std::vector<double>(ye + e0 * f_e, ye + e1 * f_e));
+            sb.edge_labels.assign(lab + e0, lab + e1);
+            sb.edge_global_ids.assign(eg + e0, eg + e1);
         }
-    }
+    };
+    parallel_for(k, build);
     return out;
 }
 
@@ -229,12 +496,10 @@ std::vector<SampledBatch> bulk_shadow(const CsrMatrix& a, const std::vector<std:
                                       const SamplerConfig& cfg, ChoiceSource& choice,
                                       const FrontierObserver& observer) {
     cfg.validate();
-    const bool ids = values_are_ids(a);
-    GraphGuard g;
-    g.g = upload_csr(a, 0, !ids);
-    SampleGuard s;
-    check(hgs_sample_create(g.g, nullptr, &s.s));
-    return run_bulk(g.g, s.s, batches, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, false,
+    Lease l;
+    lease_csr(l, a);
+    const bool ids = l.owned ? l.owned->ids : l.entry->ids;
+    return run_bulk(l.graph(), l.s, batches, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, false,
                     observer ? &observer : nullptr, &a);
 }
 
@@ -244,12 +509,10 @@ SampledBatch shadow_reference(const CsrMatrix& a, std::span<const Index> roots,
     // the raw rows of A when unsymmetrized (sampler.cpp:104-106).
     cfg.validate();
     std::vector<std::vector<Index>> one{std::vector<Index>(roots.begin(), roots.end())};
-    const bool ids = values_are_ids(a);
-    GraphGuard g;
-    g.g = upload_csr(a, 0, !ids);
-    SampleGuard s;
-    check(hgs_sample_create(g.g, nullptr, &s.s));
-    return std::move(run_bulk(g.g, s.s, one, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, true).front());
+    Lease l;
+    lease_csr(l, a);
+    const bool ids = l.owned ? l.owned->ids : l.entry->ids;
+    return std::move(run_bulk(l.graph(), l.s, one, cfg, choice, false, ids ? nullptr : &a.values, 0, 0, true).front());
 }
 
 std::vector<std::vector<Index>> sample_rows(const CsrMatrix& p, Index s, ChoiceSource& choice,
@@ -334,17 +597,13 @@ void gather_features(SampledBatch& batch, const EventGraph& event) {
                          "sample from make_edge_id_matrix(event)");
         ids[i] = id;
     }
-    const CsrMatrix a = make_edge_id_matrix(event);
-    GraphGuard g;
-    g.g = upload_csr(a, 0, false);
-    check(hgs_graph_attach_features(g.g, event.node_features.data.data(), event.node_features.cols,
-                                    event.edge_features.data.data(), event.edge_features.cols,
-                                    event.labels.data()));
+    Lease l;
+    lease_event(l, event);  // the event's features stay resident across calls
     const Index V = static_cast<Index>(batch.local_to_global.size());
     batch.node_features = DenseMatrix(V, event.node_features.cols);
     batch.edge_features = DenseMatrix(m, event.edge_features.cols);
     batch.edge_labels.resize(static_cast<std::size_t>(m));
-    check(hgs_graph_gather(g.g, batch.local_to_global.data(), V, ids.data(), m,
+    check(hgs_graph_gather(l.graph(), batch.local_to_global.data(), V, ids.data(), m,
                            batch.node_features.data.data(), batch.edge_features.data.data(),
                            batch.edge_labels.data()));
     batch.edge_global_ids = std::move(ids);
@@ -384,6 +643,21 @@ CsrMatrix symmetrize_pattern(const CsrMatrix& a) {
 // ---- resident events ---------------------------------------------------------------
 
 namespace gpu {
+
+void release_cached() {
+    Cache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    // entries borrowed by running calls stay until their next release
+    c.entries.erase(std::remove_if(c.entries.begin(), c.entries.end(),
+                                   [](const std::unique_ptr<CacheEntry>& e) { return e->in_use == 0; }),
+                    c.entries.end());
+}
+
+std::size_t cached_entries() {
+    Cache& c = cache();
+    std::lock_guard<std::mutex> lk(c.mu);
+    return c.entries.size();
+}
 
 DeviceEvent::DeviceEvent(const EventGraph& event, int device) : device_(device) {
     const CsrMatrix a = make_edge_id_matrix(event);

@@ -1,5 +1,7 @@
 // tools.cpp — extern "C" wrappers (include/hgs_tools.h) for Python harnesses.
 #include <algorithm>
+#include <chrono>
+#include <memory>
 #include <string>
 
 #include "hgs_tools.h"
@@ -23,6 +25,68 @@ thread_local std::string g_tools_err;
 extern "C" {
 
 const char* hgs_tools_last_error(void) { return g_tools_err.c_str(); }
+
+// End-to-end timing of the C++ drop-in: host arrays in, the reference's
+// std::vector<SampledBatch> (with gathered features) out, wall clock per rep.
+//   mode 0: gpu::DeviceEvent::bulk_shadow(batches, cfg, source, gather = true)
+//   mode 1: the reference trainer's unmodified two lines (trainer.cpp:457-458):
+//           bulk_shadow(make_edge_id_matrix(event), chunk, cfg, source) and
+//           gather_features(batch, event) per batch, served by the
+//           resident-graph cache
+// Each rep builds a fresh PerRootChoiceSource from the seeds, as the trainer
+// does (trainer.cpp:453). ve[0..1] = V, E of the last rep.
+int hgs_dropin_time(int64_t n, const int64_t* rp, const int64_t* ci, const double* nf, int64_t f_v,
+                    const double* ef, int64_t f_e, const uint8_t* lab, const int64_t* roots,
+                    const int64_t* boff, int64_t k, const uint64_t* seeds, int64_t depth, int64_t fanout,
+                    int32_t mode, int32_t warmup, int32_t reps, double* seconds, int64_t* ve) {
+    try {
+        hitgnn::EventGraph ev;
+        ev.n = n;
+        ev.edges = hitgnn::CooMatrix(n, n);
+        const int64_t m = rp[n];
+        ev.edges.entries.resize(static_cast<size_t>(m));
+        for (int64_t u = 0; u < n; ++u)
+            for (int64_t t = rp[u]; t < rp[u + 1]; ++t) ev.edges.entries[t] = {u, ci[t], 1.0};
+        ev.node_features = hitgnn::DenseMatrix(n, f_v, std::vector<double>(nf, nf + n * f_v));
+        ev.edge_features = hitgnn::DenseMatrix(m, f_e, std::vector<double>(ef, ef + m * f_e));
+        ev.labels.assign(lab, lab + m);
+        const hitgnn::CsrMatrix a = hitgnn::make_edge_id_matrix(ev);
+        std::vector<std::vector<hitgnn::Index>> batches(static_cast<size_t>(k));
+        for (int64_t b = 0; b < k; ++b) batches[b].assign(roots + boff[b], roots + boff[b + 1]);
+        const std::vector<uint64_t> sv(seeds, seeds + boff[k]);
+        hitgnn::SamplerConfig cfg;
+        cfg.depth = depth;
+        cfg.fanout = fanout;
+        cfg.batch_size = k > 0 ? boff[1] - boff[0] : 1;
+        cfg.bulk_batches = std::max<int64_t>(k, 1);
+        std::unique_ptr<hitgnn::gpu::DeviceEvent> dev;
+        if (mode == 0) dev = std::make_unique<hitgnn::gpu::DeviceEvent>(ev);
+        for (int32_t i = 0; i < warmup + reps; ++i) {
+            const auto t0 = std::chrono::steady_clock::now();
+            hitgnn::PerRootChoiceSource src(sv);
+            std::vector<hitgnn::SampledBatch> out;
+            if (mode == 0) {
+                out = dev->bulk_shadow(batches, cfg, src, true);
+            } else {
+                out = hitgnn::bulk_shadow(a, batches, cfg, src);
+                for (auto& sb : out) hitgnn::gather_features(sb, ev);
+            }
+            const auto t1 = std::chrono::steady_clock::now();
+            if (i >= warmup) seconds[i - warmup] = std::chrono::duration<double>(t1 - t0).count();
+            int64_t V = 0, E = 0;
+            for (const auto& sb : out) {
+                V += sb.n_vertices();
+                E += sb.n_edges();
+            }
+            ve[0] = V;
+            ve[1] = E;
+        }
+        return 0;
+    } catch (const std::exception& e) {
+        g_tools_err = e.what();
+        return 1;
+    }
+}
 
 int hgs_generate_event(int64_t n_tracks, int64_t hits_min, int64_t hits_max, int64_t layers,
                        int64_t noise_hits, double false_edge_factor, int64_t f_v, int64_t f_e,

@@ -125,6 +125,11 @@ struct DevGraph {
     // guards the lazily built parts (walk_sym, recip): sample handles on
     // different host threads may share one graph
     std::recursive_mutex lazy_mu;
+    // hgs_graph_gather scratch (grow-only), guarded by gather_mu
+    std::mutex gather_mu;
+    DevBuf<int64_t> g_l2g, g_eid;
+    DevBuf<double> g_xv, g_ye;
+    DevBuf<uint8_t> g_lab;
 
     const DevCsr& full_pattern() const { return has_full ? a_full : a; }
 };

@@ -64,6 +64,8 @@ def tools() -> C.CDLL:
         L.hgs_tools_frontier_array.restype = C.c_int64
         L.hgs_tools_frontier_array.argtypes = [vp, C.c_int64, C.c_int32, vp]
         L.hgs_tools_frontiers_free.argtypes = [vp]
+        L.hgs_dropin_time.argtypes = [C.c_int64, vp, vp, vp, C.c_int64, vp, C.c_int64, vp, vp, vp, C.c_int64, vp,
+                                      C.c_int64, C.c_int64, C.c_int32, C.c_int32, C.c_int32, vp, vp]
         _tools = L
     return _tools
 
@@ -244,3 +246,26 @@ def bench_roots(n: int, b: int, k: int, seed: int = 1, rep: int = 0):
     boff = np.arange(k + 1, dtype=np.int64) * b
     seeds = derive_grid(seed, [0x7374726D, k, rep], k, b)
     return roots, boff, seeds
+
+
+def dropin_time(ev: Event, roots, batch_off, seeds, *, depth=3, fanout=6, mode=0, warmup=1, reps=3):
+    """Wall-clock seconds per call of the C++ drop-in end to end (host arrays
+    in, std::vector<SampledBatch> with gathered features out): mode 0 =
+    gpu::DeviceEvent::bulk_shadow(gather), mode 1 = the reference trainer's two
+    lines (bulk_shadow + gather_features per batch). Returns (seconds, V, E)."""
+    L = tools()
+    r = np.ascontiguousarray(roots, np.int64)
+    b = np.ascontiguousarray(batch_off, np.int64)
+    sd = np.ascontiguousarray(seeds, np.uint64)
+    nf = np.ascontiguousarray(ev.node_feat, np.float64)
+    ef = np.ascontiguousarray(ev.edge_feat, np.float64)
+    lab = np.ascontiguousarray(ev.labels, np.uint8)
+    rp = np.ascontiguousarray(ev.rp, np.int64)
+    ci = np.ascontiguousarray(ev.ci, np.int64)
+    sec = np.zeros(reps, np.float64)
+    ve = np.zeros(2, np.int64)
+    if L.hgs_dropin_time(ev.n, rp.ctypes.data, ci.ctypes.data, nf.ctypes.data, nf.shape[1], ef.ctypes.data,
+                         ef.shape[1], lab.ctypes.data, r.ctypes.data, b.ctypes.data, len(b) - 1, sd.ctypes.data,
+                         depth, fanout, mode, warmup, reps, sec.ctypes.data, ve.ctypes.data) != 0:
+        raise ValueError(L.hgs_tools_last_error().decode())
+    return sec, int(ve[0]), int(ve[1])

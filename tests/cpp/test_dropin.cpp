@@ -144,6 +144,40 @@ int main() {
         for (auto& sb : out) gather_features(sb, event);
         compare(out, oracle(adj, &event, batches, seeds, nullptr, 0, cfg), true, "bulk_shadow+gather_features");
     }
+    {   // resident-graph cache: the trainer's repeated calls reuse one upload;
+        // an in-place change of A's content is detected (new entry, new results)
+        gpu::release_cached();
+        for (int rep = 0; rep < 3; ++rep) {
+            PerRootChoiceSource src(seeds);
+            auto out = bulk_shadow(adj, batches, cfg, src);
+            for (auto& sb : out) gather_features(sb, event);
+            compare(out, oracle(adj, &event, batches, seeds, nullptr, 0, cfg), true, "cached trainer path");
+        }
+        CHECK(gpu::cached_entries() == 2);  // A and the event
+        CsrMatrix adj2 = adj;
+        {
+            PerRootChoiceSource src(seeds);
+            auto out = bulk_shadow(adj2, batches, cfg, src);
+            compare(out, oracle(adj2, nullptr, batches, seeds, nullptr, 0, cfg), false, "cache: copy of A");
+        }
+        // drop one edge of row 0 in place (same arrays, same sizes are not
+        // possible: rebuild row 0 with its last column replaced)
+        const Index r0b = adj2.row_ptr[0], r0e = adj2.row_ptr[1];
+        if (r0e > r0b) {
+            std::vector<bool> used(static_cast<std::size_t>(adj2.n_cols), false);
+            for (Index t = r0b; t < r0e; ++t) used[adj2.col_idx[t]] = true;
+            Index c = adj2.n_cols - 1;
+            while (c >= 0 && used[c]) --c;
+            if (c > adj2.col_idx[r0e - 1]) {
+                adj2.col_idx[r0e - 1] = c;  // still sorted and unique
+                PerRootChoiceSource src(seeds);
+                auto out = bulk_shadow(adj2, batches, cfg, src);
+                compare(out, oracle(adj2, nullptr, batches, seeds, nullptr, 0, cfg), false, "cache: A changed in place");
+            }
+        }
+        gpu::release_cached();
+        CHECK(gpu::cached_entries() == 0);
+    }
     {   // resident event, fused gather, reused (non-fresh) source on a second call
         gpu::DeviceEvent dev(event);
         PerRootChoiceSource src(seeds);
