@@ -220,6 +220,30 @@ def run_reference(args, world, rank):
 # the GPU arm
 
 
+def measure_ingest(ev, device) -> dict:
+    """Event ingest (§8f #2): the event as a binary file (hgs_event_save),
+    then hgs_graph_load (mmap, device-side narrowing / validation, features
+    attached) + the walk build (K0), wall clock, page cache warm; the median
+    of 3 loads."""
+    import torch
+    from paper_2504_04670_b200 import hgs
+    path = os.path.join(tempfile.mkdtemp(prefix="hgs_ingest_"), "event.hgsev")
+    hgs.save_event(path, ev.rp, ev.ci, node_feat=ev.node_feat, edge_feat=ev.edge_feat, labels=ev.labels)
+    ts = []
+    for _ in range(3):
+        torch.cuda.synchronize()
+        t0 = time.perf_counter()
+        G = hgs.Graph.load(path, device=device)
+        G.info()  # builds the symmetrized walk (K0)
+        torch.cuda.synchronize()
+        ts.append(time.perf_counter() - t0)
+        G.close()
+    size = os.path.getsize(path)
+    os.remove(path)
+    return {"ms_per_event": 1e3 * float(np.median(ts)), "file_bytes": size,
+            "path": "hgs_event_save file -> hgs_graph_load (mmap, device narrowing/validation, features) + K0 walk"}
+
+
 def distinct_devices(world, dev) -> int:
     """Number of distinct physical GPUs the ranks run on (device UUIDs). A
     multi-rank line is only printed when every rank has its own GPU; the
@@ -267,6 +291,7 @@ def run_gpu(args, world, rank, local_rank):
     log(f"[rank {rank}] event n={ev.n} m={ev.m} generated in {time.time() - t0:.1f}s")
     G = hgs.Graph(ev.rp, ev.ci, device=local_rank).attach_features(ev.node_feat, ev.edge_feat,
                                                                     ev.labels)
+    ingest = measure_ingest(ev, local_rank) if rank == 0 else None
     stream = torch.cuda.Stream(dev)  # a real (non-default) stream shared with the C ABI
     S = hgs.Sampler(G, stream=stream.cuda_stream)
     cfg = dict(depth=DEPTH, fanout=FANOUT, symmetrize=True, rng=RNG, gather=True,
@@ -451,6 +476,8 @@ def run_gpu(args, world, rank, local_rank):
         line["ranks"] = world
     if e2e_cpp:
         line["e2e_cpp"] = e2e_cpp
+    if ingest:
+        line["ingest"] = ingest
     if world == 1 and not args.no_cpu_baseline:
         # (i) all host threads on the call's own shape (K_BATCHES minibatches,
         # contiguous batch ranges per thread); (ii) one thread, the reference as
@@ -489,9 +516,16 @@ def run_epoch(args, world, rank, local_rank):
     t0 = time.time()
     with cf.ThreadPoolExecutor(max_workers=os.cpu_count() or 4) as ex:
         evs = list(ex.map(lambda e: W.generate_event(**W.GEN["C2"], event_id=e), mine))
-    log(f"[rank {rank}] {len(evs)} events generated in {time.time() - t0:.1f}s")
+    gen_s = time.time() - t0
+    log(f"[rank {rank}] {len(evs)} events generated in {gen_s:.1f}s")
+    torch.cuda.synchronize()
+    t0 = time.time()
     graphs = [hgs.Graph(e.rp, e.ci, device=local_rank).attach_features(e.node_feat, e.edge_feat, e.labels)
               for e in evs]
+    for g in graphs:
+        g.info()  # walk build (K0) per event
+    torch.cuda.synchronize()
+    ingest_s = time.time() - t0
     n_v = sum(e.n for e in evs)
     del evs
     es = EP.EpochSampler(graphs, batch_size=BATCH, bulk_batches=args.bulk_batches, depth=DEPTH, fanout=FANOUT,
@@ -537,6 +571,7 @@ def run_epoch(args, world, rank, local_rank):
                                    f" {DEPTH}-hop, fanout {FANOUT}, with gather",
                        "events": args.events, "events_per_gpu": len(graphs), "vertices_per_gpu": n_v,
                        "minibatches_per_epoch": mbs // args.steps, "parallelism": f"events split over {world} GPU(s)",
+                       "setup_s": {"generate": round(gen_s, 2), "ingest_and_walk_build": round(ingest_s, 2)},
                        "l2": "not flushed (the epoch streams ~100 events, far beyond L2)"},
             "edges_per_s": world * sum(t["E"] for t in tots) / (total_ms / 1e3),
             "calls_per_epoch": tots[0]["calls"], "gpu_launches": None, "clocks": clk.summary(),

@@ -144,6 +144,18 @@ int hgs_graph_info(hgs_graph* g, int64_t* info);
  * row_ptr[n+1], col_idx[walk nnz]. */
 int hgs_graph_walk(hgs_graph* g, int32_t symmetrize, int64_t* row_ptr, int64_t* col_idx);
 int hgs_graph_destroy(hgs_graph* g);
+/* Binary event files (the ingest path; the reference's
+ * JSON read_event/write_event, data.cpp:270-368, are its slow twins): a
+ * 64-byte-aligned header + sections row_ptr (int64, n+1), col_idx (int64,
+ * nnz), values (f64, nnz; optional), node_feat (f64, n*f_v), edge_feat
+ * (f64, nnz*f_e), labels (u8, nnz). hgs_graph_load mmaps the file and builds
+ * the graph handle (device-side narrowing / validation for edge-id files)
+ * with the features attached. info: n_rows, n_cols, nnz, f_v, f_e, flags. */
+int hgs_event_save(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                   const double* values, const double* node_feat, int64_t f_v, const double* edge_feat, int64_t f_e,
+                   const uint8_t* labels);
+int hgs_event_info(const char* path, int64_t* info);
+int hgs_graph_load(int device, const char* path, hgs_graph** out);
 /* gather_features for an arbitrary batch (sampler.cpp:211-243): node rows of
  * l2g[V] and edge rows / labels of edge ids eid[E] (input CSR positions) into
  * host xv[V*f_v], ye[E*f_e], lab[E]. Ids are range-checked (HGS_EINVAL). */

@@ -5,7 +5,13 @@
 // arithmetic runs in the kernels of sampler.cu / graph.cu.
 #include <cuda_runtime.h>
 
+#include <fcntl.h>
+#include <sys/mman.h>
+#include <sys/stat.h>
+#include <unistd.h>
+
 #include <algorithm>
+#include <cstdio>
 #include <cstdlib>
 #include <cstring>
 #include <string>
@@ -134,6 +140,27 @@ int hgs_graph_create(int device, int64_t n_rows, int64_t n_cols, const int64_t* 
         if (nnz >= ((int64_t)1 << 31) - 1) fail(HGS_ERANGE, "hgs_graph_create: more than 2^31-2 entries");
         if (nnz > 0 && !col_idx) fail(HGS_EINVAL, "hgs_graph_create: null col_idx");
         const int32_t n = (int32_t)n_rows;
+        bool rp_ok = true;  // O(n) on the host; an invalid row_ptr takes the host loop below,
+        for (int32_t u = 0; u < n && rp_ok; ++u) rp_ok = row_ptr[u + 1] >= row_ptr[u];  // which orders errors
+        if (!values && rp_ok) {  // edge-id matrix: narrowing and column checks run on the device
+            auto* h = new hgs_graph;
+            DevGraph& g = h->g;
+            try {
+                g.device = device;
+                HGS_CUDA(cudaSetDevice(device));
+                HGS_CUDA(cudaStreamCreateWithFlags(&g.stream, cudaStreamNonBlocking));
+                g.n_rows = n_rows;
+                g.n_cols = n_cols;
+                g.nnz = nnz;
+                graph_ingest_device(g, row_ptr, col_idx, g.stream);
+            } catch (...) {
+                if (g.stream) cudaStreamDestroy(g.stream);
+                delete h;
+                throw;
+            }
+            *out = h;
+            return;
+        }
         std::vector<int32_t> rp(n + 1), ci, gid, frp, fci;
         ci.reserve(nnz);
         bool zeros = false, neg = false;
@@ -220,6 +247,139 @@ int hgs_graph_attach_features(hgs_graph* h, const double* node_feat, int64_t f_v
         HGS_CUDA(cudaStreamSynchronize(g.stream));
         g.has_features = true;
     });
+}
+
+// ---- binary event files (hgs_event_save / hgs_graph_load) ------------------
+
+namespace {
+
+constexpr char kEventMagic[8] = {'H', 'G', 'S', 'E', 'V', 'T', '0', '1'};
+struct EventHeader {
+    char magic[8];
+    int64_t n_rows, n_cols, nnz, f_v, f_e, flags;  // flags: 1 = values present
+    int64_t off[6];  // row_ptr, col_idx, values, node_feat, edge_feat, labels (bytes from file start)
+    int64_t bytes[6];
+    int64_t file_bytes;
+};
+constexpr int64_t kAlign = 64;
+int64_t align_up(int64_t x) { return (x + kAlign - 1) / kAlign * kAlign; }
+
+struct Mapping {
+    void* p = MAP_FAILED;
+    size_t len = 0;
+    int fd = -1;
+    ~Mapping() {
+        if (p != MAP_FAILED) munmap(p, len);
+        if (fd >= 0) close(fd);
+    }
+};
+
+const EventHeader& map_event(Mapping& m, const char* path) {
+    if (!path) fail(HGS_EINVAL, "hgs_graph_load: null path");
+    m.fd = open(path, O_RDONLY);
+    if (m.fd < 0) fail(HGS_EINVAL, std::string("hgs_graph_load: cannot open ") + path);
+    struct stat sb {};
+    if (fstat(m.fd, &sb) != 0 || sb.st_size < (off_t)sizeof(EventHeader))
+        fail(HGS_EINVAL, std::string("hgs_graph_load: not an event file: ") + path);
+    m.len = (size_t)sb.st_size;
+    m.p = mmap(nullptr, m.len, PROT_READ, MAP_PRIVATE | MAP_POPULATE, m.fd, 0);
+    if (m.p == MAP_FAILED) fail(HGS_ECUDA, std::string("hgs_graph_load: mmap failed: ") + path);
+    const auto& h = *static_cast<const EventHeader*>(m.p);
+    if (std::memcmp(h.magic, kEventMagic, 8) != 0) fail(HGS_EINVAL, std::string("hgs_graph_load: bad magic: ") + path);
+    if (h.file_bytes != (int64_t)m.len || h.n_rows < 0 || h.n_cols < 0 || h.nnz < 0 || h.f_v < 0 || h.f_e < 0)
+        fail(HGS_EINVAL, std::string("hgs_graph_load: truncated or corrupt event file: ") + path);
+    const int64_t want[6] = {8 * (h.n_rows + 1), 8 * h.nnz, (h.flags & 1) ? 8 * h.nnz : 0, 8 * h.n_rows * h.f_v,
+                             8 * h.nnz * h.f_e, h.nnz};
+    for (int i = 0; i < 6; ++i)
+        if (h.bytes[i] != want[i] || h.off[i] < (int64_t)sizeof(EventHeader) || h.off[i] + h.bytes[i] > h.file_bytes)
+            fail(HGS_EINVAL, std::string("hgs_graph_load: truncated or corrupt event file: ") + path);
+    return h;
+}
+
+}  // namespace
+
+int hgs_event_save(const char* path, int64_t n_rows, int64_t n_cols, const int64_t* row_ptr, const int64_t* col_idx,
+                   const double* values, const double* node_feat, int64_t f_v, const double* edge_feat, int64_t f_e,
+                   const uint8_t* labels) {
+    return guarded([&] {
+        if (!path || !row_ptr || n_rows < 0 || f_v < 0 || f_e < 0) fail(HGS_EINVAL, "hgs_event_save: bad arguments");
+        EventHeader h{};
+        std::memcpy(h.magic, kEventMagic, 8);
+        h.n_rows = n_rows;
+        h.n_cols = n_cols;
+        h.nnz = row_ptr[n_rows];
+        h.f_v = node_feat ? f_v : 0;
+        h.f_e = edge_feat ? f_e : 0;
+        h.flags = values ? 1 : 0;
+        const void* src[6] = {row_ptr, col_idx, values, node_feat, edge_feat, labels};
+        const int64_t bytes[6] = {8 * (n_rows + 1), 8 * h.nnz, values ? 8 * h.nnz : 0, 8 * n_rows * h.f_v,
+                                  8 * h.nnz * h.f_e, labels ? h.nnz : 0};
+        int64_t pos = align_up((int64_t)sizeof(EventHeader));
+        for (int i = 0; i < 6; ++i) {
+            h.off[i] = pos;
+            h.bytes[i] = bytes[i];
+            pos = align_up(pos + bytes[i]);
+        }
+        h.file_bytes = pos;
+        const std::string tmp = std::string(path) + ".tmp";
+        FILE* f = std::fopen(tmp.c_str(), "wb");
+        if (!f) fail(HGS_EINVAL, std::string("hgs_event_save: cannot write ") + path);
+        bool ok = std::fwrite(&h, sizeof h, 1, f) == 1;
+        static const char zeros[kAlign] = {};
+        int64_t at = (int64_t)sizeof h;
+        for (int i = 0; i < 6 && ok; ++i) {
+            ok = ok && std::fwrite(zeros, 1, (size_t)(h.off[i] - at), f) == (size_t)(h.off[i] - at);
+            if (bytes[i]) ok = ok && std::fwrite(src[i], 1, (size_t)bytes[i], f) == (size_t)bytes[i];
+            at = h.off[i] + bytes[i];
+        }
+        ok = ok && std::fwrite(zeros, 1, (size_t)(h.file_bytes - at), f) == (size_t)(h.file_bytes - at);
+        ok = (std::fclose(f) == 0) && ok;
+        if (!ok || std::rename(tmp.c_str(), path) != 0) {
+            std::remove(tmp.c_str());
+            fail(HGS_EINVAL, std::string("hgs_event_save: write failed: ") + path);
+        }
+    });
+}
+
+int hgs_event_info(const char* path, int64_t* info) {
+    return guarded([&] {
+        if (!info) fail(HGS_EINVAL, "hgs_event_info: null argument");
+        Mapping m;
+        const EventHeader& h = map_event(m, path);
+        info[0] = h.n_rows; info[1] = h.n_cols; info[2] = h.nnz; info[3] = h.f_v; info[4] = h.f_e; info[5] = h.flags;
+    });
+}
+
+int hgs_graph_load(int device, const char* path, hgs_graph** out) {
+    if (!out) {
+        g_err = "hgs_graph_load: null out";
+        return HGS_EINVAL;
+    }
+    *out = nullptr;
+    Mapping m;
+    const EventHeader* hp = nullptr;
+    const int rc0 = guarded([&] { hp = &map_event(m, path); });
+    if (rc0 != HGS_OK) return rc0;
+    const EventHeader& h = *hp;
+    const auto* base = static_cast<const char*>(m.p);
+    auto at = [&](int i) { return h.bytes[i] ? base + h.off[i] : nullptr; };
+    hgs_graph* g = nullptr;
+    int rc = hgs_graph_create(device, h.n_rows, h.n_cols, reinterpret_cast<const int64_t*>(at(0)),
+                              reinterpret_cast<const int64_t*>(at(1)), reinterpret_cast<const double*>(at(2)), &g);
+    if (rc != HGS_OK) return rc;
+    if (h.bytes[5] || h.f_v || h.f_e) {
+        rc = hgs_graph_attach_features(g, reinterpret_cast<const double*>(at(3)), h.f_v,
+                                       reinterpret_cast<const double*>(at(4)), h.f_e,
+                                       reinterpret_cast<const uint8_t*>(at(5)));
+        if (rc != HGS_OK) {
+            const std::string keep = g_err;
+            hgs_graph_destroy(g);
+            g_err = keep;
+            return rc;
+        }
+    }
+    *out = g;
+    return HGS_OK;
 }
 
 int hgs_graph_info(hgs_graph* h, int64_t* info) {

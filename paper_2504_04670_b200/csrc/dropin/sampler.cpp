@@ -589,7 +589,12 @@ void gather_features(SampledBatch& batch, const EventGraph& event) {
     for (Index v : batch.local_to_global)
         if (v < 0 || v >= event.n) fail_invalid("gather_features: batch vertex out of range for event");
     const Index m = batch.adjacency.nnz();
-    std::vector<Index> ids(static_cast<std::size_t>(m));
+    const Index V = static_cast<Index>(batch.local_to_global.size());
+    const Index fv = event.node_features.cols, fe = event.edge_features.cols;
+    // ids and outputs through this thread's page-locked staging (slots 0-4)
+    Staging& st = staging();
+    auto* l2g = st.get<int64_t>(0, static_cast<std::size_t>(V));
+    auto* ids = st.get<int64_t>(1, static_cast<std::size_t>(m));
     for (Index i = 0; i < m; ++i) {
         const Index id = static_cast<Index>(std::llround(batch.adjacency.entries[i].value)) - 1;
         if (id < 0 || id >= event.m())
@@ -597,16 +602,17 @@ void gather_features(SampledBatch& batch, const EventGraph& event) {
                          "sample from make_edge_id_matrix(event)");
         ids[i] = id;
     }
+    std::memcpy(l2g, batch.local_to_global.data(), sizeof(int64_t) * static_cast<std::size_t>(V));
+    auto* xv = st.get<double>(2, static_cast<std::size_t>(V * fv));
+    auto* ye = st.get<double>(3, static_cast<std::size_t>(m * fe));
+    auto* lab = st.get<std::uint8_t>(4, static_cast<std::size_t>(m));
     Lease l;
     lease_event(l, event);  // the event's features stay resident across calls
-    const Index V = static_cast<Index>(batch.local_to_global.size());
-    batch.node_features = DenseMatrix(V, event.node_features.cols);
-    batch.edge_features = DenseMatrix(m, event.edge_features.cols);
-    batch.edge_labels.resize(static_cast<std::size_t>(m));
-    check(hgs_graph_gather(l.graph(), batch.local_to_global.data(), V, ids.data(), m,
-                           batch.node_features.data.data(), batch.edge_features.data.data(),
-                           batch.edge_labels.data()));
-    batch.edge_global_ids = std::move(ids);
+    check(hgs_graph_gather(l.graph(), l2g, V, ids, m, xv, ye, lab));
+    batch.node_features = DenseMatrix(V, fv, std::vector<double>(xv, xv + V * fv));
+    batch.edge_features = DenseMatrix(m, fe, std::vector<double>(ye, ye + m * fe));
+    batch.edge_labels.assign(lab, lab + m);
+    batch.edge_global_ids.assign(ids, ids + m);
     for (auto& e : batch.adjacency.entries) e.value = 1.0;
 }
 

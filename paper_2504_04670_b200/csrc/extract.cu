@@ -80,7 +80,7 @@ struct HashSet<true> {
             b = next(b);
         }
     }
-    __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)] = (v << rb) | r; }
+    __device__ __forceinline__ void set_slot_rank(int sl, uint32_t v, uint32_t r) const { slot[sl] = (v << rb) | r; }
     __device__ __forceinline__ static uint32_t bmin(const uint4& q, uint32_t hi) {
         return min(min(q.x ^ hi, q.y ^ hi), min(q.z ^ hi, q.w ^ hi));
     }
@@ -144,7 +144,7 @@ struct HashSet<false> {
             b = next(b);
         }
     }
-    __device__ __forceinline__ void set_rank(uint32_t v, uint32_t r) const { slot[find_slot(v)].y = r; }
+    __device__ __forceinline__ void set_slot_rank(int sl, uint32_t, uint32_t r) const { slot[sl].y = r; }
     __device__ __forceinline__ int find_rank(uint32_t v) const {
         uint32_t b = bucket(v);
         for (;;) {
@@ -278,18 +278,27 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             tmp[atomicAdd(&cnt[cidx((v - lo) >> shift)], 1)] = (int32_t)v;
         }
         __syncwarp();
-        // ---- rank = bucket start + smaller keys of the same bucket
-        for (int i = lane; i < U; i += 32) {
-            const uint32_t v = (uint32_t)tmp[i];
-            const uint32_t b = (v - lo) >> shift;
-            const int e = cnt[cidx(b)];
-            const int s = b ? cnt[cidx(b - 1)] : 0;
-            int rank = s;
-            for (int j = s; j < e; ++j) rank += (uint32_t)tmp[j] < v;
-            keys[rank] = (int32_t)v;
-            hs.set_rank(v, (uint32_t)rank);
+        // ---- rank = bucket start + smaller keys of the same bucket; the
+        // rank goes into the key's hash slot, found before any lane of the
+        // chunk rewrites a slot (no lane reads a slot another lane writes)
+        for (int i0 = 0; i0 < U; i0 += 32) {
+            const int i = i0 + lane;
+            int rank = 0, sl = -1;
+            uint32_t v = 0;
+            if (i < U) {
+                v = (uint32_t)tmp[i];
+                const uint32_t b = (v - lo) >> shift;
+                const int e = cnt[cidx(b)];
+                const int s = b ? cnt[cidx(b - 1)] : 0;
+                rank = s;
+                for (int j = s; j < e; ++j) rank += (uint32_t)tmp[j] < v;
+                keys[rank] = (int32_t)v;
+                sl = hs.find_slot(v);
+            }
+            __syncwarp();
+            if (sl >= 0) hs.set_slot_rank(sl, v, (uint32_t)rank);
+            __syncwarp();
         }
-        __syncwarp();
 
         // ---- sorted set back to global; nonempty A rows in local order
         int NR = 0, S = 0;

@@ -320,6 +320,82 @@ void graph_build_walk_sym(DevGraph& g) {
     graph_ensure_recip(g, w.max_deg);
 }
 
+// ---------------------------------------------------------------------------
+// ingest on the device (edge-id A, no values): int64 CSR -> int32 CSR + a_ri,
+// validated as CsrMatrix::validate does (row_ptr[0] == 0, non-decreasing,
+// columns in range), max out-degree reduced on the way. The first offending
+// entry in row-major order is reported (atomicMin over its position).
+
+__global__ void k_ingest_rows(const int64_t* __restrict__ rp64, int32_t n, int32_t* __restrict__ rp32,
+                              int2* __restrict__ ari, int32_t* __restrict__ st) {
+    // st[0] = max degree, st[1] = first row with row_ptr decreasing (or INT_MAX)
+    int32_t md = 0;
+    for (int64_t u = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; u <= n; u += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t b = rp64[u];
+        rp32[u] = (int32_t)b;
+        if (u < n) {
+            const int64_t e = rp64[u + 1];
+            if (e < b) atomicMin(&st[1], (int32_t)u);
+            const int32_t d = e > b ? (int32_t)(e - b) : 0;
+            ari[u] = make_int2((int32_t)b, d);
+            md = max(md, d);
+        }
+    }
+    md = __reduce_max_sync(kFull, md);
+    if ((threadIdx.x & 31) == 0) atomicMax(&st[0], md);
+}
+
+__global__ void k_ingest_cols(const int64_t* __restrict__ ci64, int64_t nnz, int64_t n_cols,
+                              int32_t* __restrict__ ci32, unsigned long long* __restrict__ first_bad) {
+    for (int64_t k = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; k < nnz; k += (int64_t)gridDim.x * blockDim.x) {
+        const int64_t c = ci64[k];
+        ci32[k] = (int32_t)c;
+        if (c < 0 || c >= n_cols) atomicMin(first_bad, (unsigned long long)k);
+    }
+}
+
+void graph_ingest_device(DevGraph& g, const int64_t* row_ptr, const int64_t* col_idx, cudaStream_t st) {
+    const int32_t n = (int32_t)g.n_rows;
+    const int64_t nnz = g.nnz;
+    DevBuf<int64_t> rp64, ci64;
+    DevBuf<int32_t> stat;
+    DevBuf<unsigned long long> bad;
+    rp64.reserve((size_t)n + 1);
+    ci64.reserve((size_t)std::max<int64_t>(nnz, 1));
+    stat.reserve(2);
+    bad.reserve(1);
+    HGS_CUDA(cudaMemcpyAsync(rp64.p, row_ptr, sizeof(int64_t) * ((size_t)n + 1), cudaMemcpyHostToDevice, st));
+    if (nnz) HGS_CUDA(cudaMemcpyAsync(ci64.p, col_idx, sizeof(int64_t) * (size_t)nnz, cudaMemcpyHostToDevice, st));
+    const int32_t init[2] = {0, 0x7fffffff};
+    HGS_CUDA(cudaMemcpyAsync(stat.p, init, sizeof(init), cudaMemcpyHostToDevice, st));
+    HGS_CUDA(cudaMemsetAsync(bad.p, 0xff, sizeof(unsigned long long), st));
+    g.a.n = n;
+    g.a.nnz = nnz;
+    g.a.rp.reserve((size_t)n + 1);
+    g.a.ci.reserve((size_t)std::max<int64_t>(nnz, 1));
+    g.a_ri.reserve((size_t)std::max<int32_t>(n, 1));
+    k_ingest_rows<<<148 * 4, 256, 0, st>>>(rp64.p, n, g.a.rp.p, g.a_ri.p, stat.p);
+    if (nnz) k_ingest_cols<<<148 * 8, 256, 0, st>>>(ci64.p, nnz, g.n_cols, g.a.ci.p, bad.p);
+    HGS_CUDA(cudaGetLastError());
+    int32_t hs[2];
+    unsigned long long hb = 0;
+    HGS_CUDA(cudaMemcpyAsync(hs, stat.p, sizeof(hs), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaMemcpyAsync(&hb, bad.p, sizeof(hb), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaStreamSynchronize(st));
+    // the first failure in row-major order, as the host loop would meet it:
+    // row u's pointers are checked before its entries
+    const int64_t u_bad = hs[1] != 0x7fffffff ? hs[1] : (int64_t)n;  // row_ptr monotone on [0, u_bad]
+    const bool col_first = hb != ~0ULL && (int64_t)hb < row_ptr[u_bad];
+    if (hs[1] != 0x7fffffff && !col_first) fail(HGS_EINVAL, "hgs_graph_create: row_ptr not non-decreasing");
+    if (hb != ~0ULL) {  // first bad entry in row-major order: its row by binary search
+        const int64_t k = (int64_t)hb;
+        const int64_t u = std::upper_bound(row_ptr, row_ptr + u_bad + 1, k) - row_ptr - 1;
+        fail(HGS_EINVAL, "CsrMatrix: entry (" + std::to_string(u) + ", " + std::to_string(col_idx[k]) +
+                             ") out of range for " + std::to_string(g.n_rows) + "x" + std::to_string(g.n_cols));
+    }
+    g.a.max_deg = hs[0];
+}
+
 void graph_ensure_recip(DevGraph& g, int32_t max_m) {
     std::lock_guard<std::recursive_mutex> lock(g.lazy_mu);
     const int32_t need = max_m + 1;

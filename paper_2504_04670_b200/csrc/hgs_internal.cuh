@@ -135,6 +135,8 @@ struct DevGraph {
 };
 
 void graph_build_walk_sym(DevGraph& g);  // K0 (graph.cu)
+// int64 edge-id CSR (host) -> device int32 A + a_ri, validated on the device (graph.cu)
+void graph_ingest_device(DevGraph& g, const int64_t* row_ptr, const int64_t* col_idx, cudaStream_t st);
 
 // Inputs of one sampling call (device pointers).
 struct CallInputs {

@@ -144,6 +144,7 @@ def lib() -> C.CDLL:
         L.hgs_graph_info.argtypes = [vp, vp]
         L.hgs_graph_walk.argtypes = [vp, i32, vp, vp]
         L.hgs_graph_destroy.argtypes = [vp]
+        L.hgs_graph_gather.argtypes = [vp, vp, i64, vp, i64, vp, vp, vp]
         L.hgs_sample_create.argtypes = [vp, vp, C.POINTER(vp)]
         L.hgs_sample_destroy.argtypes = [vp]
         L.hgs_sample_run.argtypes = [vp, C.POINTER(Config), vp, vp, i64, vp, vp]
@@ -159,6 +160,10 @@ def lib() -> C.CDLL:
         L.hgs_sample_launches.argtypes = [vp, vp]
         L.hgs_sample_reruns.argtypes = [vp, vp]
         L.hgs_sample_stats.argtypes = [vp, vp, i32]
+        L.hgs_current_device.argtypes = [C.POINTER(C.c_int)]
+        L.hgs_event_save.argtypes = [C.c_char_p, i64, i64, vp, vp, vp, vp, i64, vp, i64, vp]
+        L.hgs_event_info.argtypes = [C.c_char_p, vp]
+        L.hgs_graph_load.argtypes = [C.c_int, C.c_char_p, C.POINTER(vp)]
         _lib_cache = L
     return _lib_cache
 
@@ -208,8 +213,43 @@ def philox4x32_10(ctr, key) -> np.ndarray:
     return o
 
 
+def save_event(path: str, row_ptr, col_idx, *, values=None, node_feat=None, edge_feat=None, labels=None,
+               n_cols=None) -> None:
+    """Binary event file (hgs_event_save): the ingest format hgs_graph_load /
+    Graph.load read back with mmap (no CUDA needed to write it)."""
+    rp = np.ascontiguousarray(row_ptr, np.int64)
+    ci = np.ascontiguousarray(col_idx, np.int64)
+    va = None if values is None else np.ascontiguousarray(values, np.float64)
+    nf = None if node_feat is None else np.ascontiguousarray(node_feat, np.float64)
+    ef = None if edge_feat is None else np.ascontiguousarray(edge_feat, np.float64)
+    lb = None if labels is None else np.ascontiguousarray(labels, np.uint8)
+    n = len(rp) - 1
+    f_v = 0 if nf is None else (nf.shape[1] if nf.ndim == 2 else nf.size // max(n, 1))
+    f_e = 0 if ef is None else (ef.shape[1] if ef.ndim == 2 else ef.size // max(int(rp[-1]), 1))
+    _check(lib().hgs_event_save(os.fsencode(path), n, n if n_cols is None else int(n_cols), _p(rp), _p(ci), _p(va),
+                                _p(nf), f_v, _p(ef), f_e, _p(lb)))
+
+
+def event_info(path: str) -> dict:
+    a = np.zeros(6, np.int64)
+    _check(lib().hgs_event_info(os.fsencode(path), _p(a)))
+    return dict(zip(["n_rows", "n_cols", "nnz", "f_v", "f_e", "flags"], (int(x) for x in a)))
+
+
 class Graph:
     """Device-resident event graph (CSR A with edge ids; optional features)."""
+
+    @classmethod
+    def load(cls, path: str, device: int = 0) -> "Graph":
+        """hgs_graph_load: an event file (save_event) mmapped and built on the
+        device, features attached."""
+        info = event_info(path)
+        g = cls.__new__(cls)
+        g.n, g.n_cols, g.nnz = info["n_rows"], info["n_cols"], info["nnz"]
+        g.f_v, g.f_e = info["f_v"], info["f_e"]
+        g._h = C.c_void_p()
+        _check(lib().hgs_graph_load(device, os.fsencode(path), C.byref(g._h)))
+        return g
 
     def __init__(self, row_ptr, col_idx, values=None, n_cols=None, device=0):
         rp = np.ascontiguousarray(row_ptr, np.int64)

@@ -90,11 +90,16 @@ def test_compute_fails_loudly_without_gpu():
 
 
 def test_graph_create_validates_before_touching_the_device():
+    # host-side checks (O(n) row pointers; general-valued A entirely); the
+    # column range of an edge-id A is checked on the device
+    # (test_gpu_parity.py::test_ingest_validation_messages)
     from paper_2504_04670_b200 import hgs
     with pytest.raises(hgs.SamplerError, match="out of range"):
-        hgs.Graph(np.array([0, 1, 1]), np.array([5]))
+        hgs.Graph(np.array([0, 1, 1]), np.array([5]), np.ones(1))
     with pytest.raises(hgs.SamplerError, match="row_ptr"):
         hgs.Graph(np.array([1, 1, 1]), np.array([0]))
+    with pytest.raises(hgs.SamplerError, match="row_ptr not non-decreasing"):
+        hgs.Graph(np.array([0, 2, 1, 2]), np.array([0, 1]))
 
 
 def test_generator_matches_reference_digest():
@@ -137,3 +142,27 @@ def test_event_save_load_roundtrip(tmp_path):
     assert ev2.n == ev.n and ev2.m == ev.m
     for a in ("rp", "ci", "node_feat", "edge_feat", "labels"):
         assert np.array_equal(getattr(ev, a), getattr(ev2, a)), a
+
+
+def test_event_file_round_trip_and_corruption(tmp_path):
+    """hgs_event_save / hgs_event_info (no GPU needed): header round trip,
+    64-byte-aligned sections, truncated and foreign files rejected."""
+    from paper_2504_04670_b200 import hgs
+    rp = np.array([0, 2, 3, 3], np.int64)
+    ci = np.array([1, 2, 0], np.int64)
+    nf = np.arange(6, dtype=np.float64).reshape(3, 2)
+    ef = np.arange(3, dtype=np.float64).reshape(3, 1)
+    lab = np.array([1, 0, 1], np.uint8)
+    p = str(tmp_path / "ev.hgsev")
+    hgs.save_event(p, rp, ci, node_feat=nf, edge_feat=ef, labels=lab)
+    assert hgs.event_info(p) == {"n_rows": 3, "n_cols": 3, "nnz": 3, "f_v": 2, "f_e": 1, "flags": 0}
+    raw = open(p, "rb").read()
+    assert len(raw) % 64 == 0
+    open(p + ".cut", "wb").write(raw[:-64])
+    with pytest.raises(hgs.SamplerError, match="truncated or corrupt"):
+        hgs.event_info(p + ".cut")
+    open(p + ".bad", "wb").write(b"NOTANEVT" + raw[8:])
+    with pytest.raises(hgs.SamplerError, match="bad magic"):
+        hgs.event_info(p + ".bad")
+    with pytest.raises(hgs.SamplerError, match="cannot open"):
+        hgs.event_info(str(tmp_path / "missing"))

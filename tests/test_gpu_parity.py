@@ -673,3 +673,41 @@ def test_k1_xoshiro_serial_fallback(monkeypatch, every):
         dev, _ = device_run(g, roots, boff, seeds, depth=3, fanout=6, gather=True, state=st)
         ref = O.bulk_shadow(g, roots, boff, seeds, depth=3, fanout=6, gather=True, state=st)
         assert_same(dev, ref, True)
+
+
+def test_event_file_load_matches_arrays(tmp_path):
+    """Ingest (§8f #2): a C1 event written with hgs_event_save and loaded
+    with hgs_graph_load (mmap, device-side narrowing and validation) samples
+    exactly like the graph built from host arrays; reference digests hold."""
+    from paper_2504_04670_b200 import workload as W
+    H = hgs()
+    ev = W.preset_event("C1")
+    p = str(tmp_path / "c1.hgsev")
+    H.save_event(p, ev.rp, ev.ci, node_feat=ev.node_feat, edge_feat=ev.edge_feat, labels=ev.labels)
+    G = H.Graph.load(p)
+    assert (G.n, G.nnz, G.f_v, G.f_e) == (ev.n, ev.m, 6, 2)
+    roots, boff, seeds = W.bench_roots(ev.n, 256, 16, seed=1, rep=0)
+    c1 = load_json("c1.json")
+    S = H.Sampler(G)
+    for run in c1["runs"]:
+        S.bulk_shadow(roots, boff, seeds, rng=run["rng"], depth=run["depth"], fanout=6, gather=True)
+        dev = S.to_host()
+        for f in ("l2g", "e_row", "e_col", "e_gid"):
+            assert sha(np.asarray(dev[f]).astype(np.int64)) == run["digests"][f], f
+        for f in ("xv", "ye", "lab"):
+            assert sha(dev[f]) == run["digests"][f], f
+
+
+@pytest.mark.parametrize("values", [False, True])
+def test_ingest_validation_messages(values):
+    """Device-side ingest (edge-id A) and the host path (general values) report
+    the first invalid entry in row-major order with the same text."""
+    H = hgs()
+    va = np.ones(4) if values else None
+    with pytest.raises(H.SamplerError, match=r"^CsrMatrix: entry \(1, 7\) out of range for 3x3$"):
+        H.Graph(np.array([0, 1, 3, 4]), np.array([1, 2, 7, 9]), va)
+    with pytest.raises(H.SamplerError, match="row_ptr not non-decreasing"):
+        H.Graph(np.array([0, 3, 2, 4]), np.array([1, 2, 0, 1]), va)
+    # a bad column in a row before the first decreasing row pointer is met first
+    with pytest.raises(H.SamplerError, match=r"^CsrMatrix: entry \(0, 5\) out of range for 3x3$"):
+        H.Graph(np.array([0, 2, 1, 4]), np.array([5, 2, 0, 1]), va)
