@@ -676,6 +676,148 @@ __global__ void __launch_bounds__(256) k_pack(PackParams p) {
     }
 }
 
+// K3 fused: pack + gather_features in one pass per root (warp per root).
+// The root's outputs are contiguous ranges (its vertices [vb, vb+Vr), edges
+// [eb, eb+Er)), so a warp writes them with consecutive lanes on consecutive
+// 16-byte pieces: local_to_global and the node rows (read from the L2-resident
+// feature table by the set it just read), the COO edges / edge ids and the
+// edge rows + labels (one 32-byte record per edge when f_e == 2). One read of
+// the sets and edge slots, no re-read of l2g / e_gid, one launch.
+#ifndef HGS_K3_U
+#define HGS_K3_U 4
+#endif
+__global__ void __launch_bounds__(256) k_pack_gather(PackParams p, const uint4* __restrict__ erec) {
+    const int lane = lane_id();
+    const int nwarps = gridDim.x * (blockDim.x >> 5);
+    constexpr int U = HGS_K3_U;
+    const uint64_t pol = l2_keep_policy();
+    for (int r = p.r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
+        int b;
+        {
+            int lo = 0, hi = p.k;  // largest b with batch_off[b] <= r
+            while (lo < hi) {
+                const int mid = (lo + hi + 1) >> 1;
+                if (p.batch_off[mid] <= r) lo = mid; else hi = mid - 1;
+            }
+            b = lo;
+        }
+        const int f = (int)p.batch_off[b];
+        const int64_t vb = p.root_voff[r], eb = p.root_eoff[r];
+        const int Vr = p.root_voff[r + 1] - (int32_t)vb;
+        const int Er = p.root_eoff[r + 1] - (int32_t)eb;
+        const int ecap = p.e_off ? p.e_off[r + 1] - p.e_off[r] : p.e_stride;
+        if (Er > ecap) continue;  // slot overflowed in K2 (reported there): the call is re-run
+        if (vb + Vr > p.v_cap || eb + Er > p.e_cap) {
+            if (lane == 0) report(p.ticket, kErrCapacity, r, -1);
+            continue;
+        }
+        const int32_t loc = (int32_t)vb - p.root_voff[f];
+        if (lane == 0) {
+            p.roots_local[r] = loc + p.root_rloc[r];
+            p.comp_off[r + b] = loc;
+            if (r == p.batch_off[b + 1] - 1) p.comp_off[r + 1 + b] = loc + Vr;
+        }
+        const int32_t* set = p.touched + (size_t)r * p.stride;
+        // local_to_global
+        for (int i0 = 0; i0 < Vr; i0 += 32 * U) {
+            int32_t u[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + 32 * k + lane;
+                u[k] = i < Vr ? set[i] : 0;
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int i = i0 + 32 * k + lane;
+                if (i < Vr) __stcs(p.l2g + vb + i, u[k]);
+            }
+        }
+        // node rows: Vr * f_v/2 sixteen-byte pieces (even f_v), else doubles
+        if (p.gather && p.f_v > 0) {
+            if ((p.f_v & 1) == 0) {
+                const int q2 = p.f_v >> 1;
+                const int np = Vr * q2;
+                const uint4* src = reinterpret_cast<const uint4*>(p.node_feat);
+                uint4* dst = reinterpret_cast<uint4*>(p.xv) + vb * q2;
+                for (int e0 = 0; e0 < np; e0 += 32 * U) {
+                    uint4 x[U];
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        const int e = e0 + 32 * k + lane;
+                        if (e < np) {
+                            const int vi = q2 == 1 ? e : p.fv_magic_local ? (int)__umulhi((unsigned)e, p.fv_magic_local)
+                                                                          : e / q2;
+                            x[k] = __ldg(src + (int64_t)__ldg(set + vi) * q2 + (e - vi * q2));
+                        }
+                    }
+#pragma unroll
+                    for (int k = 0; k < U; ++k) {
+                        const int e = e0 + 32 * k + lane;
+                        if (e < np) __stcs(dst + e, x[k]);
+                    }
+                }
+            } else {
+                const int np = Vr * p.f_v;
+                for (int e = lane; e < np; e += 32) {
+                    const int vi = e / p.f_v;
+                    __stcs(p.xv + vb * p.f_v + e, __ldg(p.node_feat + (int64_t)__ldg(set + vi) * p.f_v + (e - vi * p.f_v)));
+                }
+            }
+        }
+        // COO edges (block_diag rebasing), edge ids, edge rows + labels
+        const int2* ed = p.escratch + (p.e_off ? (size_t)p.e_off[r] : (size_t)r * p.e_stride);
+        for (int t0 = 0; t0 < Er; t0 += 32 * U) {
+            int2 e[U];
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int t = t0 + 32 * k + lane;
+                e[k] = t < Er ? ed[t] : make_int2(0, 0);
+            }
+            uint4 fr[U];
+            uint32_t lb[U];
+            if (p.gather && erec) {
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    if (t0 + 32 * k + lane < Er) {
+                        fr[k] = ldg_keep(erec + 2 * (int64_t)e[k].y, pol);
+                        lb[k] = ldg_keep(&erec[2 * (int64_t)e[k].y + 1].x, pol);
+                    }
+                }
+            }
+#pragma unroll
+            for (int k = 0; k < U; ++k) {
+                const int t = t0 + 32 * k + lane;
+                if (t < Er) {
+                    __stcs(p.e_row + eb + t, loc + (e[k].x >> 16));
+                    __stcs(p.e_col + eb + t, loc + (e[k].x & 0xffff));
+                    __stcs(p.e_gid + eb + t, e[k].y);
+                    if (p.gather && erec) {
+                        __stcs(reinterpret_cast<uint4*>(p.ye) + eb + t, fr[k]);
+                        __stcs(p.lab + eb + t, (uint8_t)lb[k]);
+                    }
+                }
+            }
+            if (p.gather && !erec) {  // general f_e: feature by feature
+#pragma unroll
+                for (int k = 0; k < U; ++k) {
+                    const int t = t0 + 32 * k + lane;
+                    if (t < Er) {
+                        const int64_t g = e[k].y;
+                        p.lab[eb + t] = __ldg(p.labels + g);
+                        for (int c = 0; c < p.f_e; ++c)
+                            __stcs(p.ye + (eb + t) * p.f_e + c, __ldg(p.edge_feat + g * p.f_e + c));
+                    }
+                }
+            }
+        }
+    }
+}
+
+void launch_pack_gather(int grid, const PackParams& pp, const uint4* erec, cudaStream_t st) {
+    k_pack_gather<<<grid, 256, 0, st>>>(pp, erec);
+    HGS_CUDA(cudaGetLastError());
+}
+
 // gather_features (sampler.cpp:211-243) over the packed outputs: node rows
 // of l2g, edge rows and labels of the edge ids. Flat grid-stride streams.
 // Random rows come from L2 (the event's features are L2-resident), where the

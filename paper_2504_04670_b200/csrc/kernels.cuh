@@ -122,6 +122,7 @@ struct PackParams {
     int32_t f_v, f_e, gather;
     uint32_t fv_magic;  // ceil(2^32 / (f_v/2)) for even f_v (0 when f_v/2 == 1)
     uint32_t fv_err;    // (f_v/2) * fv_magic - 2^32: the magic quotient is exact for e * fv_err < 2^32
+    uint32_t fv_magic_local;  // the same magic when exact for every per-root piece index (< set_cap * f_v/2), else 0
     int64_t v_cap, e_cap;
     int32_t set_cap;  // per-warp staging of the root's set (>= max set size)
     int32_t* __restrict__ ticket;
@@ -148,6 +149,8 @@ void launch_scan(const int32_t* nv, const int32_t* ne, int32_t r0, int32_t r1, i
                  int32_t* eoff, int32_t* ticket, cudaStream_t st);
 int64_t scan_tmp_words(int64_t R);
 void launch_pack(int grid, const PackParams& pp, cudaStream_t st);
+// K3 fused: pack + node/edge gathers per root (erec nullable: general f_e)
+void launch_pack_gather(int grid, const PackParams& pp, const uint4* erec, cudaStream_t st);
 // node / edge feature gather over the packed call outputs
 // over vertices [*vb, *ve) and edges [*eb, *ee) of the call (device pointers)
 void launch_gather_packed(int blocks, const PackParams& pp, const uint4* erec, const int32_t* vb,

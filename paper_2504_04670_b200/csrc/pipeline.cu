@@ -152,6 +152,15 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     return c;
 }
 
+// K3 as pack + two flat gathers (default) or one fused per-root pack+gather
+// kernel (HGS_K3_FUSED=1; B200, C2: 0.464 ms against 0.384 — the flat
+// kernels sweep the outputs with all warps together, the per-root warps
+// write ~9.5k scattered streams)
+bool k3_fused() {
+    const char* e = getenv("HGS_K3_FUSED");
+    return e && e[0] == '1';
+}
+
 int sm_count(int device) {
     int n = 0;
     HGS_CUDA(cudaDeviceGetAttribute(&n, cudaDevAttrMultiProcessorCount, device));
@@ -265,6 +274,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         const uint64_t m = ((((uint64_t)1 << 32) + q2 - 1) / q2);  // 2^32 for q2 == 1: unused then
         pp.fv_magic = q2 > 1 ? (uint32_t)m : 0u;
         pp.fv_err = q2 > 1 ? (uint32_t)(q2 * m - ((uint64_t)1 << 32)) : 0u;
+        // per-root piece indices stay below (kMaxSet + 1) * q2
+        pp.fv_magic_local = (q2 > 1 && (uint64_t)(kMaxSet + 1) * q2 * pp.fv_err < ((uint64_t)1 << 32)) ? (uint32_t)m : 0u;
     }
     pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
     pp.set_cap = c.set_cap;
@@ -384,9 +395,14 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         }
         pp.r0 = r0; pp.R = r1;
         const int64_t pgrid = split ? (Rc + 7) / 8 : std::min<int64_t>((int64_t)sm_count(g.device) * 8, (Rc + 7) / 8);
+        if (k3_fused()) {  // pack + gathers in one pass per root
+            launch_pack_gather((int)std::max<int64_t>(pgrid, 1), pp, g.erec.p, pst);
+            ++s->launches;
+        } else {
         launch_pack((int)std::max<int64_t>(pgrid, 1), pp, pst);
         ++s->launches;
-        if (cfg.gather) {  // this chunk's vertices / edges
+        }
+        if (cfg.gather && !k3_fused()) {  // this chunk's vertices / edges
 #ifndef HGS_GATHER_BPSM
 #define HGS_GATHER_BPSM 8
 #endif

@@ -711,3 +711,26 @@ def test_ingest_validation_messages(values):
     # a bad column in a row before the first decreasing row pointer is met first
     with pytest.raises(H.SamplerError, match=r"^CsrMatrix: entry \(0, 5\) out of range for 3x3$"):
         H.Graph(np.array([0, 2, 1, 4]), np.array([5, 2, 0, 1]), va)
+
+
+@pytest.mark.parametrize("fused", ["1", "0"])
+@pytest.mark.parametrize("f_v,f_e", [(1, 1), (2, 2), (3, 5), (8, 2), (510, 3)])
+def test_feature_widths(monkeypatch, fused, f_v, f_e):
+    """gather_features for any row widths, through the fused K3 and the
+    pack + flat-gather path: f_v = 2 (a single 16-byte piece per row, where a
+    magic divisor of 2^32 would wrap) and f_v = 510 (q = 255, whose rounded
+    reciprocal is inexact beyond ~66k pieces: 4,000 vertices x 255 pieces
+    exceed that) included."""
+    monkeypatch.setenv("HGS_K3_FUSED", fused)
+    H = hgs()
+    g = random_graph(5000, 40000, 3)
+    rs = np.random.default_rng(f_v + f_e)
+    g.node_feat = rs.standard_normal((g.n, f_v))
+    g.edge_feat = rs.standard_normal((len(g.ci), f_e))
+    roots = np.concatenate([rs.permutation(g.n)[:700] for _ in range(2)]).astype(np.int64)
+    boff = np.array([0, 700, 1400], np.int64)
+    seeds = rs.integers(0, 2**63, 1400, dtype=np.uint64)
+    dev, S = device_run(g, roots, boff, seeds, depth=3, fanout=4, gather=True)
+    assert S.counts.V > 4000
+    ref = O.bulk_shadow(g, roots, boff, seeds, depth=3, fanout=4, gather=True)
+    assert_same(dev, ref, True)
