@@ -55,9 +55,10 @@ int ceil_log2(int64_t x) {
 // Opt-in (HGS_K2_DIR=1): measured on B200 at C2 it is no faster than the
 // hash-set kernel (0.774 vs 0.752 ms at 24 warps per SM; K2 is bound by its
 // per-warp latency chain and occupancy, not by the probe), see DESIGN.md.
-bool plan_extract_dir(CallPlan& c, int64_t bound, int64_t n) {
+bool plan_extract_dir(CallPlan& c, int64_t bound, int64_t n, int32_t max_out_deg) {
     if (!getenv("HGS_K2_DIR")) return false;
     if (bound > 2048) return false;
+    (void)max_out_deg;
     c.set_cap = (int32_t)std::max<int64_t>(16, (bound + 3) / 4 * 4);
     c.row_cap = c.set_cap;
     c.win_cap = std::max(16, c.set_cap / 2);  // windows per pass (larger rows: several passes)
@@ -120,8 +121,8 @@ bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
     return c.k2_warps > 0;
 }
 
-bool plan_k2(CallPlan& c, int64_t bound, int64_t n) {
-    return plan_extract_dir(c, bound, n) || plan_extract(c, bound, n);
+bool plan_k2(CallPlan& c, int64_t bound, int64_t n, int32_t max_out_deg) {
+    return plan_extract_dir(c, bound, n, max_out_deg) || plan_extract(c, bound, n);
 }
 
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
@@ -147,8 +148,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
         c.cache_entries = 0;
         c.expand_smem = rbytes;
     }
-    if (c.max_t > kMaxSet || !plan_k2(c, c.max_t, n)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
-    (void)a;
+    if (c.max_t > kMaxSet || !plan_k2(c, c.max_t, n, a.max_deg)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
     return c;
 }
 
@@ -326,7 +326,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         int32_t tmax = 0;
         HGS_CUDA(cudaMemcpyAsync(&tmax, s->ticket.p + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         HGS_CUDA(cudaStreamSynchronize(st));
-        if (!plan_k2(c, std::max<int32_t>(tmax, 1), g.n_rows)) {
+        if (!plan_k2(c, std::max<int32_t>(tmax, 1), g.n_rows, g.a.max_deg)) {
             // beyond one warp's shared memory: K2 keeps its working sets in
             // a global scratch slot per warp (3 hash slots per key)
             plan_extract(c, 1, g.n_rows);  // rank bits / packing for the real bound below
@@ -344,7 +344,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
             c.k2_gmem = true;
         }
     }
-    if (c.k2_warps == 0) plan_k2(c, 1, g.n_rows);  // R == 0: nothing to extract
+    if (c.k2_warps == 0) plan_k2(c, 1, g.n_rows, g.a.max_deg);  // R == 0: nothing to extract
     set_layout();
     const size_t xsmem = c.k2_gmem ? 0 : (size_t)c.k2_warps * c.warp_bytes;
     const int xper_sm = c.k2_gmem ? 2
