@@ -396,6 +396,67 @@ void graph_ingest_device(DevGraph& g, const int64_t* row_ptr, const int64_t* col
     g.a.max_deg = hs[0];
 }
 
+// ---------------------------------------------------------------------------
+// Quad layout of A for k_extract_bm: every row padded to a multiple of 4
+// entries (pad = n, never a vertex) so a lane reads 4 entries of ONE row with
+// one 16-byte load. Entries are stored as probe words of k_extract_bm's
+// directory: ((c >> 4) * 4) << 8 | (15 - (c & 15)) = the byte offset of the
+// directory word holding column c and the left shift that moves c's member bit
+// to bit 15. a_qid holds the entries' edge ids (input CSR positions, through
+// a_gid when explicit zeros were dropped) and a_rq[v] = (first quad, out-degree).
+
+__global__ void k_quad_counts(const int32_t* __restrict__ rp, int32_t n, int32_t* __restrict__ qc) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x)
+        qc[v] = (rp[v + 1] - rp[v] + 3) >> 2;
+}
+
+__global__ void k_quad_fill(const int32_t* __restrict__ rp, const int32_t* __restrict__ ci,
+                            const int32_t* __restrict__ gid, int32_t n, const int32_t* __restrict__ qrp,
+                            int4* __restrict__ aq, int4* __restrict__ aqid, int2* __restrict__ arq) {
+    for (int32_t v = blockIdx.x * blockDim.x + threadIdx.x; v < n; v += gridDim.x * blockDim.x) {
+        const int32_t b = rp[v], d = rp[v + 1] - b, q0 = qrp[v];
+        arq[v] = make_int2(q0, d);
+        for (int32_t i = 0; 4 * i < d; ++i) {
+            int32_t c[4], e[4];
+#pragma unroll
+            for (int s = 0; s < 4; ++s) {
+                const int32_t k = b + 4 * i + s;
+                const bool in = 4 * i + s < d;
+                const uint32_t col = in ? (uint32_t)ci[k] : (uint32_t)n;
+                c[s] = (int32_t)((((col >> 4) << 2) << 8) | (15u - (col & 15u)));
+                e[s] = in ? (gid ? gid[k] : k) : -1;
+            }
+            aq[q0 + i] = make_int4(c[0], c[1], c[2], c[3]);
+            aqid[q0 + i] = make_int4(e[0], e[1], e[2], e[3]);
+        }
+    }
+}
+
+void graph_ensure_quads(DevGraph& g) {
+    std::lock_guard<std::recursive_mutex> lock(g.lazy_mu);
+    if (g.quads_built) return;
+    const int32_t n = g.a.n;
+    cudaStream_t st = g.stream;
+    DevBuf<int32_t> qc, qrp;
+    qc.reserve((size_t)n + 1);
+    qrp.reserve((size_t)n + 1);
+    const unsigned grid = (unsigned)std::max<int64_t>(1, std::min<int64_t>((n + 255) / 256, 148 * 8));
+    k_quad_counts<<<grid, 256, 0, st>>>(g.a.rp.p, n, qc.p);
+    HGS_CUDA(cudaGetLastError());
+    scan_exclusive_i32(qc.p, qrp.p, n, st);
+    int32_t nq = 0;
+    HGS_CUDA(cudaMemcpyAsync(&nq, qrp.p + n, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
+    HGS_CUDA(cudaStreamSynchronize(st));
+    g.a_q.reserve((size_t)std::max(nq, 1));
+    g.a_qid.reserve((size_t)std::max(nq, 1));
+    g.a_rq.reserve((size_t)std::max(n, 1));
+    k_quad_fill<<<grid, 256, 0, st>>>(g.a.rp.p, g.a.ci.p, g.has_gid ? g.a_gid.p : nullptr, n, qrp.p, g.a_q.p,
+                                      g.a_qid.p, g.a_rq.p);
+    HGS_CUDA(cudaGetLastError());
+    HGS_CUDA(cudaStreamSynchronize(st));
+    g.quads_built = true;
+}
+
 void graph_ensure_recip(DevGraph& g, int32_t max_m) {
     std::lock_guard<std::recursive_mutex> lock(g.lazy_mu);
     const int32_t need = max_m + 1;

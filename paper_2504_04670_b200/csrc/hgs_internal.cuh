@@ -109,6 +109,10 @@ struct DevGraph {
     bool has_gid = false;
     DevCsr a_full;           // full pattern of A (only if zeros dropped; else == a)
     bool has_full = false;
+    DevBuf<int4> a_q;        // A's rows padded to 4-entry quads (pad entry = n_rows), built lazily for K2
+    DevBuf<int4> a_qid;      // edge id (input CSR position) of every a_q entry, -1 for pads
+    DevBuf<int2> a_rq;       // per vertex: (first quad, out-degree)
+    bool quads_built = false;
     DevCsr walk_sym;         // pattern(A ∪ Aᵀ), built lazily by K0
     bool sym_built = false;
     DevBuf<uint8_t> neg_row; // rows of A holding a negative value (only if any)
@@ -135,6 +139,7 @@ struct DevGraph {
 };
 
 void graph_build_walk_sym(DevGraph& g);  // K0 (graph.cu)
+void graph_ensure_quads(DevGraph& g);    // a_q / a_rq for k_extract_bm (graph.cu)
 // int64 edge-id CSR (host) -> device int32 A + a_ri, validated on the device (graph.cu)
 void graph_ingest_device(DevGraph& g, const int64_t* row_ptr, const int64_t* col_idx, cudaStream_t st);
 

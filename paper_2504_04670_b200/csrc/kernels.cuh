@@ -93,6 +93,10 @@ struct ExtractParams {
     unsigned char* gscratch;            // nullable: per-warp working sets in global memory
     int32_t lnb;                        // k_extract_dir: log2 of the rank-directory buckets
     const int32_t* __restrict__ e_off;  // nullable: exact edge-slot offsets [R+1] (re-run after overflow)
+    int32_t tab_n;                      // k_extract_bm: directory words (multiple of 32, > n / 16)
+    const int4* __restrict__ a_q;       // k_extract_bm: A in 4-entry quads (DevGraph::a_q)
+    const int4* __restrict__ a_qid;     // k_extract_bm: edge ids of the a_q entries
+    const int2* __restrict__ a_rq;      // k_extract_bm: per vertex (first quad, out-degree)
 };
 
 // K3: packing + gather.
@@ -133,6 +137,13 @@ int extract_blocks_per_sm(size_t smem, int warps, bool packed);
 // K2, directory variant (extract_dir.cu): the default path
 void launch_extract_dir(int grid, int warps, size_t smem, const ExtractParams& xp, cudaStream_t st);
 int extract_dir_prepare(size_t smem, int warps);
+// K2, one root per CTA with a bitmap rank directory (extract_bm.cu): the default
+// for touched lists of <= 512 entries on graphs whose directory fits shared memory
+#ifndef HGS_K2M_WARPS
+#define HGS_K2M_WARPS 4  // warps per k_extract_bm CTA (one root per CTA)
+#endif
+void launch_extract_bm(int grid, int warps, size_t smem, const ExtractParams& xp, cudaStream_t st);
+int extract_bm_prepare(size_t smem, int warps);
 // Shared-memory opt-in + occupancy (CTAs per SM, min over the kernels) of
 // kernels launched with `smem` dynamic bytes and 32*warps threads, cached per
 // (device, kernels, smem, warps): no driver calls on the per-call path.

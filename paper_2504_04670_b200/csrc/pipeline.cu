@@ -7,6 +7,7 @@
 
 #include <algorithm>
 #include <cstdlib>
+#include <cstring>
 #include <string>
 #include <vector>
 
@@ -36,6 +37,8 @@ struct CallPlan {
     int32_t k2_warps;  // warps per K2 CTA (0: not planned yet)
     bool k2_gmem;      // K2 working sets in global scratch (sets beyond shared memory)
     bool k2_dir;       // K2 = k_extract_dir (rank directory); else the hash-set k_extract
+    bool k2_bm;        // K2 = k_extract_bm (one root per CTA, bitmap rank directory)
+    int32_t tab_n;     // k_extract_bm: directory words (16 vertex ids each)
     int32_t lnb;       // k_extract_dir: log2 of the directory buckets
 };
 
@@ -56,7 +59,8 @@ int ceil_log2(int64_t x) {
 // hash-set kernel (0.774 vs 0.752 ms at 24 warps per SM; K2 is bound by its
 // per-warp latency chain and occupancy, not by the probe), see DESIGN.md.
 bool plan_extract_dir(CallPlan& c, int64_t bound, int64_t n, int32_t max_out_deg) {
-    if (!getenv("HGS_K2_DIR")) return false;
+    const char* sel = getenv("HGS_K2");
+    if (!getenv("HGS_K2_DIR") && !(sel && strcmp(sel, "dir") == 0)) return false;
     if (bound > 2048) return false;
     (void)max_out_deg;
     c.set_cap = (int32_t)std::max<int64_t>(16, (bound + 3) / 4 * 4);
@@ -121,8 +125,39 @@ bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
     return c.k2_warps > 0;
 }
 
+// k_extract_bm (extract_bm.cu): one root per CTA of HGS_K2M_WARPS warps; the
+// CTA's shared memory holds the bitmap rank directory of the whole id range
+// (one 32-bit word per 16 vertex ids: 16 membership bits + the rank of the
+// word's first member) plus the set, row and window arrays of one root.
+// Applies to touched lists of <= 512 entries on graphs whose directory leaves
+// room for >= 3 CTAs per SM (n up to ~290k ids).
+// Opt-in (HGS_K2=bm): measured on B200 at C2 it runs in 0.78 ms against the
+// hash-set kernel's 0.76 ms (fewer shared wavefronts, but as many warp
+// instructions per root: see DESIGN.md §4).
+bool plan_extract_bm(CallPlan& c, int64_t bound, int64_t n) {
+    const char* sel = getenv("HGS_K2");
+    if (!sel || strcmp(sel, "bm") != 0) return false;
+    if (bound > 512 || n <= 0) return false;
+    c.tab_n = (int32_t)((n + 1 + 16 * 32 - 1) / (16 * 32) * 32);  // covers the pad id n
+    c.set_cap = (int32_t)((bound + 3) / 4 * 4);
+    c.row_cap = c.set_cap;
+    const int64_t nw2r = (c.tab_n / 32 + 3) & ~3;
+    c.win_cap = 1024;  // flat quads per pass (the quad-owner array)
+    const int64_t qw = std::max<int64_t>(c.win_cap / 2, nw2r);
+    const size_t bytes = 4 * (size_t)c.tab_n + 4 * (size_t)nw2r + 4 * (size_t)(c.set_cap + 4) +
+                         8 * (size_t)c.row_cap + 4 * (size_t)qw + 256;
+    if (bytes > 72 * 1024) return false;
+    c.warp_bytes = (int32_t)((bytes + 127) / 128 * 128);  // per CTA
+    c.k2_warps = HGS_K2M_WARPS;
+    c.k2_bm = true;
+    c.k2_dir = false;
+    c.k2_gmem = false;
+    return true;
+}
+
 bool plan_k2(CallPlan& c, int64_t bound, int64_t n, int32_t max_out_deg) {
-    return plan_extract_dir(c, bound, n, max_out_deg) || plan_extract(c, bound, n);
+    c.k2_bm = false;
+    return plan_extract_bm(c, bound, n) || plan_extract_dir(c, bound, n, max_out_deg) || plan_extract(c, bound, n);
 }
 
 CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
@@ -258,6 +293,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         xp.win_cap = c.win_cap; xp.warp_bytes = c.warp_bytes; xp.rank_bits = c.rank_bits;
         xp.cnt_lg = 31 - __builtin_clz((unsigned)(2 * c.row_cap));
         xp.lnb = c.lnb;
+        xp.tab_n = c.tab_n;
     };
 
     PackParams pp{};
@@ -346,11 +382,18 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     }
     if (c.k2_warps == 0) plan_k2(c, 1, g.n_rows, g.a.max_deg);  // R == 0: nothing to extract
     set_layout();
-    const size_t xsmem = c.k2_gmem ? 0 : (size_t)c.k2_warps * c.warp_bytes;
+    const size_t xsmem = c.k2_gmem ? 0 : c.k2_bm ? (size_t)c.warp_bytes : (size_t)c.k2_warps * c.warp_bytes;
     const int xper_sm = c.k2_gmem ? 2
+                        : c.k2_bm ? extract_bm_prepare(xsmem, c.k2_warps)
                         : c.k2_dir ? extract_dir_prepare(xsmem, c.k2_warps)
                                    : extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
     xp.gscratch = nullptr;
+    if (c.k2_bm) {
+        graph_ensure_quads(g);
+        xp.a_q = g.a_q.p;
+        xp.a_qid = g.a_qid.p;
+        xp.a_rq = g.a_rq.p;
+    }
     if (c.k2_gmem) {
         const size_t slots = (size_t)xper_sm * sm_count(g.device) * c.k2_warps;
         s->k2g.reserve(slots * (size_t)c.warp_bytes);
@@ -368,13 +411,14 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         const int32_t r0 = (int32_t)(ci * chunk), r1 = (int32_t)std::min<int64_t>(R, r0 + chunk);
         const int64_t Rc = r1 - r0;
         xp.r0 = r0; xp.R = r1;
-        const int64_t per_cta = c.k2_warps;
+        const int64_t per_cta = c.k2_bm ? 1 : c.k2_warps;  // roots in flight per CTA
         const int64_t xgrid = (split && !c.k2_gmem)
                                   ? (Rc + per_cta - 1) / per_cta
                                   : std::min<int64_t>((int64_t)xper_sm * sm_count(g.device), (Rc + per_cta - 1) / per_cta);
         xp.work = s->ticket.p + 5;
         HGS_CUDA(cudaMemsetAsync(xp.work, 0, sizeof(int32_t), st));
-        if (c.k2_dir) launch_extract_dir((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, st);
+        if (c.k2_bm) launch_extract_bm((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, st);
+        else if (c.k2_dir) launch_extract_dir((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, st);
         else launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);
         ++s->launches;
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));

@@ -88,7 +88,7 @@ def run(rs, *, secs=None, max_cases=None, log=print):
 def main():
     secs = float(sys.argv[1]) if len(sys.argv) > 1 else 300
     seed = int(sys.argv[2]) if len(sys.argv) > 2 else 12345
-    print(f"fuzz_gpu: seed {seed}, {secs:.0f}s, K2 = {'directory' if os.environ.get('HGS_K2_DIR') else 'hash-set'}",
+    print(f"fuzz_gpu: seed {seed}, {secs:.0f}s, K2 = {os.environ.get('HGS_K2', 'hash')}",
           flush=True)
     _, bad = run(np.random.default_rng(seed), secs=secs, log=lambda m: print(m, flush=True))
     sys.exit(1 if bad else 0)

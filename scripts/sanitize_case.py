@@ -1,6 +1,6 @@
 """Small sampling calls for compute-sanitizer (memcheck / racecheck / synccheck /
-initcheck): K0, K1 (serial, Philox group, xoshiro group), K2 (hash-set and
-directory variants), offset scan, K3 pack + gathers, the standalone gather and
+initcheck): K0, K1 (serial, Philox group, xoshiro group), K2 (hash-set,
+directory and bitmap-directory variants), offset scan, K3 pack + gathers, the standalone gather and
 the ingest kernels, each checked against the oracle.
 usage: compute-sanitizer --tool <tool> python scripts/sanitize_case.py"""
 import os
@@ -19,7 +19,7 @@ roots = np.concatenate([rs.permutation(1500)[:64] for _ in range(3)]).astype(np.
 boff = np.array([0, 64, 128, 192], np.int64)
 seeds = rs.integers(0, 2**63, 192, dtype=np.uint64)
 bad = 0
-for env in ({}, {"HGS_K2_DIR": "1"}, {"HGS_K1_GROUPX": "1"}):
+for env in ({}, {"HGS_K2": "dir"}, {"HGS_K2": "bm"}, {"HGS_K1_GROUPX": "1"}):
     for k, v in env.items():
         os.environ[k] = v
     S = hgs.Sampler(G)

@@ -173,10 +173,13 @@ def test_fuzz_slice():
 
 
 @pytest.mark.parametrize("case", ["random", "clustered", "c1"])
-def test_k2_directory_variant(monkeypatch, case):
-    """The opt-in rank-directory K2 (HGS_K2_DIR=1, csrc/extract_dir.cu) gives
-    the same outputs as the oracle."""
-    monkeypatch.setenv("HGS_K2_DIR", "1")
+@pytest.mark.parametrize("kernel", ["dir", "bm"])
+def test_k2_alternative_kernels(monkeypatch, case, kernel):
+    """The opt-in K2 kernels give the same outputs as the oracle: the
+    rank-directory kernel with a shared-memory counting sort (HGS_K2=dir,
+    csrc/extract_dir.cu) and the CTA-per-root bitmap-directory kernel over
+    A's 4-entry quads (HGS_K2=bm, csrc/extract_bm.cu)."""
+    monkeypatch.setenv("HGS_K2", kernel)
     hg = H()
     if case == "c1":
         c1 = load_json("c1.json")
