@@ -262,6 +262,64 @@ int hgs_sample_rows(int device, int64_t n_rows, int64_t n_cols, const int64_t* r
                     const uint64_t* rng_state, const int64_t* row_streams, int64_t* out_off, int64_t* out_cols,
                     uint32_t* draws, uint32_t* decisions);
 
+/* ---- consumer --------------------------------------------
+ * Device-resident counterparts of what the reference trainer does with a
+ * sampled batch: slice_components (trainer.cpp:221-269, the DDP split of a
+ * minibatch's components), the IGNN message-passing gathers and scatters
+ * (Tape::gather_rows / scatter_add, autodiff.cpp:121-157, used at
+ * ignn.cpp:158-164, and their backward passes, autodiff.cpp:260-281) and the
+ * reduction step of the coalesced gradient all-reduce (allreduce_coalesced
+ * -> InMemoryComm::allreduce_mean, trainer.cpp:84-123, 155-157). Device
+ * pointers throughout; fp64 results are bit-identical with the reference
+ * (sums in the reference's order, no floating-point atomics). */
+
+/* One slice of a batch of the last run. e_row / e_col / comp_off /
+ * roots_local are rebased to the slice (written by a kernel into buffers of
+ * the sample handle, valid until its next slice or run); the other pointers
+ * are views into the run's outputs (valid until its next run). */
+typedef struct {
+    int64_t n_vertices, n_edges, n_components, f_v, f_e;
+    const int32_t *e_row, *e_col; /* [n_edges] slice-local endpoints, row-major */
+    const int32_t* comp_off;      /* [n_components+1], comp_off[0] = 0 */
+    const int32_t* roots_local;   /* [n_components] */
+    const int32_t* l2g;           /* [n_vertices] */
+    const int32_t* e_gid;         /* [n_edges] */
+    const double *xv, *ye;        /* [n_vertices*f_v], [n_edges*f_e]; NULL without gather */
+    const uint8_t* lab;           /* [n_edges]; NULL without gather */
+} hgs_slice_views;
+
+/* slice_components(batch `batch` of the last run, components [begin, end)):
+ * HGS_EINVAL "slice_components: bad component range" as the reference.
+ * Enqueued on the handle's stream after one small synchronous read of the
+ * batch's offsets. */
+int hgs_sample_slice(hgs_sample* s, int64_t batch, int64_t begin, int64_t end, hgs_slice_views* out);
+
+/* Tape::gather_rows forward: out[i, :] = x[idx[i], :] for i < m (row-major
+ * fp64 with `cols` columns). An index outside [0, n_rows) is HGS_EINVAL
+ * "gather_rows: index <value> out of range" (the first in order; checked on
+ * the device, so the call synchronizes `stream`). stream: a cudaStream_t. */
+int hgs_gather_rows(const double* x, int64_t n_rows, int64_t cols, const int32_t* idx, int64_t m, double* out,
+                    void* stream);
+
+/* Tape::scatter_add: out[j, :] = sum of y[i, :] over i ascending with
+ * idx[i] == j, rows of out without an index are 0; accumulate != 0 adds onto
+ * out's current values in the same order (the backward of gather_rows,
+ * autodiff.cpp:260-270). A plan = stable sort of idx + per-row segment
+ * offsets, built once per index list (HGS_EINVAL "scatter_add: index
+ * <value> out of range") and reused by forward and backward passes. */
+typedef struct hgs_scatter_plan hgs_scatter_plan;
+int hgs_scatter_plan_create(int device, const int32_t* idx, int64_t m, int64_t n_rows, void* stream,
+                            hgs_scatter_plan** out);
+int hgs_scatter_add(const hgs_scatter_plan* plan, const double* y, int64_t cols, double* out, int32_t accumulate,
+                    void* stream);
+int hgs_scatter_plan_destroy(hgs_scatter_plan* plan);
+
+/* The reduction step of InMemoryComm::allreduce_mean: parts[q*n + e] is rank
+ * q's element e (q < w); out[e] = (parts[0][e] + ... + parts[w-1][e]) * (1/w)
+ * accumulated in rank order. The exchange around it (chunks to their owning
+ * rank, reduced chunks back to every rank) is NCCL's. */
+int hgs_ordered_mean(const double* parts, int32_t w, int64_t n, double* out, void* stream);
+
 /* ---- RNG helpers (host, no GPU needed) -------------------------------------- */
 uint64_t hgs_derive(uint64_t seed, const uint64_t* path, int32_t len);
 void hgs_philox4x32_10(const uint32_t ctr[4], const uint32_t key[2], uint32_t out[4]);

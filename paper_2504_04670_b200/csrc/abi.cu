@@ -43,6 +43,12 @@ int guarded(F&& f) {
     }
 }
 
+}  // namespace
+
+int hgs::abi_guard(const std::function<void()>& f) { return guarded(f); }
+
+namespace {
+
 void upload(void* dst, const void* src, size_t bytes, cudaStream_t st) {
     if (bytes) HGS_CUDA(cudaMemcpyAsync(dst, src, bytes, cudaMemcpyHostToDevice, st));
 }
@@ -559,6 +565,8 @@ int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
         in.state = rng_state ? s->rng_state.p : nullptr;
         in.R = R;
         in.k = n_batches;
+        s->last_in = in;  // device copies: hgs_sample_slice reads the batch offsets
+        s->last_cfg = *cfg;
         sample_enqueue(s, *cfg, in);
         sample_finish(s, *cfg, in);
     });

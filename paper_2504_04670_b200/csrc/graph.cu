@@ -189,8 +189,8 @@ __global__ void k_radix_scatter(const uint32_t* __restrict__ keys, const int32_t
 
 // Sorts (keys, vals) in place using the given temporaries; key_bits = number
 // of low bits that can be nonzero.
-static void radix_sort_pairs(uint32_t* keys, int32_t* vals, uint32_t* tkeys, int32_t* tvals,
-                             int64_t n, int key_bits, cudaStream_t st) {
+void radix_sort_pairs(uint32_t* keys, int32_t* vals, uint32_t* tkeys, int32_t* tvals, int64_t n, int key_bits,
+                      cudaStream_t st) {
     if (n <= 1) return;
     const int64_t tiles = (n + kSortTile - 1) / kSortTile;
     int32_t* hist = nullptr;

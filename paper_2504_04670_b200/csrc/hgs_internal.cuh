@@ -1,5 +1,6 @@
 // hgs_internal.cuh — device graph store, workspaces and shared device helpers.
 #pragma once
+#include <functional>
 #include <mutex>
 #include <cuda_runtime.h>
 #include <stdint.h>
@@ -157,6 +158,11 @@ void graph_ensure_recip(DevGraph& g, int32_t max_m);
 
 // Device exclusive scan: out[0..n] with out[n] = total (int32, total < 2^31).
 void scan_exclusive_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t st);
+// Stable LSD radix sort of (uint32 key, int32 value) pairs in place (graph.cu).
+void radix_sort_pairs(uint32_t* keys, int32_t* vals, uint32_t* tkeys, int32_t* tvals, int64_t n, int key_bits,
+                      cudaStream_t st);
+// Runs f with the C ABI's error convention (HGS_* code + hgs_last_error text).
+int abi_guard(const std::function<void()>& f);
 
 // ---- warp helpers -----------------------------------------------------------
 #if defined(__CUDACC__)
@@ -303,6 +309,8 @@ struct hgs_sample {
     cudaEvent_t ev[6] = {};
     int64_t launches = 0;     // kernels launched by the last run, re-runs included
     int64_t reruns = 0;       // capacity re-runs of the last run (0 in a steady state)
+    // slice_components outputs (hgs_sample_slice)
+    hgs::DevBuf<int32_t> sl_row, sl_col, sl_comp, sl_roots;
     // chunked pipeline: packing runs on a higher-priority side stream
     cudaStream_t aux = nullptr;
     std::vector<cudaEvent_t> chunk_ev;

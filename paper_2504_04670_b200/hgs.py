@@ -34,6 +34,8 @@ EXPORTS = [
     "hgs_sample_kernel_times", "hgs_sample_stats", "hgs_sample_launches", "hgs_derive", "hgs_philox4x32_10",
     "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind", "hgs_sample_copy_frontiers",
     "hgs_sample_rows", "hgs_sample_reruns",
+    "hgs_sample_slice", "hgs_gather_rows", "hgs_scatter_plan_create", "hgs_scatter_add",
+    "hgs_scatter_plan_destroy", "hgs_ordered_mean",
 ]
 
 
@@ -63,6 +65,14 @@ class DeviceViews(C.Structure):
                                             "root_voff", "root_eoff", "xv", "ye", "lab", "draws",
                                             "decisions", "touched", "touched_count",
                                             "level_counts")] + [("touched_stride", C.c_int64)]
+
+
+class SliceViews(C.Structure):
+    """hgs_slice_views: one slice_components result (device pointers)."""
+    _fields_ = [("n_vertices", C.c_int64), ("n_edges", C.c_int64), ("n_components", C.c_int64),
+                ("f_v", C.c_int64), ("f_e", C.c_int64)] + \
+               [(n, C.c_void_p) for n in ("e_row", "e_col", "comp_off", "roots_local", "l2g", "e_gid",
+                                            "xv", "ye", "lab")]
 
 
 class SeedSpec(C.Structure):
@@ -164,6 +174,12 @@ def lib() -> C.CDLL:
         L.hgs_event_save.argtypes = [C.c_char_p, i64, i64, vp, vp, vp, vp, i64, vp, i64, vp]
         L.hgs_event_info.argtypes = [C.c_char_p, vp]
         L.hgs_graph_load.argtypes = [C.c_int, C.c_char_p, C.POINTER(vp)]
+        L.hgs_sample_slice.argtypes = [vp, i64, i64, i64, C.POINTER(SliceViews)]
+        L.hgs_gather_rows.argtypes = [vp, i64, i64, vp, i64, vp, vp]
+        L.hgs_scatter_plan_create.argtypes = [C.c_int, vp, i64, i64, vp, C.POINTER(vp)]
+        L.hgs_scatter_add.argtypes = [vp, vp, i64, vp, i32, vp]
+        L.hgs_scatter_plan_destroy.argtypes = [vp]
+        L.hgs_ordered_mean.argtypes = [vp, i32, i64, vp, vp]
         _lib_cache = L
     return _lib_cache
 
@@ -247,6 +263,7 @@ class Graph:
         g = cls.__new__(cls)
         g.n, g.n_cols, g.nnz = info["n_rows"], info["n_cols"], info["nnz"]
         g.f_v, g.f_e = info["f_v"], info["f_e"]
+        g.device = device
         g._h = C.c_void_p()
         _check(lib().hgs_graph_load(device, os.fsencode(path), C.byref(g._h)))
         return g
@@ -258,6 +275,7 @@ class Graph:
         self.n = len(rp) - 1
         self.n_cols = self.n if n_cols is None else int(n_cols)
         self.nnz = int(rp[-1])
+        self.device = device
         self._h = C.c_void_p()
         _check(lib().hgs_graph_create(device, self.n, self.n_cols, _p(rp), _p(ci), _p(va),
                                       C.byref(self._h)))
@@ -388,6 +406,13 @@ class Sampler:
     def device_views(self) -> DeviceViews:
         v = DeviceViews()
         _check(lib().hgs_sample_device_views(self._h, C.byref(v)))
+        return v
+
+    def slice(self, batch: int, begin: int, end: int) -> SliceViews:
+        """slice_components (trainer.cpp:221-269) of batch `batch` of the last
+        run on the device: see paper_2504_04670_b200.consumer."""
+        v = SliceViews()
+        _check(lib().hgs_sample_slice(self._h, batch, begin, end, C.byref(v)))
         return v
 
     def kernel_times(self) -> np.ndarray:

@@ -1,7 +1,7 @@
 """Small sampling calls for compute-sanitizer (memcheck / racecheck / synccheck /
 initcheck): K0, K1 (serial, Philox group, xoshiro group), K2 (hash-set,
-directory and bitmap-directory variants), offset scan, K3 pack + gathers, the standalone gather and
-the ingest kernels, each checked against the oracle.
+directory and bitmap-directory variants), offset scan, K3 pack + gathers, the standalone gather,
+the ingest kernels and the consumer kernels, each checked against the oracle.
 usage: compute-sanitizer --tool <tool> python scripts/sanitize_case.py"""
 import os
 import sys
@@ -32,6 +32,29 @@ for env in ({}, {"HGS_K2": "dir"}, {"HGS_K2": "bm"}, {"HGS_K1_GROUPX": "1"}):
     S.close()
     for k in env:
         del os.environ[k]
+# consumer kernels (slice_components, gather_rows / scatter_add, ordered mean) on the last run
+import torch  # noqa: E402
+from oracle import consumer as CO  # noqa: E402
+from paper_2504_04670_b200 import consumer  # noqa: E402
+S = hgs.Sampler(G)
+S.bulk_shadow(roots, boff, seeds, rng=0, depth=2, fanout=5, gather=True)
+ref = O.bulk_shadow(g, roots, boff, seeds, rng=0, depth=2, fanout=5, gather=True)
+sl = consumer.slice_components(S, 1, 7, 40)
+want = CO.slice_components(CO.batch_of(ref, boff, 1, 6, 2), 7, 40)
+plan = consumer.ScatterPlan(sl.e_col, sl.n_vertices)
+ok = np.array_equal(sl.e_col.cpu().numpy(), want["e_col"])
+ok &= np.array_equal(consumer.scatter_add(sl.edge_features, plan).cpu().numpy().view(np.uint64),
+                     CO.scatter_add(want["ye"], want["e_col"], sl.n_vertices).view(np.uint64))
+ok &= np.array_equal(consumer.gather_rows(sl.node_features, sl.e_row).cpu().numpy().view(np.uint64),
+                     CO.gather_rows(want["xv"], want["e_row"]).view(np.uint64))
+parts = np.random.default_rng(1).standard_normal((3, 100))
+ok &= np.array_equal(consumer.ordered_mean(torch.as_tensor(parts, device="cuda")).cpu().numpy().view(np.uint64),
+                     CO.allreduce_mean(parts).view(np.uint64))
+torch.cuda.synchronize()
+plan.close()
+S.close()
+bad += not ok
+print("consumer", "ok" if ok else "MISMATCH", flush=True)
 xv, ye, lab = np.zeros(10 * 6), np.zeros(10 * 2), np.zeros(10, np.uint8)
 out = hgs.lib().hgs_graph_gather(G._h, hgs._p(np.arange(10, dtype=np.int64)), 10,
                                  hgs._p(np.arange(10, dtype=np.int64)), 10, hgs._p(xv), hgs._p(ye), hgs._p(lab))
