@@ -12,8 +12,13 @@ want = ["Duration", "DRAM Throughput", "Memory Throughput", "L1/TEX Cache Throug
         "Dynamic Shared Memory Per Block", "Grid Size", "Block Size"]
 r = csv.reader(io.StringIO(run(["--page", "details", "--csv"])))
 hdr = next(r)
+cur = None
 for row in r:
     d = dict(zip(hdr, row))
+    k = (d.get("ID"), d.get("Kernel Name"))
+    if k != cur and d.get("Kernel Name"):
+        cur = k
+        print(f"== [{d.get('ID')}] {d.get('Kernel Name')[:100]}")
     if d.get("Metric Name") in want:
         print(f"  {d['Metric Name']:40s} {d['Metric Value']:>16s} {d['Metric Unit']}")
 raw = run(["--page", "raw", "--csv"])

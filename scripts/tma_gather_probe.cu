@@ -1,0 +1,153 @@
+// tma_gather_probe.cu — microbenchmark for the node-row gather of K3
+// (gather_features, sampler.cpp:211-243): out[i] = table[idx[i]] for 48-byte
+// fp64 rows (f_v = 6) from an L2-resident table, V = 14.3M rows (C2).
+//   A: the product kernel's scheme (k_gather_nodes): 16-byte pieces, adjacent
+//      threads on adjacent pieces, streaming stores.
+//   B: bulk-async copies (cp.async.bulk, the TMA's non-tensor path): one
+//      48-byte global->shared copy per row into a 64-row tile, an mbarrier
+//      with the tile's byte count, then one bulk shared->global store of the
+//      3 KB tile; STAGES tiles in flight per CTA.
+// usage: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/tg scripts/tma_gather_probe.cu && /tmp/tg
+#include <cuda_runtime.h>
+
+#include <cstdint>
+#include <cstdio>
+#include <cstdlib>
+#include <vector>
+
+#define CK(x)                                                                        \
+    do {                                                                             \
+        cudaError_t e = (x);                                                         \
+        if (e != cudaSuccess) {                                                      \
+            printf("CUDA %s at %s:%d\n", cudaGetErrorString(e), __FILE__, __LINE__); \
+            exit(1);                                                                 \
+        }                                                                            \
+    } while (0)
+
+__global__ void __launch_bounds__(256) k_pieces(const uint4* __restrict__ tab, const int32_t* __restrict__ idx,
+                                                int64_t V, uint4* __restrict__ out) {
+    const int64_t n = V * 3, stride = (int64_t)gridDim.x * blockDim.x;
+    for (int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; e < n; e += stride) {
+        const int64_t i = (int64_t)__umulhi((unsigned)e, 1431655766u);  // e / 3 (exact for e < 2^31)
+        __stcs(out + e, __ldg(tab + (int64_t)__ldg(idx + i) * 3 + (e - i * 3)));
+    }
+}
+
+constexpr int TILE = 64, ROWB = 48;
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) { return (uint32_t)__cvta_generic_to_shared(p); }
+
+template <int STAGES>
+__global__ void __launch_bounds__(128) k_bulk(const char* __restrict__ tab, const int32_t* __restrict__ idx, int64_t V,
+                                              char* __restrict__ out) {
+    __shared__ __align__(128) char buf[STAGES][TILE * ROWB];
+    __shared__ __align__(8) uint64_t bar[STAGES];
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        for (int s = 0; s < STAGES; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    __syncthreads();
+    const int64_t tiles = (V + TILE - 1) / TILE;
+    uint32_t phase[STAGES] = {};
+    int64_t t0 = blockIdx.x;
+    const int64_t step = gridDim.x;
+    auto issue = [&](int s, int64_t t) {
+        const int64_t base = t * TILE;
+        const int rows = (int)(V - base < TILE ? V - base : TILE);
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])),
+                         "r"(rows * ROWB));
+        __syncwarp();
+        if (tid < rows) {
+            const char* src = tab + (int64_t)__ldg(idx + base + tid) * ROWB;
+            asm volatile(
+                "cp.async.bulk.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1], %2, [%3];" ::"r"(
+                    smem_u32(buf[s] + tid * ROWB)),
+                "l"(src), "r"(ROWB), "r"(smem_u32(&bar[s]))
+                : "memory");
+        }
+    };
+    // prologue
+    for (int s = 0; s < STAGES; ++s)
+        if (t0 + s * step < tiles) issue(s, t0 + s * step);
+    for (int64_t t = t0, k = 0; t < tiles; t += step, ++k) {
+        const int s = (int)(k % STAGES);
+        // wait for the tile's rows
+        asm volatile(
+            "{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+                smem_u32(&bar[s])),
+            "r"(phase[s]));
+        phase[s] ^= 1;
+        const int64_t base = t * TILE;
+        const int rows = (int)(V - base < TILE ? V - base : TILE);
+        if (tid == 0) {
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(out + base * ROWB),
+                         "r"(smem_u32(buf[s])), "r"(rows * ROWB)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");  // slot reusable
+        }
+        __syncthreads();
+        const int64_t tn = t + (int64_t)STAGES * step;
+        if (tn < tiles) issue(s, tn);
+    }
+    if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
+int main() {
+    const int64_t n = 120373, V = 14330269;
+    std::vector<double> h(n * 6);
+    for (size_t i = 0; i < h.size(); ++i) h[i] = (double)i;
+    std::vector<int32_t> hi(V);
+    uint64_t x = 88172645463325252ull;
+    for (int64_t i = 0; i < V; ++i) {
+        x ^= x << 13; x ^= x >> 7; x ^= x << 17;
+        hi[i] = (int32_t)(x % n);
+    }
+    double *tab, *o1, *o2;
+    int32_t* idx;
+    char* flush;
+    CK(cudaMalloc(&tab, n * 48));
+    CK(cudaMalloc(&idx, V * 4));
+    CK(cudaMalloc(&o1, V * 48));
+    CK(cudaMalloc(&o2, V * 48));
+    CK(cudaMalloc(&flush, 512 << 20));
+    CK(cudaMemcpy(tab, h.data(), n * 48, cudaMemcpyHostToDevice));
+    CK(cudaMemcpy(idx, hi.data(), V * 4, cudaMemcpyHostToDevice));
+    cudaEvent_t a, b;
+    cudaEventCreate(&a);
+    cudaEventCreate(&b);
+    auto timeit = [&](const char* name, auto launch) {
+        float best = 1e9;
+        for (int r = 0; r < 6; ++r) {
+            CK(cudaMemset(flush, r, 512 << 20));
+            cudaEventRecord(a);
+            launch();
+            cudaEventRecord(b);
+            CK(cudaEventSynchronize(b));
+            float ms;
+            cudaEventElapsedTime(&ms, a, b);
+            if (r) best = ms < best ? ms : best;
+        }
+        printf("%-28s %.4f ms  %.0f GB/s (out write)\n", name, best, V * 48 / best / 1e6);
+    };
+    timeit("A pieces (k_gather_nodes)", [&] {
+        k_pieces<<<148 * 8, 256>>>((const uint4*)tab, idx, V, (uint4*)o1);
+    });
+    CK(cudaGetLastError());
+    timeit("B bulk 2 stages", [&] { k_bulk<2><<<148 * 8, 128>>>((const char*)tab, idx, V, (char*)o2); });
+    CK(cudaGetLastError());
+    CK(cudaDeviceSynchronize());
+    std::vector<double> r1(V * 6), r2(V * 6);
+    CK(cudaMemcpy(r1.data(), o1, V * 48, cudaMemcpyDeviceToHost));
+    CK(cudaMemcpy(r2.data(), o2, V * 48, cudaMemcpyDeviceToHost));
+    bool ok = true;
+    for (int64_t i = 0; i < V * 6 && ok; ++i) ok = r1[i] == r2[i] && r1[i] == h[(int64_t)hi[i / 6] * 6 + i % 6];
+    printf("outputs %s\n", ok ? "equal" : "DIFFER");
+    timeit("B bulk 4 stages", [&] { k_bulk<4><<<148 * 4, 128>>>((const char*)tab, idx, V, (char*)o2); });
+    timeit("B bulk 4 stages x8", [&] { k_bulk<4><<<148 * 8, 128>>>((const char*)tab, idx, V, (char*)o2); });
+    timeit("B bulk 8 stages", [&] { k_bulk<8><<<148 * 4, 128>>>((const char*)tab, idx, V, (char*)o2); });
+    CK(cudaGetLastError());
+    return 0;
+}
