@@ -7,8 +7,13 @@
 //      48-byte global->shared copy per row into a 64-row tile, an mbarrier
 //      with the tile's byte count, then one bulk shared->global store of the
 //      3 KB tile; STAGES tiles in flight per CTA.
+//   C: TMA gather4 (cp.async.bulk.tensor.2d...tile::gather4, sm_100a): one
+//      tensor op brings 4 rows of a 2D tensor map [n][6] fp64 into shared
+//      memory; 16 ops per 64-row tile, then the same bulk tile store.
 // usage: nvcc -gencode arch=compute_100a,code=sm_100a -O3 -o /tmp/tg scripts/tma_gather_probe.cu && /tmp/tg
+#include <cuda.h>
 #include <cuda_runtime.h>
+#include <cudaTypedefs.h>
 
 #include <cstdint>
 #include <cstdio>
@@ -95,6 +100,59 @@ __global__ void __launch_bounds__(128) k_bulk(const char* __restrict__ tab, cons
     if (tid == 0) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
 }
 
+template <int STAGES>
+__global__ void __launch_bounds__(128) k_gather4(const __grid_constant__ CUtensorMap tmap, const int32_t* __restrict__ idx,
+                                                 int64_t V, char* __restrict__ out) {
+    __shared__ __align__(128) char buf[STAGES][TILE / 4 * 256];  // tensor copies land 128-byte aligned: 4 rows per 256-byte slot
+    __shared__ __align__(8) uint64_t bar[STAGES];
+    const int tid = threadIdx.x;
+    if (tid == 0)
+        for (int s = 0; s < STAGES; ++s)
+            asm volatile("mbarrier.init.shared::cta.b64 [%0], 1;" ::"r"(smem_u32(&bar[s])));
+    asm volatile("fence.mbarrier_init.release.cluster;");
+    __syncthreads();
+    const int64_t tiles = V / TILE;  // full tiles only (the probe's V tail is ignored)
+    uint32_t phase[STAGES] = {};
+    const int64_t t0 = blockIdx.x, step = gridDim.x;
+    auto issue = [&](int s, int64_t t) {
+        const int64_t base = t * TILE;
+        if (tid == 0)
+            asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(&bar[s])),
+                         "r"(TILE * ROWB));
+        __syncwarp();
+        if (tid < TILE / 4) {
+            const int4 r = *reinterpret_cast<const int4*>(idx + base + 4 * tid);
+            asm volatile(
+                "cp.async.bulk.tensor.2d.shared::cta.global.tile::gather4.mbarrier::complete_tx::bytes"
+                " [%0], [%1, {%2, %3, %4, %5, %6}], [%7];" ::"r"(smem_u32(buf[s] + tid * 256)),
+                "l"(&tmap), "r"(0), "r"(r.x), "r"(r.y), "r"(r.z), "r"(r.w), "r"(smem_u32(&bar[s]))
+                : "memory");
+        }
+    };
+    for (int s = 0; s < STAGES; ++s)
+        if (t0 + s * step < tiles) issue(s, t0 + s * step);
+    for (int64_t t = t0, k = 0; t < tiles; t += step, ++k) {
+        const int s = (int)(k % STAGES);
+        asm volatile(
+            "{ .reg .pred p; W: mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1; @!p bra W; }" ::"r"(
+                smem_u32(&bar[s])),
+            "r"(phase[s]));
+        phase[s] ^= 1;
+        if (tid < TILE / 4) {  // one 192-byte store per 4-row group
+            asm volatile("cp.async.bulk.global.shared::cta.bulk_group [%0], [%1], %2;" ::"l"(
+                             out + (t * TILE + 4 * tid) * ROWB),
+                         "r"(smem_u32(buf[s] + tid * 256)), "r"(4 * ROWB)
+                         : "memory");
+            asm volatile("cp.async.bulk.commit_group;");
+            asm volatile("cp.async.bulk.wait_group.read 0;" ::: "memory");
+        }
+        __syncthreads();
+        const int64_t tn = t + (int64_t)STAGES * step;
+        if (tn < tiles) issue(s, tn);
+    }
+    if (tid < TILE / 4) asm volatile("cp.async.bulk.wait_group 0;" ::: "memory");
+}
+
 int main() {
     const int64_t n = 120373, V = 14330269;
     std::vector<double> h(n * 6);
@@ -148,6 +206,35 @@ int main() {
     timeit("B bulk 4 stages", [&] { k_bulk<4><<<148 * 4, 128>>>((const char*)tab, idx, V, (char*)o2); });
     timeit("B bulk 4 stages x8", [&] { k_bulk<4><<<148 * 8, 128>>>((const char*)tab, idx, V, (char*)o2); });
     timeit("B bulk 8 stages", [&] { k_bulk<8><<<148 * 4, 128>>>((const char*)tab, idx, V, (char*)o2); });
+    timeit("B bulk 2 stages x16", [&] { k_bulk<2><<<148 * 16, 128>>>((const char*)tab, idx, V, (char*)o2); });
+    timeit("B bulk 2 stages x32", [&] { k_bulk<2><<<148 * 32, 128>>>((const char*)tab, idx, V, (char*)o2); });
     CK(cudaGetLastError());
+    // C: gather4 through a 2D tensor map [n][6] fp64, box {6, 1}
+    PFN_cuTensorMapEncodeTiled_v12000 encode = nullptr;
+    cudaDriverEntryPointQueryResult qr;
+    CK(cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", (void**)&encode, cudaEnableDefault, &qr));
+    CUtensorMap tmap;
+    cuuint64_t dims[2] = {6, (cuuint64_t)n};
+    cuuint64_t strides[1] = {48};
+    cuuint32_t box[2] = {6, 1}, estr[2] = {1, 1};
+    CUresult cr = encode(&tmap, CU_TENSOR_MAP_DATA_TYPE_FLOAT64, 2, tab, dims, strides, box, estr,
+                         CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_NONE, CU_TENSOR_MAP_L2_PROMOTION_L2_128B,
+                         CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+    printf("tensor map encode: %d\n", (int)cr);
+    CK(cudaMemset(o2, 0, V * 48));
+    for (int sts : {2, 4}) {
+        for (int per : {8, 16, 32}) {
+            char name[64];
+            snprintf(name, sizeof name, "C gather4 %d stages x%d", sts, per);
+            if (sts == 2) timeit(name, [&] { k_gather4<2><<<148 * per, 128>>>(tmap, idx, V, (char*)o2); });
+            else timeit(name, [&] { k_gather4<4><<<148 * per, 128>>>(tmap, idx, V, (char*)o2); });
+            CK(cudaGetLastError());
+        }
+    }
+    CK(cudaDeviceSynchronize());
+    CK(cudaMemcpy(r2.data(), o2, V * 48, cudaMemcpyDeviceToHost));
+    ok = true;
+    for (int64_t i = 0; i < (V / TILE) * TILE * 6 && ok; ++i) ok = r1[i] == r2[i];
+    printf("gather4 outputs %s\n", ok ? "equal" : "DIFFER");
     return 0;
 }
