@@ -2,7 +2,7 @@
 // sampling pipeline. Host work here is input validation with the reference's
 // error semantics, graph ingest (int64 -> int32 narrowing, explicit-zero and
 // negative-value bookkeeping) and host<->device copies; all sampling
-// arithmetic runs in the kernels of sampler.cu / graph.cu.
+// arithmetic runs in the kernels (graph.cu, expand.cu, extract*.cu, consumer.cu).
 #include <cuda_runtime.h>
 
 #include <fcntl.h>

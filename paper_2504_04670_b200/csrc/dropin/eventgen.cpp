@@ -5,7 +5,9 @@
 // random-call sequence, geometry, false-edge candidate rule, 90th-percentile
 // distance cut, shuffle, truncation, canonical edge order and features, so
 // the produced EventGraph is bit-identical (checked against the compiled
-// reference in tests/test_eventgen.py). The one algorithmic change is the
+// reference in tests/test_abi.py::test_generator_matches_reference_digest and
+// _presets, and at C2 size in tests/test_gpu_bench_parity.py). The one
+// algorithmic change is the
 // false-edge candidate search: the reference scans all pairs of adjacent
 // layers (O(|L_i|·|L_{i+1}|), 3 GB and 30 s at 120k hits); here each inner hit
 // binary-searches the phi window of the phi-sorted outer layer and tests the
