@@ -23,3 +23,10 @@ def shard(roots: np.ndarray, batch_off: np.ndarray, seeds: np.ndarray, rank: int
     b0, b1 = batch_range(k, rank, world)
     r0, r1 = int(batch_off[b0]), int(batch_off[b1])
     return roots[r0:r1], batch_off[b0:b1 + 1] - r0, seeds[r0:r1]
+
+
+def worker_component_range(n_components: int, rank: int, world: int) -> tuple[int, int]:
+    """The contiguous component range rank r of world owns within one batch
+    (trainer.cpp:214-219), the slice the reference's DDP worker trains on
+    (slice_components, trainer.cpp:342-343)."""
+    return n_components * rank // world, n_components * (rank + 1) // world
