@@ -244,6 +244,47 @@ def measure_ingest(ev, device) -> dict:
             "path": "hgs_event_save file -> hgs_graph_load (mmap, device narrowing/validation, features) + K0 walk"}
 
 
+def measure_consumer(S, k: int) -> dict:
+    """The training step's device-side use of the last call's batches
+    (SURVEY §8f #3): per minibatch slice_components (the whole batch), scatter
+    plans for the row and column lists, the four IGNN message-passing ops of
+    ignn.cpp:158-164 on the gathered features (x by rows / cols, y into rows /
+    cols), then the rank-ordered reduction of a gradient-sized buffer. Wall
+    clock with a device sync; slices include their small host reads."""
+    import torch
+    from paper_2504_04670_b200 import consumer as C
+    torch.cuda.synchronize()
+    t0 = time.perf_counter()
+    nbytes = 0
+    for b in range(k):
+        sl = C.slice_components(S, b, 0, int(S.batch_components(b)))
+        prow, pcol = C.ScatterPlan(sl.e_row, sl.n_vertices), C.ScatterPlan(sl.e_col, sl.n_vertices)
+        x, y = sl.node_features, sl.edge_features
+        for t in (C.gather_rows_planned(x, prow), C.gather_rows_planned(x, pcol), C.scatter_add(y, prow),
+                  C.scatter_add(y, pcol)):
+            nbytes += 2 * t.numel() * 8
+        prow.close()
+        pcol.close()
+    torch.cuda.synchronize()
+    t1 = time.perf_counter()
+    parts = torch.randn(8, 1 << 20, dtype=torch.float64, device="cuda")
+    C.ordered_mean(parts)
+    torch.cuda.synchronize()
+    e0, e1 = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    e0.record()
+    for _ in range(10):
+        C.ordered_mean(parts)
+    e1.record()
+    torch.cuda.synchronize()
+    om = e0.elapsed_time(e1) / 10
+    return {"ms_per_minibatch": (t1 - t0) * 1e3 / k, "minibatches": k,
+            "gather_scatter_gbs": nbytes / (t1 - t0) / 1e9,
+            "ordered_mean_8x1M_ms": om, "ordered_mean_gbs": 9 * (1 << 20) * 8 / (om / 1e3) / 1e9,
+            "path": "consumer.slice_components + 2 ScatterPlans + gather_rows_planned(x, rows/cols) + scatter_add(y, rows/cols) "
+                    "per minibatch of the last e2e call (wall, incl. plan builds and slice host reads); "
+                    "hgs_ordered_mean over 8 ranks x 1M doubles (CUDA events)"}
+
+
 def distinct_devices(world, dev) -> int:
     """Number of distinct physical GPUs the ranks run on (device UUIDs). A
     multi-rank line is only printed when every rank has its own GPU; the
@@ -421,6 +462,9 @@ def run_gpu(args, world, rank, local_rank):
                            "features out, wall clock: device_event = gpu::DeviceEvent::bulk_shadow(gather); "
                            "trainer_two_lines = hitgnn::bulk_shadow(edge-id A) + gather_features per batch "
                            "(trainer.cpp:457-458) through the resident-graph cache")
+    consumer_leg = None
+    if rank == 0 and world == 1 and WORKLOAD in ("C1", "C2") and cfg.get("gather"):
+        consumer_leg = measure_consumer(S, K_BATCHES)
     if rank != 0:
         return
     mb = world * K_BATCHES * args.steps
@@ -478,6 +522,8 @@ def run_gpu(args, world, rank, local_rank):
         line["e2e_cpp"] = e2e_cpp
     if ingest:
         line["ingest"] = ingest
+    if consumer_leg:
+        line["consumer"] = consumer_leg
     if world == 1 and not args.no_cpu_baseline:
         # (i) all host threads on the call's own shape (K_BATCHES minibatches,
         # contiguous batch ranges per thread); (ii) one thread, the reference as

@@ -313,6 +313,12 @@ int hgs_scatter_plan_create(int device, const int32_t* idx, int64_t m, int64_t n
 int hgs_scatter_add(const hgs_scatter_plan* plan, const double* y, int64_t cols, double* out, int32_t accumulate,
                     void* stream);
 int hgs_scatter_plan_destroy(hgs_scatter_plan* plan);
+/* gather_rows over a plan's (already validated) index list: no range check,
+ * no synchronisation. The index list must outlive the plan; a non-decreasing
+ * list (e.g. a batch's rows) is planned without a sort. Plans and their
+ * buffers are stream-ordered on the stream they were created on. */
+int hgs_gather_rows_planned(const hgs_scatter_plan* plan, const double* x, int64_t n_rows, int64_t cols, double* out,
+                            void* stream);
 
 /* The reduction step of InMemoryComm::allreduce_mean: parts[q*n + e] is rank
  * q's element e (q < w); out[e] = (parts[0][e] + ... + parts[w-1][e]) * (1/w)

@@ -115,7 +115,9 @@ def gather_rows(x: torch.Tensor, idx: torch.Tensor) -> torch.Tensor:
 
 class ScatterPlan:
     """Stable sort of an index list + per-destination segments (built once,
-    used by scatter_add and by the backward of gather_rows)."""
+    used by scatter_add, by gather_rows_planned and by the backward passes).
+    The indices are range-checked once here; a non-decreasing list (a batch's
+    rows) needs no sort. Buffers are stream-ordered on the current stream."""
 
     def __init__(self, idx: torch.Tensor, n_rows: int):
         _need_cuda(idx)
@@ -136,6 +138,18 @@ class ScatterPlan:
             self.close()
         except Exception:
             pass
+
+
+def gather_rows_planned(x: torch.Tensor, plan: ScatterPlan) -> torch.Tensor:
+    """gather_rows(x, plan.idx) without a second range check or host sync
+    (x must have plan.n_rows rows)."""
+    _need_cuda(x)
+    x = x.contiguous()
+    cols = x.shape[1] if x.dim() == 2 else 1
+    out = torch.empty((plan.idx.numel(), cols), dtype=torch.float64, device=x.device)
+    hgs._check(hgs.lib().hgs_gather_rows_planned(plan._h, C.c_void_p(x.data_ptr()), x.shape[0], cols,
+                                                 C.c_void_p(out.data_ptr()), _stream(x)))
+    return out
 
 
 def scatter_add(y: torch.Tensor, plan: ScatterPlan, out: torch.Tensor | None = None,
@@ -163,7 +177,7 @@ class GatherRows(torch.autograd.Function):
     @staticmethod
     def forward(ctx, x, idx, plan):
         ctx.plan = plan
-        return gather_rows(x, idx)
+        return gather_rows_planned(x, plan) if plan.n_rows == x.shape[0] else gather_rows(x, idx)
 
     @staticmethod
     def backward(ctx, g):
@@ -181,7 +195,7 @@ class ScatterAdd(torch.autograd.Function):
 
     @staticmethod
     def backward(ctx, g):
-        return gather_rows(g, ctx.plan.idx), None
+        return gather_rows_planned(g, ctx.plan), None
 
 
 def ordered_mean(parts: torch.Tensor) -> torch.Tensor:

@@ -19,6 +19,7 @@
 #include <cuda_runtime.h>
 
 #include <algorithm>
+#include <mutex>
 #include <string>
 
 #include "kernels.cuh"
@@ -26,8 +27,10 @@
 struct hgs_scatter_plan {
     int device = 0;
     int64_t m = 0, n_rows = 0;
-    hgs::DevBuf<int32_t> perm;  // positions of idx, stably sorted by destination
-    hgs::DevBuf<int32_t> seg;   // [n_rows + 1] segment offsets into perm
+    const int32_t* idx = nullptr;  // the caller's index list (must outlive the plan)
+    int32_t* perm = nullptr;       // positions of idx, stably sorted by destination (stream-ordered pool)
+    int32_t* seg = nullptr;        // [n_rows + 1] segment offsets into perm
+    cudaStream_t stream = nullptr;
 };
 
 namespace hgs {
@@ -49,11 +52,32 @@ __global__ void k_slice(const int32_t* __restrict__ e_row, const int32_t* __rest
     }
 }
 
-// first position i with idx[i] outside [0, n) (atomicMin over positions)
+// first position i with idx[i] outside [0, n) (atomicMin over positions);
+// first[1] != 0 when the list is not non-decreasing
 __global__ void k_first_bad(const int32_t* __restrict__ idx, int64_t m, int64_t n,
                             unsigned long long* __restrict__ first) {
+    for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x) {
+        const int32_t v = idx[i];
+        if (v < 0 || v >= n) atomicMin(first, (unsigned long long)i);
+        if (i + 1 < m && idx[i + 1] < v) first[1] = 1ull;
+    }
+}
+
+__global__ void k_iota(int32_t* __restrict__ p, int64_t m) {
     for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < m; i += (int64_t)gridDim.x * blockDim.x)
-        if (idx[i] < 0 || idx[i] >= n) atomicMin(first, (unsigned long long)i);
+        p[i] = (int32_t)i;
+}
+
+// seg[j] = first position with idx >= j over a non-decreasing index list
+__global__ void k_segments_i32(const int32_t* __restrict__ sorted, int64_t m, int64_t n, int32_t* __restrict__ seg) {
+    for (int64_t j = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; j <= n; j += (int64_t)gridDim.x * blockDim.x) {
+        int64_t lo = 0, hi = m;
+        while (lo < hi) {
+            const int64_t mid = (lo + hi) >> 1;
+            if ((int64_t)sorted[mid] < j) lo = mid + 1; else hi = mid;
+        }
+        seg[j] = (int32_t)lo;
+    }
 }
 
 __global__ void k_gather_rows(const double* __restrict__ x, int64_t cols, const int32_t* __restrict__ idx,
@@ -117,23 +141,42 @@ __global__ void k_ordered_mean(const double* __restrict__ parts, int32_t w, int6
     }
 }
 
+// The stream-ordered pool trims its memory back to the driver at every
+// synchronisation by default (release threshold 0), which turns each
+// cudaMallocAsync after a sync into a driver allocation; the consumer's
+// small per-batch plans keep the memory instead.
+void pool_keep(int device) {
+    static std::once_flag once[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(once[device], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
 unsigned grid_for(int64_t work) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 16));
 }
 
-// First out-of-range index, or -1 (synchronizes st).
-int64_t first_bad_index(const int32_t* idx, int64_t m, int64_t n, cudaStream_t st) {
+// First out-of-range index, or -1 (synchronizes st); *sorted = non-decreasing.
+int64_t first_bad_index(const int32_t* idx, int64_t m, int64_t n, cudaStream_t st, bool* sorted = nullptr) {
+    if (sorted) *sorted = true;
     if (m <= 0) return -1;
     unsigned long long* d = nullptr;
-    HGS_CUDA(cudaMallocAsync(&d, sizeof(unsigned long long), st));
+    HGS_CUDA(cudaMallocAsync(&d, 2 * sizeof(unsigned long long), st));
     HGS_CUDA(cudaMemsetAsync(d, 0xff, sizeof(unsigned long long), st));
+    HGS_CUDA(cudaMemsetAsync(d + 1, 0, sizeof(unsigned long long), st));
     k_first_bad<<<grid_for(m), 256, 0, st>>>(idx, m, n, d);
     HGS_CUDA(cudaGetLastError());
-    unsigned long long h = 0;
-    HGS_CUDA(cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
+    unsigned long long h[2] = {0, 0};
+    HGS_CUDA(cudaMemcpyAsync(h, d, sizeof(h), cudaMemcpyDeviceToHost, st));
     HGS_CUDA(cudaFreeAsync(d, st));
     HGS_CUDA(cudaStreamSynchronize(st));
-    return h == ~0ULL ? -1 : (int64_t)h;
+    if (sorted) *sorted = h[1] == 0;
+    return h[0] == ~0ULL ? -1 : (int64_t)h[0];
 }
 
 int32_t read_i32(const int32_t* p, cudaStream_t st) {
@@ -203,6 +246,9 @@ int hgs_gather_rows(const double* x, int64_t n_rows, int64_t cols, const int32_t
     return abi_guard([&] {
         if (m < 0 || cols < 0 || n_rows < 0) fail(HGS_EINVAL, "gather_rows: negative size");
         cudaStream_t st = (cudaStream_t)stream;
+        int dev = 0;
+        HGS_CUDA(cudaGetDevice(&dev));
+        pool_keep(dev);
         const int64_t bad = first_bad_index(idx, m, n_rows, st);
         if (bad >= 0)
             fail(HGS_EINVAL, "gather_rows: index " + std::to_string(read_i32(idx + bad, st)) + " out of range");
@@ -219,35 +265,41 @@ int hgs_scatter_plan_create(int device, const int32_t* idx, int64_t m, int64_t n
         if (m < 0 || n_rows < 0 || m >= ((int64_t)1 << 31) || n_rows >= ((int64_t)1 << 31))
             fail(HGS_ERANGE, "scatter_add: sizes beyond 2^31 are not supported by this build");
         HGS_CUDA(cudaSetDevice(device));
+        pool_keep(device);
         cudaStream_t st = (cudaStream_t)stream;
-        const int64_t bad = first_bad_index(idx, m, n_rows, st);
+        bool sorted = true;
+        const int64_t bad = first_bad_index(idx, m, n_rows, st, &sorted);
         if (bad >= 0)
             fail(HGS_EINVAL, "scatter_add: index " + std::to_string(read_i32(idx + bad, st)) + " out of range");
         auto* p = new hgs_scatter_plan();
         p->device = device;
         p->m = m;
         p->n_rows = n_rows;
-        try {
-            p->perm.reserve((size_t)std::max<int64_t>(m, 1));
-            p->seg.reserve((size_t)n_rows + 1);
-            DevBuf<uint32_t> keys, tkeys;
-            DevBuf<int32_t> tvals;
-            keys.reserve((size_t)std::max<int64_t>(m, 1));
-            tkeys.reserve((size_t)std::max<int64_t>(m, 1));
-            tvals.reserve((size_t)std::max<int64_t>(m, 1));
-            if (m > 0) {
-                k_iota_keys<<<grid_for(m), 256, 0, st>>>(idx, m, keys.p, p->perm.p);
-                int bits = 1;
-                while (bits < 32 && ((int64_t)1 << bits) < n_rows) ++bits;
-                radix_sort_pairs(keys.p, p->perm.p, tkeys.p, tvals.p, m, bits, st);
-            }
-            k_segments<<<grid_for(n_rows + 1), 256, 0, st>>>(keys.p, m, n_rows, p->seg.p);
-            HGS_CUDA(cudaGetLastError());
-            HGS_CUDA(cudaStreamSynchronize(st));  // temporaries are freed on return
-        } catch (...) {
-            delete p;
-            throw;
+        p->idx = idx;
+        p->stream = st;
+        // plan buffers and temporaries come from the stream-ordered pool: no
+        // cudaMalloc / device-wide synchronisation per plan
+        HGS_CUDA(cudaMallocAsync(&p->perm, sizeof(int32_t) * (size_t)std::max<int64_t>(m, 1), st));
+        HGS_CUDA(cudaMallocAsync(&p->seg, sizeof(int32_t) * (size_t)(n_rows + 1), st));
+        if (sorted) {  // e.g. the row list of a batch (CSR order): identity permutation
+            if (m > 0) k_iota<<<grid_for(m), 256, 0, st>>>(p->perm, m);
+            k_segments_i32<<<grid_for(n_rows + 1), 256, 0, st>>>(idx, m, n_rows, p->seg);
+        } else {
+            uint32_t *keys = nullptr, *tkeys = nullptr;
+            int32_t* tvals = nullptr;
+            HGS_CUDA(cudaMallocAsync(&keys, sizeof(uint32_t) * (size_t)m, st));
+            HGS_CUDA(cudaMallocAsync(&tkeys, sizeof(uint32_t) * (size_t)m, st));
+            HGS_CUDA(cudaMallocAsync(&tvals, sizeof(int32_t) * (size_t)m, st));
+            k_iota_keys<<<grid_for(m), 256, 0, st>>>(idx, m, keys, p->perm);
+            int bits = 1;
+            while (bits < 32 && ((int64_t)1 << bits) < n_rows) ++bits;
+            radix_sort_pairs(keys, p->perm, tkeys, tvals, m, bits, st);
+            k_segments<<<grid_for(n_rows + 1), 256, 0, st>>>(keys, m, n_rows, p->seg);
+            HGS_CUDA(cudaFreeAsync(keys, st));
+            HGS_CUDA(cudaFreeAsync(tkeys, st));
+            HGS_CUDA(cudaFreeAsync(tvals, st));
         }
+        HGS_CUDA(cudaGetLastError());
         *out = p;
     });
 }
@@ -260,8 +312,23 @@ int hgs_scatter_add(const hgs_scatter_plan* plan, const double* y, int64_t cols,
         if (plan->n_rows * cols == 0) return;
         HGS_CUDA(cudaSetDevice(plan->device));
         cudaStream_t st = (cudaStream_t)stream;
-        k_scatter<<<grid_for(plan->n_rows * cols), 256, 0, st>>>(y, cols, plan->perm.p, plan->seg.p, plan->n_rows,
+        if (st != plan->stream) HGS_CUDA(cudaStreamSynchronize(plan->stream));  // plan built on another stream
+        k_scatter<<<grid_for(plan->n_rows * cols), 256, 0, st>>>(y, cols, plan->perm, plan->seg, plan->n_rows,
                                                                   accumulate, out);
+        HGS_CUDA(cudaGetLastError());
+    });
+}
+
+int hgs_gather_rows_planned(const hgs_scatter_plan* plan, const double* x, int64_t n_rows, int64_t cols, double* out,
+                            void* stream) {
+    return abi_guard([&] {
+        if (!plan) fail(HGS_EINVAL, "hgs: null plan");
+        if (n_rows != plan->n_rows) fail(HGS_EINVAL, "gather_rows: table rows differ from the plan's");
+        if (plan->m * cols == 0) return;
+        HGS_CUDA(cudaSetDevice(plan->device));
+        cudaStream_t st = (cudaStream_t)stream;
+        if (st != plan->stream) HGS_CUDA(cudaStreamSynchronize(plan->stream));
+        k_gather_rows<<<grid_for(plan->m * cols), 256, 0, st>>>(x, cols, plan->idx, plan->m, out);
         HGS_CUDA(cudaGetLastError());
     });
 }
@@ -270,6 +337,8 @@ int hgs_scatter_plan_destroy(hgs_scatter_plan* plan) {
     return abi_guard([&] {
         if (!plan) return;
         HGS_CUDA(cudaSetDevice(plan->device));
+        HGS_CUDA(cudaFreeAsync(plan->perm, plan->stream));
+        HGS_CUDA(cudaFreeAsync(plan->seg, plan->stream));
         delete plan;
     });
 }

@@ -35,7 +35,7 @@ EXPORTS = [
     "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind", "hgs_sample_copy_frontiers",
     "hgs_sample_rows", "hgs_sample_reruns",
     "hgs_sample_slice", "hgs_gather_rows", "hgs_scatter_plan_create", "hgs_scatter_add",
-    "hgs_scatter_plan_destroy", "hgs_ordered_mean",
+    "hgs_scatter_plan_destroy", "hgs_ordered_mean", "hgs_gather_rows_planned",
 ]
 
 
@@ -180,6 +180,7 @@ def lib() -> C.CDLL:
         L.hgs_scatter_add.argtypes = [vp, vp, i64, vp, i32, vp]
         L.hgs_scatter_plan_destroy.argtypes = [vp]
         L.hgs_ordered_mean.argtypes = [vp, i32, i64, vp, vp]
+        L.hgs_gather_rows_planned.argtypes = [vp, vp, i64, i64, vp, vp]
         _lib_cache = L
     return _lib_cache
 
@@ -335,6 +336,7 @@ class Sampler:
                                        C.byref(self._h)))
         self.counts = SampleCounts(0, 0, 0, 0)
         self.gathered = False
+        self._batch_off = None
 
     @staticmethod
     def config(depth=3, fanout=6, symmetrize=True, rng=RNG_XOSHIRO, gather=False, profile=False,
@@ -351,11 +353,13 @@ class Sampler:
         c = self.config(**cfg)
         _check(lib().hgs_sample_run(self._h, C.byref(c), _p(r), _p(b), len(b) - 1, _p(s), _p(st)))
         self.gathered = bool(c.gather)
+        self._batch_off = b.copy()
         return self.wait()
 
     def run_device(self, d_roots: int, d_batch_off: int, n_roots: int, n_batches: int,
                    d_seeds: int, **cfg) -> None:
         """Enqueue with device pointers (int32 roots, int64 batch_off, u64 seeds)."""
+        self._batch_off = None
         c = self.config(**cfg)
         self.gathered = bool(c.gather)
         _check(lib().hgs_sample_run_device(self._h, C.byref(c), C.c_void_p(d_roots),
@@ -370,6 +374,7 @@ class Sampler:
     def run_device_spec(self, d_roots: int, d_batch_off: int, n_roots: int, n_batches: int,
                         spec: SeedSpec, **cfg) -> None:
         """Enqueue with device roots/offsets; per-root seeds derived on the device."""
+        self._batch_off = None
         c = self.config(**cfg)
         self.gathered = bool(c.gather)
         _check(lib().hgs_sample_run_device_spec(self._h, C.byref(c), C.c_void_p(d_roots),
@@ -407,6 +412,12 @@ class Sampler:
         v = DeviceViews()
         _check(lib().hgs_sample_device_views(self._h, C.byref(v)))
         return v
+
+    def batch_components(self, batch: int) -> int:
+        """Number of components (roots) of batch `batch` of the last host-input run."""
+        if self._batch_off is None:
+            raise SamplerError("batch_components: last run had device inputs (batch offsets not on the host)")
+        return int(self._batch_off[batch + 1] - self._batch_off[batch])
 
     def slice(self, batch: int, begin: int, end: int) -> SliceViews:
         """slice_components (trainer.cpp:221-269) of batch `batch` of the last

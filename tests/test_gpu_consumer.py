@@ -80,6 +80,12 @@ def test_gather_scatter_forward_backward_golden(case):
     # backward passes as the reference tape computes them
     assert np.array_equal(bits(co.scatter_add(cuda(G[f"gs{case}_gather_gout"]), plan)), bits(G[f"gs{case}_gather_gin"]))
     assert np.array_equal(bits(co.gather_rows(cuda(G[f"gs{case}_scatter_gout"]), di)), bits(G[f"gs{case}_scatter_gin"]))
+    # the planned gather (no re-check) gives the same rows; a sorted list takes the no-sort plan
+    assert np.array_equal(bits(co.gather_rows_planned(cuda(x), plan)), bits(G[f"gs{case}_gather"]))
+    sidx = np.sort(idx)
+    splan = co.ScatterPlan(cuda(sidx, torch.int32), n)
+    assert np.array_equal(bits(co.scatter_add(cuda(y), splan)), bits(CO.scatter_add(y, sidx, n)))
+    splan.close()
     # the same through torch autograd
     xt = cuda(x).requires_grad_(True)
     out = co.GatherRows.apply(xt, di, plan)
