@@ -1,28 +1,30 @@
-// extract_bm.cu — K2, the default extraction kernel: dedup, sort and
-// induced-subgraph extraction of one root per CTA against a bitmap rank
-// directory in shared memory.
+// extract_bm.cu — K2, bitmap-directory variant (opt-in, HGS_K2=bm): dedup,
+// sort and induced-subgraph extraction of one root per CTA against a bitmap
+// rank directory in shared memory. Parity-green; at C2 it runs as fast as the
+// default hash-set kernel (0.78 vs 0.76 ms), see DESIGN.md §4.
 //
 // The directory covers the whole vertex id range: word w describes ids
 // 16w .. 16w+15 as 16 membership bits (low half) and the rank of the word's
-// first member (high half). A second-level bitmap marks the nonzero words.
+// first member (high half). A second-level bitmap marks the nonzero words and
+// per-block counters hold the members of each run of 32 words.
 //
 // sorted_vertex_set (sampler.cpp:48-53) without a sort: the CTA sets the
-//   touched list's bits (atomicOr; duplicates collapse), walks the nonzero
-//   words in id order through the second-level bitmap, and writes each word's
-//   rank prefix and its members — the set comes out ascending, and a vertex's
-//   local id is its rank.
+//   touched list's bits (atomicOr; duplicates collapse); the first setter of
+//   each word owns it and, after an exclusive scan of the block counters,
+//   computes the word's rank prefix and writes its members into the set —
+//   the set comes out ascending, and a vertex's local id is its rank.
 // induced_subgraph = S·A·Sᵀ (sparse.cpp:177-191) on the directed edge-id A:
-//   the nonempty A rows of the set, in local order, are flattened and scanned
-//   in 32-entry windows (row owner of each lane = per-window cursor + popc of a
-//   row-start bitmask), each column tested with ONE 4-byte shared load of its
-//   directory word: member bit and local id (rank prefix + popc of the lower
-//   member bits) come out of the same word, no collisions, no slow path. The
-//   CTA's warps take consecutive windows in rounds; one barrier per round
-//   orders their hits, so they land in the root's edge slot in the
-//   reference's CSR order (rows ascending, columns ascending within a row).
-// Undo: the set's directory words are zeroed after the root (the second-level
-//   bitmap is cleared while it is walked), so the directory is never cleared
-//   in full.
+//   A's rows are stored padded to 4-entry quads (DevGraph::a_q, as probe
+//   words); the set's nonempty rows, in local order, are flattened in quads
+//   and scanned in windows of 32 quads (owner row of each quad from a
+//   per-pass u16 owner array), one 16-byte load per lane. Each column is
+//   tested with ONE 4-byte shared load of its directory word: member bit and
+//   local id (rank prefix + popc of the lower member bits) come out of the
+//   same word, no collisions, no slow path. The CTA's warps take consecutive
+//   windows in rounds; one barrier per round orders their hits, so they land
+//   in the root's edge slot in the reference's CSR order.
+// Undo: the set's directory words and second-level bits are zeroed after the
+//   root, the block counters cleared, so the directory is never cleared in full.
 //
 // Outputs as the other K2 kernels: sorted set written back over the touched
 // slot, (V_r, E_r, local id of the root, S_r) per root, edge slots of
