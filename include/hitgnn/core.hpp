@@ -297,6 +297,13 @@ namespace gpu {
 // the cache (upload per call, the pre-cache behaviour).
 void release_cached();
 std::size_t cached_entries();
+// Gather prefetch (the trainer's two lines, trainer.cpp:457-458): once the
+// event is resident with its features (after any gather_features call),
+// bulk_shadow(edge-id A) gathers on the device as it samples, and the
+// following gather_features(batch, event) calls on the same thread take the
+// prebuilt features. Returns how many gather_features calls on this thread
+// were served that way.
+std::size_t prefetched_gathers();
 
 // An event resident on one GPU: A (edge ids), walk, features. Create once per
 // event (next to make_edge_id_matrix in Trainer's constructor) and sample

@@ -154,6 +154,20 @@ int main() {
             compare(out, oracle(adj, &event, batches, seeds, nullptr, 0, cfg), true, "cached trainer path");
         }
         CHECK(gpu::cached_entries() == 2);  // A and the event
+        // reps 1 and 2 found the event resident: their gathers were prefetched
+        CHECK(gpu::prefetched_gathers() >= static_cast<std::size_t>(2 * k));
+        {   // a copied batch, a reordered gather and an untouched batch still get exact features
+            const std::size_t before = gpu::prefetched_gathers();
+            PerRootChoiceSource src(seeds);
+            auto out = bulk_shadow(adj, batches, cfg, src);
+            compare(out, oracle(adj, nullptr, batches, seeds, nullptr, 0, cfg), false, "prefetch: values before gather");
+            std::vector<SampledBatch> copy(out.begin(), out.end());  // new buffers: no prefetch match
+            for (Index bi = k - 1; bi >= 0; --bi) gather_features(out[bi], event);
+            for (auto& sb : copy) gather_features(sb, event);
+            compare(out, oracle(adj, &event, batches, seeds, nullptr, 0, cfg), true, "prefetch: reverse order");
+            compare(copy, oracle(adj, &event, batches, seeds, nullptr, 0, cfg), true, "prefetch: copies");
+            CHECK(gpu::prefetched_gathers() == before + static_cast<std::size_t>(k));
+        }
         CsrMatrix adj2 = adj;
         {
             PerRootChoiceSource src(seeds);
