@@ -183,6 +183,18 @@ int hgs_sample_bind(hgs_sample* s, hgs_graph* g);
 int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
                    const int64_t* batch_off, int64_t n_batches, const uint64_t* seeds,
                    const uint64_t* rng_state);
+/* One call over minibatches of several resident events (SURVEY.md §8(e),
+ * multi-event launches): batch b samples graphs[batch_event[b]] (all graphs
+ * on the handle's device; batch_event non-decreasing, so each event's batches
+ * are contiguous; equal feature widths when gathering). Roots are checked
+ * against their batch's event. Outputs as hgs_sample_run over the
+ * concatenated batches; under per-root streams they equal one call per event
+ * (the trainer's event loop, trainer.cpp:433-467). Each event's expand,
+ * extract and pack kernels run on its own graph; offsets carry across events
+ * on the device, so the call synchronises once. Blocks like hgs_sample_run. */
+int hgs_sample_run_multi(hgs_sample* s, const hgs_config* cfg, hgs_graph* const* graphs, int32_t n_graphs,
+                         const int32_t* batch_event, const int64_t* roots, const int64_t* batch_off,
+                         int64_t n_batches, const uint64_t* seeds);
 /* Same, with device-resident int32 roots[n_roots], int64 batch_off[n_batches+1]
  * and u64 seeds; enqueued asynchronously on the handle's stream. Roots are
  * range-checked on the device (reported by hgs_sample_wait); per-batch

@@ -572,6 +572,89 @@ int hgs_sample_run(hgs_sample* s, const hgs_config* cfg, const int64_t* roots,
     });
 }
 
+int hgs_sample_run_multi(hgs_sample* s, const hgs_config* cfg, hgs_graph* const* graphs, int32_t n_graphs,
+                         const int32_t* batch_event, const int64_t* roots, const int64_t* batch_off,
+                         int64_t n_batches, const uint64_t* seeds) {
+    return guarded([&] {
+        if (!s) fail(HGS_EINVAL, "hgs: null sample handle");
+        validate_cfg(cfg);
+        if (n_graphs < 1 || !graphs) fail(HGS_EINVAL, "hgs_sample_run_multi: no graphs");
+        if (n_batches < 0 || !batch_off || (n_batches > 0 && !batch_event))
+            fail(HGS_EINVAL, "hgs_sample_run_multi: bad batch offsets");
+        if (batch_off[0] != 0) fail(HGS_EINVAL, "hgs_sample_run_multi: batch_off[0] must be 0");
+        const int device = s->graph->g.device;
+        for (int32_t e = 0; e < n_graphs; ++e) {
+            if (!graphs[e]) fail(HGS_EINVAL, "hgs_sample_run_multi: null graph");
+            if (graphs[e]->g.device != device)
+                fail(HGS_EINVAL, "hgs_sample_run_multi: every graph must be on the sample handle's device");
+            check_square(graphs[e]->g, cfg->symmetrize);
+            if (cfg->gather && (graphs[e]->g.f_v != graphs[0]->g.f_v || graphs[e]->g.f_e != graphs[0]->g.f_e))
+                fail(HGS_EINVAL, "hgs_sample_run_multi: feature widths differ across graphs");
+        }
+        // events contiguous in batch order: event e owns the roots [ev_r0[e], ev_r0[e+1])
+        std::vector<int64_t> ev_r0((size_t)n_graphs + 1, 0);
+        int32_t prev = 0;
+        for (int64_t b = 0; b < n_batches; ++b) {
+            const int32_t e = batch_event[b];
+            if (e < 0 || e >= n_graphs) fail(HGS_EINVAL, "hgs_sample_run_multi: batch event out of range");
+            if (e < prev) fail(HGS_EINVAL, "hgs_sample_run_multi: batch events must be non-decreasing");
+            if (batch_off[b + 1] < batch_off[b]) fail(HGS_EINVAL, "hgs_sample_run_multi: batch_off not non-decreasing");
+            prev = e;
+        }
+        for (int32_t e = 0, b = 0; e <= n_graphs; ++e) {  // first root of each event
+            while (b < n_batches && batch_event[b] < e) ++b;
+            ev_r0[(size_t)e] = batch_off[b];
+        }
+        const int64_t R = batch_off[n_batches];
+        if (R >= ((int64_t)1 << 31) - 1) fail(HGS_ERANGE, "hgs_sample_run_multi: too many roots");
+        // check_roots per batch (sampler.cpp:12-20) against the batch's event
+        static thread_local std::vector<uint8_t> seen;
+        for (int64_t b = 0; b < n_batches; ++b) {
+            const int64_t n = graphs[batch_event[b]]->g.n_rows;
+            if ((int64_t)seen.size() < n) seen.assign((size_t)n, 0);
+            int64_t i = batch_off[b];
+            for (; i < batch_off[b + 1]; ++i) {
+                const int64_t r = roots[i];
+                if (r < 0 || r >= n) {
+                    for (int64_t j = batch_off[b]; j < i; ++j) seen[roots[j]] = 0;
+                    fail(HGS_EINVAL, "sampler: root " + std::to_string(r) + " out of range");
+                }
+                if (seen[r]) {
+                    for (int64_t j = batch_off[b]; j < i; ++j) seen[roots[j]] = 0;
+                    fail(HGS_EINVAL, "sampler: duplicate root " + std::to_string(r));
+                }
+                seen[r] = 1;
+            }
+            for (int64_t j = batch_off[b]; j < batch_off[b + 1]; ++j) seen[roots[j]] = 0;
+        }
+        if (R > 0 && !seeds) fail(HGS_EINVAL, "hgs_sample_run_multi: null seeds");
+        HGS_CUDA(cudaSetDevice(device));
+        if (s->pending) HGS_CUDA(cudaStreamSynchronize(s->stream));
+        s->pending = false;
+        s->boff64.reserve((size_t)n_batches + 1);
+        s->seeds.reserve((size_t)R + 1);
+        s->roots64.reserve((size_t)R + 1);
+        upload(s->roots64.p, roots, sizeof(int64_t) * R, s->stream);
+        upload(s->boff64.p, batch_off, sizeof(int64_t) * (n_batches + 1), s->stream);
+        upload(s->seeds.p, seeds, sizeof(uint64_t) * R, s->stream);
+        s->multi_graphs.assign(graphs, graphs + n_graphs);
+        s->multi_r0 = ev_r0;
+        CallInputs in;
+        in.roots64 = s->roots64.p;
+        in.batch_off = s->boff64.p;
+        in.seeds = s->seeds.p;
+        in.R = R;
+        in.k = n_batches;
+        in.n_events = n_graphs;
+        in.events = s->multi_graphs.data();
+        in.ev_r0 = s->multi_r0.data();
+        s->last_in = in;
+        s->last_cfg = *cfg;
+        sample_enqueue(s, *cfg, in);
+        sample_finish(s, *cfg, in);
+    });
+}
+
 int hgs_sample_run_device(hgs_sample* s, const hgs_config* cfg, const int32_t* d_roots,
                           const int64_t* d_batch_off, int64_t n_roots, int64_t n_batches,
                           const uint64_t* d_seeds) {

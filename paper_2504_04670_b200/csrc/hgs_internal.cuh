@@ -153,6 +153,11 @@ struct CallInputs {
     const uint64_t* state = nullptr;
     const hgs_seed_spec* spec = nullptr;  // seeds derived on the device when seeds == nullptr
     int64_t R = 0, k = 0;
+    // multi-event call (hgs_sample_run_multi): event e samples graph events[e]
+    // for the roots [ev_r0[e], ev_r0[e+1]) (host arrays, owned by the handle)
+    int32_t n_events = 0;
+    hgs_graph* const* events = nullptr;
+    const int64_t* ev_r0 = nullptr;
 };
 void graph_ensure_recip(DevGraph& g, int32_t max_m);
 
@@ -309,6 +314,9 @@ struct hgs_sample {
     cudaEvent_t ev[6] = {};
     int64_t launches = 0;     // kernels launched by the last run, re-runs included
     int64_t reruns = 0;       // capacity re-runs of the last run (0 in a steady state)
+    // multi-event call inputs (kept for a capacity re-run)
+    std::vector<hgs_graph*> multi_graphs;
+    std::vector<int64_t> multi_r0;
     // slice_components outputs (hgs_sample_slice)
     hgs::DevBuf<int32_t> sl_row, sl_col, sl_comp, sl_roots;
     // chunked pipeline: packing runs on a higher-priority side stream

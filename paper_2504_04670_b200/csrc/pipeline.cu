@@ -160,9 +160,9 @@ bool plan_k2(CallPlan& c, int64_t bound, int64_t n, int32_t max_out_deg) {
     return plan_extract_bm(c, bound, n) || plan_extract_dir(c, bound, n, max_out_deg) || plan_extract(c, bound, n);
 }
 
-CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth, int64_t fanout) {
+CallPlan plan_call(int32_t walk_max_deg, int32_t a_max_deg, int64_t n, int64_t depth, int64_t fanout) {
     CallPlan c{};
-    c.kmax = std::min<int64_t>(fanout, walk.max_deg);
+    c.kmax = std::min<int64_t>(fanout, walk_max_deg);
     if (c.kmax > ((int64_t)1 << 24))
         fail(HGS_ERANGE, "hgs: min(fanout, max degree) > 2^24 is not supported by this build");
     c.max_t = tree_bound(c.kmax, depth);
@@ -172,7 +172,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
     if (c.max_t > ((int64_t)1 << 30))
         fail(HGS_ERANGE, "hgs: per-root tree bound " + std::to_string(c.max_t) + " is too large; reduce depth/fanout");
     c.cache_entries = tree_bound(c.kmax, depth - 1);
-    c.recip_smem = walk.max_deg + 1 <= 4096 ? walk.max_deg + 1 : 0;
+    c.recip_smem = walk_max_deg + 1 <= 4096 ? walk_max_deg + 1 : 0;
     const size_t rbytes = (size_t)c.recip_smem * sizeof(uint64_t);
     // 64-lane blocks: K1's time per SM is linear in its lanes, and finer
     // blocks even out the SMs (C2: 1024 blocks = 6.9 per SM; 128-lane blocks
@@ -183,7 +183,7 @@ CallPlan plan_call(const DevCsr& walk, const DevCsr& a, int64_t n, int64_t depth
         c.cache_entries = 0;
         c.expand_smem = rbytes;
     }
-    if (c.max_t > kMaxSet || !plan_k2(c, c.max_t, n, a.max_deg)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
+    if (c.max_t > kMaxSet || !plan_k2(c, c.max_t, n, a_max_deg)) c.k2_warps = 0;  // decided after K1 (see sample_enqueue)
     return c;
 }
 
@@ -205,14 +205,34 @@ int sm_count(int device) {
 }  // namespace
 
 void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, bool rerun) {
-    DevGraph& g = s->graph->g;
+    // The graphs of the call: the handle's graph, or one per event of a
+    // multi-event call (hgs_sample_run_multi), all on the handle's device.
+    const bool multi = in.n_events > 0;
+    std::vector<DevGraph*> gs;
+    if (multi)
+        for (int32_t e = 0; e < in.n_events; ++e) gs.push_back(&in.events[e]->g);
+    else
+        gs.push_back(&s->graph->g);
+    DevGraph& g = *gs[0];
     HGS_CUDA(cudaSetDevice(g.device));
-    if (cfg.symmetrize) graph_build_walk_sym(g);
     const bool seq_walk = (cfg.flags & HGS_FLAG_SEQ_WALK) != 0;
-    const DevCsr& walk = cfg.symmetrize ? g.walk_sym : (seq_walk ? g.full_pattern() : g.a);
-    graph_ensure_recip(g, walk.max_deg);
-    if (cfg.gather && !g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
-    CallPlan c = plan_call(walk, g.a, g.n_rows, cfg.depth, cfg.fanout);
+    auto walk_of = [&](DevGraph& h) -> const DevCsr& {
+        return cfg.symmetrize ? h.walk_sym : (seq_walk ? h.full_pattern() : h.a);
+    };
+    int32_t walk_max = 0, a_max = 0;
+    int64_t n_max = 0;
+    for (DevGraph* h : gs) {
+        if (cfg.symmetrize) graph_build_walk_sym(*h);
+        graph_ensure_recip(*h, walk_of(*h).max_deg);
+        if (cfg.gather && !h->has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
+        walk_max = std::max(walk_max, walk_of(*h).max_deg);
+        a_max = std::max(a_max, h->a.max_deg);
+        n_max = std::max<int64_t>(n_max, h->n_rows);
+    }
+    if (multi)  // K1 stages recip_smem entries of every event's table
+        for (DevGraph* h : gs) graph_ensure_recip(*h, walk_max);
+    const DevCsr& walk = walk_of(g);
+    CallPlan c = plan_call(walk_max, a_max, n_max, cfg.depth, cfg.fanout);
     const int64_t R = in.R, k = in.k;
     if (R * c.max_t >= ((int64_t)1 << 40)) fail(HGS_ERANGE, "hgs: too many roots for one call");
     cudaStream_t st = s->stream;
@@ -315,6 +335,20 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     }
     pp.v_cap = (int64_t)s->v_cap; pp.e_cap = (int64_t)s->e_cap; pp.ticket = s->ticket.p;
     pp.set_cap = c.set_cap;
+    const uint4* erec = g.erec.p;
+    // point the kernels at one event's graph (multi-event calls rebind per event)
+    auto bind = [&](DevGraph& h) {
+        const DevCsr& w = walk_of(h);
+        ep.w_rp = w.rp.p; ep.w_ci = w.ci.p; ep.recip = h.recip.p;
+        ep.neg_row = (!cfg.symmetrize && !seq_walk && h.has_neg) ? h.neg_row.p : nullptr;
+        ep.n = (int32_t)h.n_rows;
+        xp.a_rp = h.a.rp.p; xp.a_ci = h.a.ci.p; xp.a_gid = h.has_gid ? h.a_gid.p : nullptr; xp.a_ri = h.a_ri.p;
+        pp.node_feat = h.node_feat.p; pp.edge_feat = h.edge_feat.p; pp.labels = h.labels.p;
+        erec = h.erec.p;
+    };
+    // the event of each root range: one range per event (multi) or the whole call
+    std::vector<int64_t> ev_r0{0, R};
+    if (multi) ev_r0.assign(in.ev_r0, in.ev_r0 + in.n_events + 1);
 
     // Roots go through the stages in chunks: K1 -> K2 -> offset scan of chunk
     // c on the handle's stream, K3 of chunk c on a higher-priority side
@@ -324,10 +358,10 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     // Off by default: measured on B200 at C2, packing next to extraction
     // slows both (they contend for the LSU pipe), see DESIGN.md.
     int64_t chunk = R;
-    if (!s->profiled)
+    if (!s->profiled && !multi)
         if (const char* e = getenv("HGS_CHUNK_ROOTS")) chunk = std::max<int64_t>(32, atoll(e));
-    const int64_t nchunks = R > 0 ? (R + chunk - 1) / chunk : 0;
-    const bool split = nchunks > 1;
+    const int64_t nchunks = multi ? in.n_events : (R > 0 ? (R + chunk - 1) / chunk : 0);
+    const bool split = !multi && nchunks > 1;  // side-stream packing (opt-in experiment)
     cudaStream_t pst = st;
     if (split) {
         if (!s->aux) {
@@ -350,8 +384,12 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         s->kbig.reserve((size_t)R * 3 * (size_t)c.kmax);
         ep.big = s->kbig.p;
     }
-    if (R > 0) {  // K1 over all roots at once: one lane per root, its length is one root's chain
-        ep.r0 = 0; ep.R = (int32_t)R;
+    // K1 over all roots at once (one lane per root, its length is one root's
+    // chain); a multi-event call runs it per event, each on its own walk
+    for (size_t e = 0; e + 1 < ev_r0.size(); ++e) {
+        if (ev_r0[e + 1] <= ev_r0[e]) continue;
+        bind(*gs[multi ? e : 0]);
+        ep.r0 = (int32_t)ev_r0[e]; ep.R = (int32_t)ev_r0[e + 1];
         launch_expand(c.expand_threads, c.expand_smem, c.kmax, ep, cfg.rng == HGS_RNG_PHILOX, st);
         ++s->launches;
     }
@@ -362,13 +400,13 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         int32_t tmax = 0;
         HGS_CUDA(cudaMemcpyAsync(&tmax, s->ticket.p + 6, sizeof(int32_t), cudaMemcpyDeviceToHost, st));
         HGS_CUDA(cudaStreamSynchronize(st));
-        if (!plan_k2(c, std::max<int32_t>(tmax, 1), g.n_rows, g.a.max_deg)) {
+        if (!plan_k2(c, std::max<int32_t>(tmax, 1), n_max, a_max)) {
             // beyond one warp's shared memory: K2 keeps its working sets in
             // a global scratch slot per warp (3 hash slots per key)
-            plan_extract(c, 1, g.n_rows);  // rank bits / packing for the real bound below
+            plan_extract(c, 1, n_max);  // rank bits / packing for the real bound below
             c.rank_bits = 1;
             while (((int64_t)1 << c.rank_bits) < tmax) ++c.rank_bits;
-            c.packed = (g.n_rows + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
+            c.packed = (n_max + 1 < ((int64_t)1 << (32 - c.rank_bits))) ? 1 : 0;
             c.set_cap = (tmax + 3) / 4 * 4;
             c.row_cap = c.set_cap;
             c.win_cap = c.set_cap / 2;
@@ -380,7 +418,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
             c.k2_gmem = true;
         }
     }
-    if (c.k2_warps == 0) plan_k2(c, 1, g.n_rows, g.a.max_deg);  // R == 0: nothing to extract
+    if (c.k2_warps == 0) plan_k2(c, 1, n_max, a_max);  // R == 0: nothing to extract
     set_layout();
     const size_t xsmem = c.k2_gmem ? 0 : c.k2_bm ? (size_t)c.warp_bytes : (size_t)c.k2_warps * c.warp_bytes;
     const int xper_sm = c.k2_gmem ? 2
@@ -388,12 +426,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
                         : c.k2_dir ? extract_dir_prepare(xsmem, c.k2_warps)
                                    : extract_blocks_per_sm(xsmem, c.k2_warps, c.packed != 0);
     xp.gscratch = nullptr;
-    if (c.k2_bm) {
-        graph_ensure_quads(g);
-        xp.a_q = g.a_q.p;
-        xp.a_qid = g.a_qid.p;
-        xp.a_rq = g.a_rq.p;
-    }
+    if (c.k2_bm)
+        for (DevGraph* h : gs) graph_ensure_quads(*h);
     if (c.k2_gmem) {
         const size_t slots = (size_t)xper_sm * sm_count(g.device) * c.k2_warps;
         s->k2g.reserve(slots * (size_t)c.warp_bytes);
@@ -408,7 +442,16 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[1], st));
     bool small_scan = false;  // scan + batch offsets done by one small launch
     for (int64_t ci = 0; ci < nchunks; ++ci) {
-        const int32_t r0 = (int32_t)(ci * chunk), r1 = (int32_t)std::min<int64_t>(R, r0 + chunk);
+        const int32_t r0 = (int32_t)(multi ? ev_r0[ci] : ci * chunk);
+        const int32_t r1 = (int32_t)(multi ? ev_r0[ci + 1] : std::min<int64_t>(R, r0 + chunk));
+        if (r1 <= r0) continue;  // an event without roots
+        DevGraph& h = *gs[multi ? ci : 0];
+        bind(h);
+        if (c.k2_bm) {
+            xp.a_q = h.a_q.p;
+            xp.a_qid = h.a_qid.p;
+            xp.a_rq = h.a_rq.p;
+        }
         const int64_t Rc = r1 - r0;
         xp.r0 = r0; xp.R = r1;
         const int64_t per_cta = c.k2_bm ? 1 : c.k2_warps;  // roots in flight per CTA
@@ -422,7 +465,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         else launch_extract((int)std::max<int64_t>(xgrid, 1), c.k2_warps, xsmem, xp, c.packed != 0, st);
         ++s->launches;
         if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[2], st));
-        if (!split && launch_scan_small(s->root_nv.p, s->root_ne.p, (int32_t)R, s->root_voff.p, s->root_eoff.p,
+        if (nchunks == 1 && launch_scan_small(s->root_nv.p, s->root_ne.p, (int32_t)R, s->root_voff.p, s->root_eoff.p,
                                         s->ticket.p, in.batch_off, (int32_t)k, s->batch_voff.p, s->batch_eoff.p,
                                         s->comp_off.p, st)) {
             small_scan = true;
@@ -440,7 +483,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
         pp.r0 = r0; pp.R = r1;
         const int64_t pgrid = split ? (Rc + 7) / 8 : std::min<int64_t>((int64_t)sm_count(g.device) * 8, (Rc + 7) / 8);
         if (k3_fused()) {  // pack + gathers in one pass per root
-            launch_pack_gather((int)std::max<int64_t>(pgrid, 1), pp, g.erec.p, pst);
+            launch_pack_gather((int)std::max<int64_t>(pgrid, 1), pp, erec, pst);
             ++s->launches;
         } else {
         launch_pack((int)std::max<int64_t>(pgrid, 1), pp, pst);
@@ -452,7 +495,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
 #endif
             const int gblocks = split ? std::max<int64_t>(1, std::min<int64_t>(sm_count(g.device) * HGS_GATHER_BPSM, Rc * 4))
                                       : sm_count(g.device) * HGS_GATHER_BPSM;
-            launch_gather_packed(gblocks, pp, g.erec.p, s->root_voff.p + r0, s->root_voff.p + r1,
+            launch_gather_packed(gblocks, pp, erec, s->root_voff.p + r0, s->root_voff.p + r1,
                                  s->root_eoff.p + r0, s->root_eoff.p + r1, pst);
             s->launches += 2;
         }

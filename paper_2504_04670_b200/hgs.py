@@ -35,7 +35,7 @@ EXPORTS = [
     "hgs_sample_run_device_spec", "hgs_derive_seeds", "hgs_sample_bind", "hgs_sample_copy_frontiers",
     "hgs_sample_rows", "hgs_sample_reruns",
     "hgs_sample_slice", "hgs_gather_rows", "hgs_scatter_plan_create", "hgs_scatter_add",
-    "hgs_scatter_plan_destroy", "hgs_ordered_mean", "hgs_gather_rows_planned",
+    "hgs_scatter_plan_destroy", "hgs_ordered_mean", "hgs_gather_rows_planned", "hgs_sample_run_multi",
 ]
 
 
@@ -181,6 +181,7 @@ def lib() -> C.CDLL:
         L.hgs_scatter_plan_destroy.argtypes = [vp]
         L.hgs_ordered_mean.argtypes = [vp, i32, i64, vp, vp]
         L.hgs_gather_rows_planned.argtypes = [vp, vp, i64, i64, vp, vp]
+        L.hgs_sample_run_multi.argtypes = [vp, C.POINTER(Config), vp, i32, vp, vp, vp, i64, vp]
         _lib_cache = L
     return _lib_cache
 
@@ -352,6 +353,21 @@ class Sampler:
         st = None if state is None else np.ascontiguousarray(state, np.uint64)
         c = self.config(**cfg)
         _check(lib().hgs_sample_run(self._h, C.byref(c), _p(r), _p(b), len(b) - 1, _p(s), _p(st)))
+        self.gathered = bool(c.gather)
+        self._batch_off = b.copy()
+        return self.wait()
+
+    def bulk_shadow_multi(self, graphs, batch_event, roots, batch_off, seeds, **cfg) -> SampleCounts:
+        """One call over batches of several resident events (hgs_sample_run_multi):
+        batch b samples graphs[batch_event[b]]; batch_event non-decreasing."""
+        hs = (C.c_void_p * len(graphs))(*[g._h.value for g in graphs])
+        be = np.ascontiguousarray(batch_event, np.int32)
+        r = np.ascontiguousarray(roots, np.int64)
+        b = np.ascontiguousarray(batch_off, np.int64)
+        s = np.ascontiguousarray(seeds, np.uint64)
+        c = self.config(**cfg)
+        _check(lib().hgs_sample_run_multi(self._h, C.byref(c), C.cast(hs, C.c_void_p), len(graphs), _p(be), _p(r),
+                                          _p(b), len(b) - 1, _p(s)))
         self.gathered = bool(c.gather)
         self._batch_off = b.copy()
         return self.wait()

@@ -14,7 +14,7 @@ import os
 import numpy as np
 import pytest
 
-from tests.helpers import O, OUT_FIELDS, load_json, load_small_cases, random_graph, sha
+from tests.helpers import O, OUT_FIELDS, compare, load_json, load_small_cases, random_graph, sha
 
 pytestmark = pytest.mark.gpu
 
@@ -573,6 +573,76 @@ def test_multi_handle_sharding_matches_single_call():
         parts.append(out)
     for f in ("l2g", "e_row", "e_col", "e_gid", "xv", "ye", "lab"):
         assert np.array_equal(np.concatenate([p[f] for p in parts]), full[f]), f
+
+
+def _batch_slices(out, boff, f_v, f_e):
+    """Per batch: its arrays of a flat device result (batch-local ids)."""
+    res = []
+    for b in range(len(boff) - 1):
+        v0, v1 = int(out["batch_voff"][b]), int(out["batch_voff"][b + 1])
+        e0, e1 = int(out["batch_eoff"][b]), int(out["batch_eoff"][b + 1])
+        f, nb = int(boff[b]), int(boff[b + 1] - boff[b])
+        res.append({"l2g": out["l2g"][v0:v1], "e_row": out["e_row"][e0:e1], "e_col": out["e_col"][e0:e1],
+                    "e_gid": out["e_gid"][e0:e1], "comp_off": out["comp_off"][f + b:f + b + nb + 1],
+                    "roots_local": out["roots_local"][f:f + nb], "xv": out["xv"][v0 * f_v:v1 * f_v],
+                    "ye": out["ye"][e0 * f_e:e1 * f_e], "lab": out["lab"][e0:e1],
+                    "draws": out["draws"][f:f + nb], "decisions": out["decisions"][f:f + nb]})
+    return res
+
+
+@pytest.mark.parametrize("rng", [0, 1])
+def test_multi_event_call_matches_per_event_calls(rng):
+    """hgs_sample_run_multi (SURVEY §8(e) multi-event launches): one call over
+    batches of several resident events (one without batches, different sizes
+    and degrees) equals one call per event, batch for batch, and the oracle."""
+    H = hgs()
+    graphs = [random_graph(3000, 30000, 31), random_graph(500, 2000, 32), random_graph(8000, 120000, 33)]
+    Gs = [H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels) for g in graphs]
+    rs = np.random.default_rng(9)
+    plan = [(0, 3, 120), (2, 4, 200)]  # (event, batches, batch size); event 1 has none
+    roots, boff, bev, seeds = [], [0], [], []
+    per_event = {}
+    for e, k, b in plan:
+        rr = np.concatenate([rs.permutation(graphs[e].n)[:b] for _ in range(k)]).astype(np.int64)
+        ss = rs.integers(0, 2**63, k * b, dtype=np.uint64)
+        per_event[e] = (rr, np.arange(k + 1, dtype=np.int64) * b, ss)
+        roots.append(rr)
+        seeds.append(ss)
+        for _ in range(k):
+            boff.append(boff[-1] + b)
+            bev.append(e)
+    roots, seeds, boff = np.concatenate(roots), np.concatenate(seeds), np.array(boff, np.int64)
+    S = H.Sampler(Gs[0])
+    S.bulk_shadow_multi(Gs, bev, roots, boff, seeds, depth=3, fanout=5, rng=rng, gather=True)
+    multi = _batch_slices(S.to_host(), boff, 6, 2)
+    got = []
+    for e, k, b in plan:
+        rr, bo, ss = per_event[e]
+        Se = H.Sampler(Gs[e])
+        Se.bulk_shadow(rr, bo, ss, depth=3, fanout=5, rng=rng, gather=True)
+        got += _batch_slices(Se.to_host(), bo, 6, 2)
+        ref = O.bulk_shadow(graphs[e], rr, bo, ss, rng=rng, depth=3, fanout=5, gather=True)
+        assert not compare(Se.to_host(), ref, gather=True)
+    assert len(got) == len(multi)
+    for b, (m, p) in enumerate(zip(multi, got)):
+        for f in m:
+            assert np.array_equal(np.asarray(m[f]).view(np.uint8), np.asarray(p[f]).view(np.uint8)), (b, f)
+
+
+def test_multi_event_call_errors():
+    H = hgs()
+    g0, g1 = random_graph(300, 2000, 41), random_graph(100, 500, 42)
+    Gs = [H.Graph(g.rp, g.ci) for g in (g0, g1)]
+    S = H.Sampler(Gs[0])
+    roots = np.array([5, 7, 150, 3], np.int64)
+    boff = np.array([0, 2, 4], np.int64)
+    seeds = np.arange(4, dtype=np.uint64)
+    with pytest.raises(H.SamplerError, match="sampler: root 150 out of range"):
+        S.bulk_shadow_multi(Gs, [0, 1], roots, boff, seeds, depth=2, fanout=3)
+    with pytest.raises(H.SamplerError, match="batch events must be non-decreasing"):
+        S.bulk_shadow_multi(Gs, [1, 0], np.array([5, 7, 1, 3], np.int64), boff, seeds, depth=2, fanout=3)
+    S.bulk_shadow_multi(Gs, [0, 1], np.array([5, 7, 99, 3], np.int64), boff, seeds, depth=2, fanout=3)
+    assert S.counts.k == 2
 
 
 # ------------------------------------------------------------------ C1 / C2 ----
