@@ -302,8 +302,8 @@ typedef struct {
 
 /* slice_components(batch `batch` of the last run, components [begin, end)):
  * HGS_EINVAL "slice_components: bad component range" as the reference.
- * Enqueued on the handle's stream after one small synchronous read of the
- * batch's offsets. */
+ * Runs on the handle's stream and returns with the slice complete, so any
+ * stream may consume it. */
 int hgs_sample_slice(hgs_sample* s, int64_t batch, int64_t begin, int64_t end, hgs_slice_views* out);
 
 /* Tape::gather_rows forward: out[i, :] = x[idx[i], :] for i < m (row-major

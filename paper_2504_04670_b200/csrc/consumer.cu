@@ -223,6 +223,8 @@ int hgs_sample_slice(hgs_sample* s, int64_t batch, int64_t begin, int64_t end, h
             s->e_row.p + h[3], s->e_col.p + h[3], ne, s->comp_off.p + f + batch + begin, s->roots_local.p + f + begin,
             nc, vshift, s->sl_row.p, s->sl_col.p, s->sl_comp.p, s->sl_roots.p);
         HGS_CUDA(cudaGetLastError());
+        // the slice is consumed on the caller's streams: make it complete here
+        HGS_CUDA(cudaStreamSynchronize(st));
         const DevGraph& g = s->graph->g;
         out->n_vertices = nv;
         out->n_edges = ne;

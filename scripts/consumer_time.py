@@ -6,7 +6,8 @@ import numpy as np, torch
 from paper_2504_04670_b200 import hgs, workload as W, consumer as C
 ev = W.preset_event("C2")
 G = hgs.Graph(ev.rp, ev.ci).attach_features(ev.node_feat, ev.edge_feat, ev.labels)
-S = hgs.Sampler(G)
+side = torch.cuda.Stream()  # the sampler on its own (non-blocking) torch stream, as in bench.py
+S = hgs.Sampler(G, stream=side.cuda_stream)
 roots, boff, seeds = W.bench_roots(ev.n, 1024, 64, seed=1, rep=0)
 S.bulk_shadow(roots, boff, seeds, depth=3, fanout=6, gather=True)
 acc = {}
