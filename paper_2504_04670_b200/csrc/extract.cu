@@ -254,7 +254,7 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         // counter of bucket b lives at ((b & pm) << 5) | (b >> lp): lane l's
         // consecutive buckets are one bank apart (conflict-free scan)
         auto cidx = [&](uint32_t b) -> int { return (int)(((b & pm) << 5) | (b >> lp)); };
-        for (int i = lane; i < (32 << lp); i += 32) cnt[i] = 0;
+        for (int i = lane; i < (8 << lp); i += 32) reinterpret_cast<int4*>(cnt)[i] = make_int4(0, 0, 0, 0);
         __syncwarp();
         for (int i = lane; i < U; i += 32) atomicAdd(&cnt[cidx(((uint32_t)keys[i] - lo) >> shift)], 1);
         __syncwarp();
@@ -290,8 +290,10 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 const uint32_t b = (v - lo) >> shift;
                 const int e = cnt[cidx(b)];
                 const int s = b ? cnt[cidx(b - 1)] : 0;
-                rank = s;
-                for (int j = s; j < e; ++j) rank += (uint32_t)tmp[j] < v;
+                // buckets hold ~1-2 keys: the first two compares without a loop
+                const uint32_t t0 = (uint32_t)tmp[s], t1 = s + 1 < e ? (uint32_t)tmp[s + 1] : v;
+                rank = s + (t0 < v) + (t1 < v);
+                for (int j = s + 2; j < e; ++j) rank += (uint32_t)tmp[j] < v;
                 keys[rank] = (int32_t)v;
                 sl = hs.find_slot(v);
             }

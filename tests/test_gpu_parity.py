@@ -590,11 +590,14 @@ def _batch_slices(out, boff, f_v, f_e):
     return res
 
 
-@pytest.mark.parametrize("rng", [0, 1])
-def test_multi_event_call_matches_per_event_calls(rng):
+@pytest.mark.parametrize("rng,k2", [(0, "hash"), (1, "hash"), (0, "bm"), (1, "dir")])
+def test_multi_event_call_matches_per_event_calls(rng, k2, monkeypatch):
     """hgs_sample_run_multi (SURVEY §8(e) multi-event launches): one call over
     batches of several resident events (one without batches, different sizes
-    and degrees) equals one call per event, batch for batch, and the oracle."""
+    and degrees) equals one call per event, batch for batch, and the oracle —
+    with every K2 kernel (the bitmap one sizes its directory for the largest
+    event)."""
+    monkeypatch.setenv("HGS_K2", k2)
     H = hgs()
     graphs = [random_graph(3000, 30000, 31), random_graph(500, 2000, 32), random_graph(8000, 120000, 33)]
     Gs = [H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels) for g in graphs]
@@ -627,6 +630,41 @@ def test_multi_event_call_matches_per_event_calls(rng):
     for b, (m, p) in enumerate(zip(multi, got)):
         for f in m:
             assert np.array_equal(np.asarray(m[f]).view(np.uint8), np.asarray(p[f]).view(np.uint8)), (b, f)
+
+
+def test_slice_after_multi_and_device_runs():
+    """hgs_sample_slice reads the last run's batch offsets for host-input,
+    device-input and multi-event runs alike."""
+    import torch
+    from oracle import consumer as CO
+    from paper_2504_04670_b200 import consumer
+    H = hgs()
+    g0, g1 = random_graph(2000, 16000, 51), random_graph(900, 7000, 52)
+    Gs = [H.Graph(g.rp, g.ci).attach_features(g.node_feat, g.edge_feat, g.labels) for g in (g0, g1)]
+    rs = np.random.default_rng(4)
+    r0 = np.concatenate([rs.permutation(2000)[:50] for _ in range(2)])
+    r1 = np.concatenate([rs.permutation(900)[:40] for _ in range(3)])
+    roots = np.concatenate([r0, r1]).astype(np.int64)
+    boff = np.array([0, 50, 100, 140, 180, 220], np.int64)
+    seeds = rs.integers(0, 2**63, len(roots), dtype=np.uint64)
+    S = H.Sampler(Gs[0])
+    S.bulk_shadow_multi(Gs, [0, 0, 1, 1, 1], roots, boff, seeds, depth=2, fanout=4, gather=True)
+    ref1 = O.bulk_shadow(g1, r1.astype(np.int64), np.array([0, 40, 80, 120], np.int64), seeds[100:],
+                         depth=2, fanout=4, gather=True)
+    sl = consumer.slice_components(S, 3, 5, 30)  # event 1's second batch
+    want = CO.slice_components(CO.batch_of(ref1, np.array([0, 40, 80, 120]), 1, 6, 2), 5, 30)
+    assert np.array_equal(sl.e_col.cpu().numpy(), want["e_col"])
+    assert np.array_equal(sl.edge_features.cpu().numpy().view(np.uint64), want["ye"].view(np.uint64))
+    # device inputs
+    d_r = torch.as_tensor(r1.astype(np.int32), device="cuda")
+    d_b = torch.as_tensor(np.array([0, 40, 80, 120], np.int64), device="cuda")
+    d_s = torch.as_tensor(seeds[100:].view(np.int64), device="cuda")
+    S1 = H.Sampler(Gs[1])
+    S1.run_device(d_r.data_ptr(), d_b.data_ptr(), 120, 3, d_s.data_ptr(), depth=2, fanout=4, gather=True)
+    S1.wait()
+    sl = consumer.slice_components(S1, 1, 5, 30)
+    assert np.array_equal(sl.e_col.cpu().numpy(), want["e_col"])
+    assert np.array_equal(sl.node_features.cpu().numpy().view(np.uint64), want["xv"].view(np.uint64))
 
 
 def test_multi_event_call_errors():
