@@ -56,7 +56,8 @@ struct HashSet<true> {
         for (int i = lane_id(); i < nslots / 4; i += 32)
             reinterpret_cast<uint4*>(slot)[i] = make_uint4(kEmpty, kEmpty, kEmpty, kEmpty);
     }
-    __device__ __forceinline__ bool insert(uint32_t v) const {
+    // spill is set when the key lands outside its home bucket
+    __device__ __forceinline__ bool insert(uint32_t v, bool& spill) const {
         const uint32_t e = (v << rb) | rmask, hi = v << rb;
         uint32_t b = bucket(v);
         for (;;) {
@@ -67,6 +68,7 @@ struct HashSet<true> {
                 if ((prev ^ hi) <= rmask) return false;
             }
             b = next(b);
+            spill = true;
         }
     }
     __device__ __forceinline__ int find_slot(uint32_t v) const {
@@ -106,6 +108,12 @@ struct HashSet<true> {
         }
         return d <= rmask ? (int)d : -1;
     }
+    // find_rank when no key of the set left its home bucket: one probe, no loop
+    __device__ __forceinline__ int find_rank_home(uint32_t v) const {
+        const uint32_t hi = v << rb;
+        const uint32_t d = bmin(*reinterpret_cast<const Vec*>(slot + BW * bucket(v)), hi);
+        return d <= rmask ? (int)d : -1;
+    }
 };
 
 template <>
@@ -119,7 +127,7 @@ struct HashSet<false> {
     __device__ __forceinline__ void clear(int nslots) const {
         for (int i = lane_id(); i < nslots; i += 32) slot[i] = make_uint2(kEmpty, 0);
     }
-    __device__ __forceinline__ bool insert(uint32_t v) const {
+    __device__ __forceinline__ bool insert(uint32_t v, bool& spill) const {
         uint32_t b = bucket(v);
         for (;;) {
 #pragma unroll
@@ -129,6 +137,7 @@ struct HashSet<false> {
                 if (prev == v) return false;
             }
             b = next(b);
+            spill = true;
         }
     }
     __device__ __forceinline__ int find_slot(uint32_t v) const {
@@ -158,6 +167,17 @@ struct HashSet<false> {
             if (r >= 0 || q1.z == kEmpty) return r;
             b = next(b);
         }
+    }
+    __device__ __forceinline__ int find_rank_home(uint32_t v) const {
+        const uint32_t b = bucket(v);
+        const uint4 q0 = *reinterpret_cast<const uint4*>(slot + 4 * b);
+        const uint4 q1 = *reinterpret_cast<const uint4*>(slot + 4 * b + 2);
+        int r = -1;
+        r = (q1.z == v) ? (int)q1.w : r;
+        r = (q1.x == v) ? (int)q1.y : r;
+        r = (q0.z == v) ? (int)q0.w : r;
+        r = (q0.x == v) ? (int)q0.y : r;
+        return r;
     }
 };
 
@@ -220,6 +240,7 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         __syncwarp();
         int U = 0;
         uint32_t lo = 0xffffffffu, hi = 0u;
+        bool spill = false;
         int32_t nxt = lane < T ? tl[lane] : 0;
         const int32_t root = __shfl_sync(kFull, nxt, 0);
 #pragma unroll 1
@@ -227,7 +248,7 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             const int32_t v = nxt;
             const bool valid = b0 + lane < T;
             nxt = b0 + 32 + lane < T ? tl[b0 + 32 + lane] : 0;
-            const bool fresh = valid && hs.insert((uint32_t)v);
+            const bool fresh = valid && hs.insert((uint32_t)v, spill);
             const unsigned fb = __ballot_sync(kFull, fresh);
             if (fresh) {
                 keys[U + __popc(fb & lt)] = v;
@@ -244,6 +265,10 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             __syncwarp();
             continue;
         }
+        // every key in its home bucket (~80% of C2 roots): probes need no
+        // chain walk. (Rebuilding the other roots' tables with another hash
+        // multiplier measured no faster.)
+        const bool home = !__any_sync(kFull, spill);
         lo = __reduce_min_sync(kFull, lo);
         hi = __reduce_max_sync(kFull, hi);
         // ---- order-preserving buckets b = (v - lo) >> shift, ~2U of them
@@ -374,10 +399,10 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
 #pragma unroll
             for (int u = 0; u < G; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
         };
-        auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G]) {
+        auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G], auto at_home) {
             int j[G];
 #pragma unroll
-            for (int u = 0; u < G; ++u) j[u] = hs.find_rank(v[u]);
+            for (int u = 0; u < G; ++u) j[u] = decltype(at_home)::value ? hs.find_rank_home(v[u]) : hs.find_rank(v[u]);
             if (edc + 32 * G <= ed_end) {
 #pragma unroll
                 for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::false_type{});
@@ -404,11 +429,20 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             const int wfull = min(we, S >> 5);  // windows of the pass with 32 entries
             const int nfg = max(0, wfull - wb) / G;
             int w = wb;
-            for (int gi = 0; gi < nfg; ++gi) {
-                int rsA[G], kkA[G];
-                uint32_t vA[G];
-                fetch(wb + gi * G, rsA, kkA, vA);
-                consume(rsA, kkA, vA);
+            if (home) {
+                for (int gi = 0; gi < nfg; ++gi) {
+                    int rsA[G], kkA[G];
+                    uint32_t vA[G];
+                    fetch(wb + gi * G, rsA, kkA, vA);
+                    consume(rsA, kkA, vA, std::true_type{});
+                }
+            } else {
+                for (int gi = 0; gi < nfg; ++gi) {
+                    int rsA[G], kkA[G];
+                    uint32_t vA[G];
+                    fetch(wb + gi * G, rsA, kkA, vA);
+                    consume(rsA, kkA, vA, std::false_type{});
+                }
             }
             w = wb + nfg * G;
             for (; w < we; ++w) {  // < G trailing windows, the last one possibly partial
