@@ -166,6 +166,40 @@ __device__ void choose_local(RootStream<PHILOX>& rs, uint32_t n, uint32_t k,
     }
 }
 
+// Appends one lane's run of touched entries in order: every aligned 4-entry
+// block the run fills completely leaves as one 16-byte store, the ragged
+// ends of the run (blocks shared with earlier entries or a neighbouring
+// root's slot) as single stores. Cuts K1's L1->L2 write requests ~4x.
+struct SeqWriter {
+    int32_t* ptr;        // next entry (the touched buffer is 16-byte aligned)
+    bool clean;          // the current block began inside this run
+    int32_t w0, w1, w2;  // its first three entries
+    __device__ __forceinline__ void start(int32_t* at) {
+        ptr = at;
+        clean = false;
+        w0 = w1 = w2 = 0;
+    }
+    __device__ __forceinline__ void put(int32_t v) {
+        const uint32_t j = (uint32_t)(reinterpret_cast<uintptr_t>(ptr) >> 2) & 3u;
+        clean |= j == 0;
+        if (!clean) *ptr = v;  // head block shared with earlier entries
+        else if (j == 3) *reinterpret_cast<int4*>(ptr - 3) = make_int4(w0, w1, w2, v);
+        w0 = j == 0 ? v : w0;
+        w1 = j == 1 ? v : w1;
+        w2 = j == 2 ? v : w2;
+        ++ptr;
+    }
+    __device__ __forceinline__ void finish() const {  // the tail block's entries, singly
+        const uint32_t j = (uint32_t)(reinterpret_cast<uintptr_t>(ptr) >> 2) & 3u;
+        if (clean && j > 0) {
+            int32_t* b = ptr - j;
+            b[0] = w0;
+            if (j > 1) b[1] = w1;
+            if (j > 2) b[2] = w2;
+        }
+    }
+};
+
 // Root seed: the uploaded seed, or Rng::derive(seed, {path..., batch_base +
 // bi, pos}) (rng.cpp:76-85) from the call's seed spec.
 __device__ __forceinline__ uint64_t root_seed(const ExpandParams& p, int r) {
@@ -279,6 +313,8 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
             // two register sets, stores of a set one decision late
             int32_t cA[KCAP], cB[KCAP];
             int TA = 0, kA = 0, TB = 0, kB = 0;
+            SeqWriter wr;
+            wr.start(out + T);
             auto issue = [&](const int2& rw, int32_t (&c)[KCAP], int& Tc, int& kc) {
                 uint32_t pos[KCAP];
                 kc = (int)decide(rw, pos);
@@ -287,10 +323,10 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
                 for (int q = 0; q < KCAP; ++q) c[q] = q < kc ? __ldg(p.w_ci + rw.x + pos[q]) : 0;
                 T += kc;
             };
-            auto flush = [&](const int32_t (&c)[KCAP], int Tc, int& kc) {
+            auto flush = [&](const int32_t (&c)[KCAP], int, int& kc) {  // in T order
 #pragma unroll
                 for (int q = 0; q < KCAP; ++q)
-                    if (q < kc) out[Tc + q] = c[q];
+                    if (q < kc) wr.put(c[q]);
                 kc = 0;
             };
             for (;;) {
@@ -303,6 +339,7 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
             }
             flush(cA, TA, kA);
             flush(cB, TB, kB);
+            wr.finish();
         }
         if (bad) {
             p.tcount[r] = T;
