@@ -348,6 +348,8 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
         if (LOCAL || in_cache) {
             // resolve parked walk positions -> vertices (+ next-level rows)
             constexpr int U = 8;
+            SeqWriter wr;
+            wr.start(out + next_begin);
             for (int t0 = next_begin; t0 < T; t0 += U) {
                 int32_t e[U], c[U];
 #pragma unroll
@@ -367,8 +369,9 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (t0 + u < T) out[t0 + u] = c[u];
+                    if (t0 + u < T) wr.put(c[u]);
             }
+            wr.finish();
         }
         lc[level + 1] = T - next_begin;
         lvl_begin = next_begin;
