@@ -240,8 +240,7 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
     lc[0] = 1;
     const bool cached = cache != nullptr;
     {
-        const int32_t b = p.w_rp[root];
-        if (cached) cache[ti] = make_int2(b, p.w_rp[root + 1] - b);
+        if (cached) cache[ti] = __ldg(p.w_ri + root);
     }
     int T = 1, lvl_begin = 0, lvl_end = 1;
     bool bad = false;
@@ -253,8 +252,7 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
             if (cached) row = cache[(size_t)i * bd + ti];
             else {
                 const int32_t v = out[i];
-                row.x = p.w_rp[v];
-                row.y = p.w_rp[v + 1] - row.x;
+                row = __ldg(p.w_ri + v);
             }
             if (row.y == 0) continue;
             if (p.neg_row && p.neg_row[out[i]]) {
@@ -359,13 +357,13 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
                 for (int u = 0; u < U; ++u)
                     if (t0 + u < T) c[u] = __ldg(p.w_ci + e[u]);
                 if (in_cache) {
-                    int32_t b0[U], b1[U];
+                    int2 ri[U];
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        if (t0 + u < T) { b0[u] = __ldg(p.w_rp + c[u]); b1[u] = __ldg(p.w_rp + c[u] + 1); }
+                        if (t0 + u < T) ri[u] = __ldg(p.w_ri + c[u]);
 #pragma unroll
                     for (int u = 0; u < U; ++u)
-                        if (t0 + u < T) cache[(size_t)(t0 + u) * bd + ti] = make_int2(b0[u], b1[u] - b0[u]);
+                        if (t0 + u < T) cache[(size_t)(t0 + u) * bd + ti] = ri[u];
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u)
@@ -476,8 +474,9 @@ __global__ void __launch_bounds__(128) k_expand_group(ExpandParams p) {
             v = 0; b = 0; deg = 0;
             if (i < lvl_end) {
                 v = out[i];
-                b = __ldg(p.w_rp + v);
-                deg = __ldg(p.w_rp + v + 1) - b;
+                const int2 ri = __ldg(p.w_ri + v);
+                b = ri.x;
+                deg = ri.y;
             }
         };
         int32_t nv_, nb_, nd_;

@@ -275,6 +275,26 @@ __global__ void k_recip(uint64_t* r, int32_t n) {
 
 }  // namespace
 
+namespace {
+__global__ void k_csr_row_info(const int32_t* __restrict__ rp, int32_t n, int2* __restrict__ ri) {
+    for (int32_t u = blockIdx.x * blockDim.x + threadIdx.x; u < n; u += gridDim.x * blockDim.x) {
+        const int32_t b = rp[u];
+        ri[u] = make_int2(b, rp[u + 1] - b);
+    }
+}
+}  // namespace
+
+void csr_ensure_row_info(DevCsr& c, cudaStream_t st) {
+    if (c.ri_built) return;
+    c.ri.reserve((size_t)std::max<int32_t>(c.n, 1));
+    if (c.n > 0) {
+        k_csr_row_info<<<(unsigned)std::min<int64_t>((c.n + 255) / 256, 148 * 8), 256, 0, st>>>(c.rp.p, c.n, c.ri.p);
+        HGS_CUDA(cudaGetLastError());
+    }
+    HGS_CUDA(cudaStreamSynchronize(st));
+    c.ri_built = true;
+}
+
 void graph_build_walk_sym(DevGraph& g) {
     std::lock_guard<std::recursive_mutex> lock(g.lazy_mu);
     if (g.sym_built) return;

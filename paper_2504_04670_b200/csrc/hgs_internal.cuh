@@ -96,6 +96,8 @@ struct DevCsr {
     int32_t n = 0;
     int64_t nnz = 0;
     int32_t max_deg = 0;
+    DevBuf<int2> ri;  // per row (start, degree): K1's row loads; built on first use as a walk
+    bool ri_built = false;
 };
 
 // Device-resident event: the extraction matrix A (directed, edge ids), the
@@ -137,6 +139,7 @@ struct DevGraph {
     DevBuf<uint8_t> g_lab;
 
     const DevCsr& full_pattern() const { return has_full ? a_full : a; }
+    DevCsr& full_pattern() { return has_full ? a_full : a; }
 };
 
 void graph_build_walk_sym(DevGraph& g);  // K0 (graph.cu)
@@ -160,6 +163,8 @@ struct CallInputs {
     const int64_t* ev_r0 = nullptr;
 };
 void graph_ensure_recip(DevGraph& g, int32_t max_m);
+// (row start, degree) per row of a walk CSR, built once (call under the graph's lazy_mu)
+void csr_ensure_row_info(DevCsr& c, cudaStream_t st);
 
 // Device exclusive scan: out[0..n] with out[n] = total (int32, total < 2^31).
 void scan_exclusive_i32(const int32_t* in, int32_t* out, int64_t n, cudaStream_t st);

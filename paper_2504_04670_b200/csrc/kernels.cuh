@@ -21,7 +21,7 @@ __device__ __forceinline__ void report(int32_t* t, int32_t code, int32_t a, int3
 }
 
 struct ExpandParams {
-    const int32_t* __restrict__ w_rp;
+    const int2* __restrict__ w_ri;      // walk rows: (row start, degree), one 8-byte load
     const int32_t* __restrict__ w_ci;
     const uint64_t* __restrict__ recip;
     const uint8_t* __restrict__ neg_row;  // nullable

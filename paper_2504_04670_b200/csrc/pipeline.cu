@@ -216,7 +216,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     DevGraph& g = *gs[0];
     HGS_CUDA(cudaSetDevice(g.device));
     const bool seq_walk = (cfg.flags & HGS_FLAG_SEQ_WALK) != 0;
-    auto walk_of = [&](DevGraph& h) -> const DevCsr& {
+    auto walk_of = [&](DevGraph& h) -> DevCsr& {
         return cfg.symmetrize ? h.walk_sym : (seq_walk ? h.full_pattern() : h.a);
     };
     int32_t walk_max = 0, a_max = 0;
@@ -224,6 +224,10 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     for (DevGraph* h : gs) {
         if (cfg.symmetrize) graph_build_walk_sym(*h);
         graph_ensure_recip(*h, walk_of(*h).max_deg);
+        {
+            std::lock_guard<std::recursive_mutex> lk(h->lazy_mu);
+            csr_ensure_row_info(walk_of(*h), h->stream);
+        }
         if (cfg.gather && !h->has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
         walk_max = std::max(walk_max, walk_of(*h).max_deg);
         a_max = std::max(a_max, h->a.max_deg);
@@ -288,7 +292,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     if (s->profiled) HGS_CUDA(cudaEventRecord(s->ev[0], st));
 
     ExpandParams ep{};
-    ep.w_rp = walk.rp.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
+    ep.w_ri = walk.ri.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
     ep.neg_row = (!cfg.symmetrize && !seq_walk && g.has_neg) ? g.neg_row.p : nullptr;
     ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
     ep.batch_off = in.batch_off; ep.k = (int32_t)k;
@@ -339,7 +343,7 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     // point the kernels at one event's graph (multi-event calls rebind per event)
     auto bind = [&](DevGraph& h) {
         const DevCsr& w = walk_of(h);
-        ep.w_rp = w.rp.p; ep.w_ci = w.ci.p; ep.recip = h.recip.p;
+        ep.w_ri = w.ri.p; ep.w_ci = w.ci.p; ep.recip = h.recip.p;
         ep.neg_row = (!cfg.symmetrize && !seq_walk && h.has_neg) ? h.neg_row.p : nullptr;
         ep.n = (int32_t)h.n_rows;
         xp.a_rp = h.a.rp.p; xp.a_ci = h.a.ci.p; xp.a_gid = h.has_gid ? h.a_gid.p : nullptr; xp.a_ri = h.a_ri.p;
