@@ -141,21 +141,6 @@ __global__ void k_ordered_mean(const double* __restrict__ parts, int32_t w, int6
     }
 }
 
-// The stream-ordered pool trims its memory back to the driver at every
-// synchronisation by default (release threshold 0), which turns each
-// cudaMallocAsync after a sync into a driver allocation; the consumer's
-// small per-batch plans keep the memory instead.
-void pool_keep(int device) {
-    static std::once_flag once[64];
-    if (device < 0 || device >= 64) return;
-    std::call_once(once[device], [device] {
-        cudaMemPool_t pool;
-        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
-            uint64_t keep = UINT64_MAX;
-            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
-        }
-    });
-}
 
 unsigned grid_for(int64_t work) {
     return (unsigned)std::max<int64_t>(1, std::min<int64_t>((work + 255) / 256, 148 * 16));

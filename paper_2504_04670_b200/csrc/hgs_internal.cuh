@@ -67,20 +67,46 @@ __device__ __forceinline__ uint32_t ldg_keep(const uint32_t* a, uint64_t pol) {
 #endif
 }
 
+// The stream-ordered pool trims its memory back to the driver at every
+// synchronisation by default (release threshold 0), which turns each
+// cudaMallocAsync after a sync into a driver allocation; the library keeps
+// the memory in the device's pool instead (like torch's caching allocator).
+inline void pool_keep(int device) {
+    static std::once_flag once[64];
+    if (device < 0 || device >= 64) return;
+    std::call_once(once[device], [device] {
+        cudaMemPool_t pool;
+        if (cudaDeviceGetDefaultMemPool(&pool, device) == cudaSuccess) {
+            uint64_t keep = UINT64_MAX;
+            cudaMemPoolSetAttribute(pool, cudaMemPoolAttrReleaseThreshold, &keep);
+        }
+    });
+}
+
+// Device buffer from the device's stream-ordered pool. cudaMalloc/cudaFree
+// cost milliseconds each on B200 boxes (a free unmaps; both synchronise), so
+// graph builds and teardown allocate from the pool: reserve completes the
+// allocation before returning, release waits for the device (cudaFree's
+// implicit synchronisation) and hands the block back to the pool.
 template <class T>
 struct DevBuf {
     T* p = nullptr;
     size_t cap = 0;
     void reserve(size_t n) {
         if (n <= cap) return;
-        if (p) cudaFree(p);
-        p = nullptr;
-        cap = 0;
-        HGS_CUDA(cudaMalloc(&p, (n ? n : 1) * sizeof(T)));
+        release();
+        int dev = 0;
+        HGS_CUDA(cudaGetDevice(&dev));
+        pool_keep(dev);
+        HGS_CUDA(cudaMallocAsync(reinterpret_cast<void**>(&p), (n ? n : 1) * sizeof(T), 0));
+        HGS_CUDA(cudaStreamSynchronize(0));
         cap = n;
     }
     void release() {
-        if (p) cudaFree(p);
+        if (p) {
+            cudaDeviceSynchronize();
+            cudaFreeAsync(p, 0);
+        }
         p = nullptr;
         cap = 0;
     }
