@@ -220,7 +220,7 @@ __device__ __forceinline__ uint64_t root_seed(const ExpandParams& p, int r) {
 // One root, one lane, in the reference's decision order. `cache` (nullable:
 // rows are then re-read from the walk CSR) holds (row start, degree) of the
 // rows still to expand, entry i of this lane at cache[i * bd + ti].
-template <int KCAP, bool PHILOX, bool LOCAL>
+template <int KCAP, bool PHILOX, bool LOCAL, bool COMBINE = false>
 __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, int ti, const uint64_t* recip) {
     const int32_t root = p.roots32 ? p.roots32[r] : (int32_t)p.roots64[r];
     if (root < 0 || root >= p.n) {
@@ -321,10 +321,13 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
                 for (int q = 0; q < KCAP; ++q) c[q] = q < kc ? __ldg(p.w_ci + rw.x + pos[q]) : 0;
                 T += kc;
             };
-            auto flush = [&](const int32_t (&c)[KCAP], int, int& kc) {  // in T order
+            auto flush = [&](const int32_t (&c)[KCAP], int Tc, int& kc) {  // in T order
 #pragma unroll
                 for (int q = 0; q < KCAP; ++q)
-                    if (q < kc) wr.put(c[q]);
+                    if (q < kc) {
+                        if constexpr (COMBINE) wr.put(c[q]);
+                        else out[Tc + q] = c[q];
+                    }
                 kc = 0;
             };
             for (;;) {
@@ -337,7 +340,7 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
             }
             flush(cA, TA, kA);
             flush(cB, TB, kB);
-            wr.finish();
+            if constexpr (COMBINE) wr.finish();
         }
         if (bad) {
             p.tcount[r] = T;
@@ -367,9 +370,12 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
                 }
 #pragma unroll
                 for (int u = 0; u < U; ++u)
-                    if (t0 + u < T) wr.put(c[u]);
+                    if (t0 + u < T) {
+                        if constexpr (COMBINE) wr.put(c[u]);
+                        else out[t0 + u] = c[u];
+                    }
             }
-            wr.finish();
+            if constexpr (COMBINE) wr.finish();
         }
         lc[level + 1] = T - next_begin;
         lvl_begin = next_begin;
@@ -380,7 +386,7 @@ __device__ void expand_root(const ExpandParams& p, int r, int2* cache, int bd, i
     p.decisions[r] = ndec - dec0;
 }
 
-template <int KCAP, bool PHILOX, bool LOCAL>
+template <int KCAP, bool PHILOX, bool LOCAL, bool COMBINE>
 __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
     extern __shared__ int2 cache[];  // [entry][thread]: (row start, degree), then the recip table
     const int r = p.r0 + blockIdx.x * blockDim.x + threadIdx.x;
@@ -393,7 +399,7 @@ __global__ void __launch_bounds__(128, 4) k_expand(ExpandParams p) {
         recip = srecip;
     }
     if (r >= p.R) return;
-    expand_root<KCAP, PHILOX, LOCAL>(p, r, p.cache_entries > 0 ? cache : nullptr, blockDim.x, threadIdx.x, recip);
+    expand_root<KCAP, PHILOX, LOCAL, COMBINE>(p, r, p.cache_entries > 0 ? cache : nullptr, blockDim.x, threadIdx.x, recip);
 }
 
 // Decision-parallel K1: the rows of one level are independent once each knows
@@ -600,7 +606,7 @@ static bool getenv_flag_k1_groupx() { return getenv("HGS_K1_GROUPX") != nullptr;
 
 template <int KCAP, bool PH, bool LOCAL>
 static void launch_expand_t(int threads, size_t smem, const ExpandParams& ep, cudaStream_t st) {
-    auto kern = k_expand<KCAP, PH, LOCAL>;
+    auto kern = ep.combine ? k_expand<KCAP, PH, LOCAL, true> : k_expand<KCAP, PH, LOCAL, false>;
     if (smem > 48 * 1024)
         HGS_CUDA(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem));
     const unsigned grid = (unsigned)((ep.R - ep.r0 + threads - 1) / threads);

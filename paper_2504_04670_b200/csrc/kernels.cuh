@@ -22,6 +22,7 @@ __device__ __forceinline__ void report(int32_t* t, int32_t code, int32_t a, int3
 
 struct ExpandParams {
     const int2* __restrict__ w_ri;      // walk rows: (row start, degree), one 8-byte load
+    int32_t combine;                    // touched stores through the per-lane write combiner (large calls)
     const int32_t* __restrict__ w_ci;
     const uint64_t* __restrict__ recip;
     const uint8_t* __restrict__ neg_row;  // nullable

@@ -293,6 +293,11 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
 
     ExpandParams ep{};
     ep.w_ri = walk.ri.p; ep.w_ci = walk.ci.p; ep.recip = g.recip.p;
+    // The write combiner saves L1->L2 write requests, the bound of large
+    // calls (C2: K1 0.148 vs 0.160 ms), but lengthens each lane's chain, the
+    // bound of small ones (C1, 16k roots: 0.023 vs 0.020 ms)
+    ep.combine = in.R >= 32 * 1024 ? 1 : 0;
+    if (const char* e = getenv("HGS_K1_COMBINE")) ep.combine = atoi(e);
     ep.neg_row = (!cfg.symmetrize && !seq_walk && g.has_neg) ? g.neg_row.p : nullptr;
     ep.roots32 = in.roots32; ep.roots64 = in.roots64; ep.seeds = in.seeds; ep.state = in.state;
     ep.batch_off = in.batch_off; ep.k = (int32_t)k;

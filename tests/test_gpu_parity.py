@@ -132,6 +132,29 @@ def test_random_graphs(n, m, depth, fanout, values, rng):
         assert_same(dev, ref, gather)
 
 
+@pytest.mark.parametrize("combine", ["0", "1"])
+@pytest.mark.parametrize("n,m,depth,fanout", [(1000, 8000, 3, 6), (3000, 30000, 3, 8), (2000, 16000, 4, 3),
+                                              (500, 20000, 2, 17), (4000, 60000, 6, 4)])
+def test_k1_store_paths(monkeypatch, combine, n, m, depth, fanout):
+    """K1's touched stores with and without the per-lane write combiner
+    (HGS_K1_COMBINE; the default picks by call size) over every K1 body:
+    fanout 3/4 (KCAP 4), 6, 8, the local-array path (17) and the uncached
+    deep tree (depth 6, rows re-read from the walk)."""
+    monkeypatch.setenv("HGS_K1_COMBINE", combine)
+    rs = np.random.default_rng(n + depth + fanout)
+    g = random_graph(n, m, n + 3 * fanout)
+    sizes = [100, 0, 37, 1, 64]
+    roots = np.concatenate([rs.permutation(n)[:s] for s in sizes]).astype(np.int64)
+    boff = np.concatenate([[0], np.cumsum(sizes)]).astype(np.int64)
+    seeds = rs.integers(0, 2**63, len(roots), dtype=np.uint64)
+    for rng in (0, 1):
+        for sym in (True, False):
+            kw = dict(rng=rng, depth=depth, fanout=fanout, symmetrize=sym)
+            dev, _ = device_run(g, roots, boff, seeds, gather=True, **kw)
+            ref = O.bulk_shadow(g, roots, boff, seeds, gather=True, **kw)
+            assert_same(dev, ref, True)
+
+
 def banded_graph(n, w, seed, outliers=0):
     """Vertex ids with locality (u -> u+1..u+w) plus a few long-range edges
     to the top ids: a root's set spans a narrow id range with outliers, which
