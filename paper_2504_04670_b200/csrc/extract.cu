@@ -603,20 +603,51 @@ __global__ void __launch_bounds__(1024) k_scan_small(const int32_t* __restrict__
     const int base = threadIdx.x * P;
     int32_t x[P], y[P];
     int64_t a = 0, b = 0;
+    // a thread's P entries are 64 contiguous bytes: 16-byte loads and stores
+    // unless the thread straddles R (or a buffer is not 16-byte aligned)
+    const bool aligned = ((reinterpret_cast<uintptr_t>(nv) | reinterpret_cast<uintptr_t>(ne) |
+                           reinterpret_cast<uintptr_t>(voff) | reinterpret_cast<uintptr_t>(eoff)) & 15) == 0;
+    const bool full = aligned && base + P <= R;
+    if (full) {
+#pragma unroll
+        for (int i = 0; i < P; i += 4) {
+            const int4 u = *reinterpret_cast<const int4*>(nv + base + i);
+            const int4 w = *reinterpret_cast<const int4*>(ne + base + i);
+            x[i] = u.x; x[i + 1] = u.y; x[i + 2] = u.z; x[i + 3] = u.w;
+            y[i] = w.x; y[i + 1] = w.y; y[i + 2] = w.z; y[i + 3] = w.w;
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i) {
+            x[i] = base + i < R ? nv[base + i] : 0;
+            y[i] = base + i < R ? ne[base + i] : 0;
+        }
+    }
 #pragma unroll
     for (int i = 0; i < P; ++i) {
-        x[i] = base + i < R ? nv[base + i] : 0;
-        y[i] = base + i < R ? ne[base + i] : 0;
         a += x[i];
         b += y[i];
     }
     int64_t ta, tb;
     block_scan_pair(a, b, sh, ta, tb);
 #pragma unroll
-    for (int i = 0; i < P; ++i) {
-        if (base + i < R) { voff[base + i] = (int32_t)a; eoff[base + i] = (int32_t)b; }
-        a += x[i];
-        b += y[i];
+    for (int i = 0; i < P; ++i) {  // exclusive offsets in place of the counts
+        const int32_t cx = x[i], cy = y[i];
+        x[i] = (int32_t)a;
+        y[i] = (int32_t)b;
+        a += cx;
+        b += cy;
+    }
+    if (full) {
+#pragma unroll
+        for (int i = 0; i < P; i += 4) {
+            *reinterpret_cast<int4*>(voff + base + i) = make_int4(x[i], x[i + 1], x[i + 2], x[i + 3]);
+            *reinterpret_cast<int4*>(eoff + base + i) = make_int4(y[i], y[i + 1], y[i + 2], y[i + 3]);
+        }
+    } else {
+#pragma unroll
+        for (int i = 0; i < P; ++i)
+            if (base + i < R) { voff[base + i] = x[i]; eoff[base + i] = y[i]; }
     }
     if (threadIdx.x == 0) {
         voff[R] = (int32_t)ta;
