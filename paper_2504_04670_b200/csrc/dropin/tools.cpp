@@ -33,6 +33,9 @@ const char* hgs_tools_last_error(void) { return g_tools_err.c_str(); }
 //           bulk_shadow(make_edge_id_matrix(event), chunk, cfg, source) and
 //           gather_features(batch, event) per batch, served by the
 //           resident-graph cache
+//   mode 2: bench-sampling's bulk leg (cli.cpp:411-418): bulk_shadow only
+//   mode 3: bench-sampling's sequential leg (cli.cpp:419-431): one
+//           shadow_reference call per batch, each on its batch's seeds
 // Each rep builds a fresh PerRootChoiceSource from the seeds, as the trainer
 // does (trainer.cpp:453). ve[0..1] = V, E of the last rep.
 int hgs_dropin_time(int64_t n, const int64_t* rp, const int64_t* ci, const double* nf, int64_t f_v,
@@ -67,9 +70,16 @@ int hgs_dropin_time(int64_t n, const int64_t* rp, const int64_t* ci, const doubl
             std::vector<hitgnn::SampledBatch> out;
             if (mode == 0) {
                 out = dev->bulk_shadow(batches, cfg, src, true);
-            } else {
+            } else if (mode == 1) {
                 out = hitgnn::bulk_shadow(a, batches, cfg, src);
                 for (auto& sb : out) hitgnn::gather_features(sb, ev);
+            } else if (mode == 2) {
+                out = hitgnn::bulk_shadow(a, batches, cfg, src);
+            } else {
+                for (int64_t b = 0; b < k; ++b) {
+                    hitgnn::PerRootChoiceSource one(std::vector<uint64_t>(seeds + boff[b], seeds + boff[b + 1]));
+                    out.push_back(hitgnn::shadow_reference(a, batches[b], cfg, one));
+                }
             }
             const auto t1 = std::chrono::steady_clock::now();
             if (i >= warmup) seconds[i - warmup] = std::chrono::duration<double>(t1 - t0).count();

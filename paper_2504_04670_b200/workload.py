@@ -252,7 +252,9 @@ def dropin_time(ev: Event, roots, batch_off, seeds, *, depth=3, fanout=6, mode=0
     """Wall-clock seconds per call of the C++ drop-in end to end (host arrays
     in, std::vector<SampledBatch> with gathered features out): mode 0 =
     gpu::DeviceEvent::bulk_shadow(gather), mode 1 = the reference trainer's two
-    lines (bulk_shadow + gather_features per batch). Returns (seconds, V, E)."""
+    lines (bulk_shadow + gather_features per batch), mode 2 = bulk_shadow
+    alone and mode 3 = one shadow_reference call per batch (the two legs of
+    `hitgnn bench-sampling`). Returns (seconds, V, E)."""
     L = tools()
     r = np.ascontiguousarray(roots, np.int64)
     b = np.ascontiguousarray(batch_off, np.int64)
