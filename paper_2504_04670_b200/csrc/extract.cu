@@ -108,6 +108,10 @@ struct HashSet<true> {
         }
         return d <= rmask ? (int)d : -1;
     }
+    // home-bucket probe, raw: the rank on a hit, a value > rmask on a miss
+    __device__ __forceinline__ uint32_t probe_home(uint32_t v) const {
+        return bmin(*reinterpret_cast<const Vec*>(slot + BW * bucket(v)), v << rb);
+    }
     // find_rank when no key of the set left its home bucket: one probe, no loop
     __device__ __forceinline__ int find_rank_home(uint32_t v) const {
         const uint32_t hi = v << rb;
@@ -154,6 +158,7 @@ struct HashSet<false> {
         }
     }
     __device__ __forceinline__ void set_slot_rank(int sl, uint32_t, uint32_t r) const { slot[sl].y = r; }
+    __device__ __forceinline__ uint32_t probe_home(uint32_t v) const { return (uint32_t)find_rank_home(v); }
     __device__ __forceinline__ int find_rank(uint32_t v) const {
         uint32_t b = bucket(v);
         for (;;) {
@@ -399,16 +404,39 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
 #pragma unroll
             for (int u = 0; u < G; ++u) v[u] = (uint32_t)__ldg(p.a_ci + kk[u]);
         };
+        // emit for a raw probe result d (the rank on a hit, > rmask on a
+        // miss): the hit predicate feeds the vote and the store directly
+        auto emit_d = [&](uint32_t d, int rowsh, int kk, auto chk) {
+            const bool hit = d <= hs.rmask;
+            const unsigned hb = __ballot_sync(kFull, hit);
+            int2* dst = edc + __popc(hb & lt);
+            if (hit && (!decltype(chk)::value || dst < ed_end))
+                *dst = make_int2(rowsh | (int)d, HAS_GID ? __ldg(p.a_gid + kk) : kk);
+            edc += __popc(hb);
+        };
         auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G], auto at_home) {
-            int j[G];
+            if constexpr (decltype(at_home)::value) {
+                uint32_t d[G];
 #pragma unroll
-            for (int u = 0; u < G; ++u) j[u] = decltype(at_home)::value ? hs.find_rank_home(v[u]) : hs.find_rank(v[u]);
-            if (edc + 32 * G <= ed_end) {
+                for (int u = 0; u < G; ++u) d[u] = hs.probe_home(v[u]);
+                if (edc + 32 * G <= ed_end) {
 #pragma unroll
-                for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::false_type{});
+                    for (int u = 0; u < G; ++u) emit_d(d[u], rs[u], kk[u], std::false_type{});
+                } else {
+#pragma unroll
+                    for (int u = 0; u < G; ++u) emit_d(d[u], rs[u], kk[u], std::true_type{});
+                }
             } else {
+                int j[G];
 #pragma unroll
-                for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::true_type{});
+                for (int u = 0; u < G; ++u) j[u] = hs.find_rank(v[u]);
+                if (edc + 32 * G <= ed_end) {
+#pragma unroll
+                    for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::false_type{});
+                } else {
+#pragma unroll
+                    for (int u = 0; u < G; ++u) emit(j[u], rs[u], kk[u], std::true_type{});
+                }
             }
         };
         // Windows go in passes of win_cap: per pass, the row cursor of each
