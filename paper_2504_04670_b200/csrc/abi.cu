@@ -308,7 +308,10 @@ int hgs_event_save(const char* path, int64_t n_rows, int64_t n_cols, const int64
                    const double* values, const double* node_feat, int64_t f_v, const double* edge_feat, int64_t f_e,
                    const uint8_t* labels) {
     return guarded([&] {
-        if (!path || !row_ptr || n_rows < 0 || f_v < 0 || f_e < 0) fail(HGS_EINVAL, "hgs_event_save: bad arguments");
+        if (!path || !row_ptr || n_rows < 0 || n_cols < 0 || f_v < 0 || f_e < 0)
+            fail(HGS_EINVAL, "hgs_event_save: bad arguments");
+        if (row_ptr[0] != 0 || row_ptr[n_rows] < 0 || (row_ptr[n_rows] > 0 && !col_idx))
+            fail(HGS_EINVAL, "hgs_event_save: bad row_ptr or null col_idx");
         EventHeader h{};
         std::memcpy(h.magic, kEventMagic, 8);
         h.n_rows = n_rows;
@@ -390,7 +393,7 @@ int hgs_graph_load(int device, const char* path, hgs_graph** out) {
 
 int hgs_graph_info(hgs_graph* h, int64_t* info) {
     return guarded([&] {
-        if (!h) fail(HGS_EINVAL, "hgs: null graph");
+        if (!h || !info) fail(HGS_EINVAL, "hgs_graph_info: null argument");
         DevGraph& g = h->g;
         HGS_CUDA(cudaSetDevice(g.device));
         if (g.n_rows == g.n_cols) graph_build_walk_sym(g);
@@ -407,7 +410,7 @@ int hgs_graph_info(hgs_graph* h, int64_t* info) {
 
 int hgs_graph_walk(hgs_graph* h, int32_t symmetrize, int64_t* row_ptr, int64_t* col_idx) {
     return guarded([&] {
-        if (!h) fail(HGS_EINVAL, "hgs: null graph");
+        if (!h || !row_ptr || !col_idx) fail(HGS_EINVAL, "hgs_graph_walk: null argument");
         DevGraph& g = h->g;
         HGS_CUDA(cudaSetDevice(g.device));
         check_square(g, symmetrize);
@@ -437,6 +440,8 @@ int hgs_graph_gather(hgs_graph* h, const int64_t* l2g, int64_t V, const int64_t*
         if (!h) fail(HGS_EINVAL, "hgs: null graph");
         DevGraph& g = h->g;
         if (!g.has_features) fail(HGS_EINVAL, "gather_features: no features attached to the graph");
+        if (V < 0 || E < 0 || (V && !l2g) || (E && (!eid || !lab)) || (V * g.f_v && !xv) || (E * g.f_e && !ye))
+            fail(HGS_EINVAL, "hgs_graph_gather: bad sizes or null buffers");
         for (int64_t i = 0; i < V; ++i)
             if (l2g[i] < 0 || l2g[i] >= g.n_rows)
                 fail(HGS_EINVAL, "gather_features: batch vertex out of range for event");

@@ -242,8 +242,13 @@ def save_event(path: str, row_ptr, col_idx, *, values=None, node_feat=None, edge
     ef = None if edge_feat is None else np.ascontiguousarray(edge_feat, np.float64)
     lb = None if labels is None else np.ascontiguousarray(labels, np.uint8)
     n = len(rp) - 1
+    nnz = int(rp[-1]) if n >= 0 else 0
     f_v = 0 if nf is None else (nf.shape[1] if nf.ndim == 2 else nf.size // max(n, 1))
-    f_e = 0 if ef is None else (ef.shape[1] if ef.ndim == 2 else ef.size // max(int(rp[-1]), 1))
+    f_e = 0 if ef is None else (ef.shape[1] if ef.ndim == 2 else ef.size // max(nnz, 1))
+    # the C entry point reads exactly these extents from the pointers
+    if n < 0 or ci.size < nnz or (va is not None and va.size < nnz) or (nf is not None and nf.size < n * f_v) \
+            or (ef is not None and ef.size < nnz * f_e) or (lb is not None and lb.size < nnz):
+        raise SamplerError("hgs_event_save: array shorter than row_ptr / feature widths require")
     _check(lib().hgs_event_save(os.fsencode(path), n, n if n_cols is None else int(n_cols), _p(rp), _p(ci), _p(va),
                                 _p(nf), f_v, _p(ef), f_e, _p(lb)))
 

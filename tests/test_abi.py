@@ -166,3 +166,9 @@ def test_event_file_round_trip_and_corruption(tmp_path):
         hgs.event_info(p + ".bad")
     with pytest.raises(hgs.SamplerError, match="cannot open"):
         hgs.event_info(str(tmp_path / "missing"))
+    with pytest.raises(hgs.SamplerError, match="bad row_ptr"):
+        hgs.save_event(str(tmp_path / "bad_rp"), np.array([1, 2, 3, 3]), ci)
+    with pytest.raises(hgs.SamplerError, match="shorter"):
+        hgs.save_event(str(tmp_path / "short_ci"), rp, ci[:2])
+    with pytest.raises(hgs.SamplerError, match="shorter"):
+        hgs.save_event(str(tmp_path / "short_lab"), rp, ci, labels=lab[:1])
