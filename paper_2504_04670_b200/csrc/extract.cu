@@ -108,6 +108,43 @@ struct HashSet<true> {
         }
         return d <= rmask ? (int)d : -1;
     }
+    // insert a final (vertex, rank) entry of a key known to be absent
+    __device__ __forceinline__ void insert_entry(uint32_t v, uint32_t r) const {
+        const uint32_t e = (v << rb) | r;
+        uint32_t b = bucket(v);
+        for (;;) {
+#pragma unroll
+            for (int s = 0; s < BW; ++s)
+                if (atomicCAS(slot + BW * b + s, kEmpty, e) == kEmpty) return;
+            b = next(b);
+        }
+    }
+    // Scan-time cuckoo layout of the same words: two one-slot tables of H
+    // entries each; a key sits in T1[h1(v)] or T2[h2(v)], so a probe is two
+    // independent 4-byte loads (~3.5 wavefronts each for 32 random lanes,
+    // against ~10 for one 16-byte bucket load) and one compare.
+    static constexpr uint32_t kC2 = 0x85EBCA77u;
+    __device__ __forceinline__ uint32_t probe_cuckoo(uint32_t v, uint32_t H) const {
+        const uint32_t hi = v << rb;
+        const uint32_t e1 = slot[__umulhi(v * 0x9E3779B1u, H)];
+        const uint32_t e2 = slot[H + __umulhi(v * kC2, H)];
+        return min(e1 ^ hi, e2 ^ hi);
+    }
+    // concurrent cuckoo insert (atomicExch chains); false when the chain
+    // exceeds its bound (the evicted entry is then dropped: caller rebuilds)
+    __device__ __forceinline__ bool insert_cuckoo(uint32_t v, uint32_t r, uint32_t H, int iters) const {
+        uint32_t e = (v << rb) | r;
+        int t = 0;
+        for (int it = 0; it < iters; ++it) {
+            uint32_t* sl = t ? slot + H + __umulhi(v * kC2, H) : slot + __umulhi(v * 0x9E3779B1u, H);
+            const uint32_t old = atomicExch(sl, e);
+            if (old == kEmpty) return true;
+            e = old;
+            v = old >> rb;
+            t ^= 1;
+        }
+        return false;
+    }
     // home-bucket probe, raw: the rank on a hit, a value > rmask on a miss
     __device__ __forceinline__ uint32_t probe_home(uint32_t v) const {
         return bmin(*reinterpret_cast<const Vec*>(slot + BW * bucket(v)), v << rb);
@@ -159,6 +196,10 @@ struct HashSet<false> {
     }
     __device__ __forceinline__ void set_slot_rank(int sl, uint32_t, uint32_t r) const { slot[sl].y = r; }
     __device__ __forceinline__ uint32_t probe_home(uint32_t v) const { return (uint32_t)find_rank_home(v); }
+    // cuckoo layout is packed-only (never called)
+    __device__ __forceinline__ uint32_t probe_cuckoo(uint32_t v, uint32_t) const { return (uint32_t)find_rank(v); }
+    __device__ __forceinline__ bool insert_cuckoo(uint32_t, uint32_t, uint32_t, int) const { return false; }
+    __device__ __forceinline__ void insert_entry(uint32_t, uint32_t) const {}
     __device__ __forceinline__ int find_rank(uint32_t v) const {
         uint32_t b = bucket(v);
         for (;;) {
@@ -211,6 +252,11 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
     unsigned char* q = GMEM ? p.gscratch + ((size_t)blockIdx.x * (blockDim.x >> 5) + warp) * p.warp_bytes
                             : smem_raw + (size_t)warp * p.warp_bytes;
     const int nslots = 4 * p.n_buckets;
+#ifndef HGS_K2_CUCKOO
+#define HGS_K2_CUCKOO 1
+#endif
+    // the scan probes a cuckoo re-layout of the hash words (packed entries)
+    constexpr bool CK = HGS_K2_CUCKOO && PACKED;
     HashSet<PACKED> hs;
     hs.slot = reinterpret_cast<decltype(hs.slot)>(q);
     q += HashSet<PACKED>::kBytesPerSlot * nslots;
@@ -325,11 +371,32 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 rank = s + (t0 < v) + (t1 < v);
                 for (int j = s + 2; j < e; ++j) rank += (uint32_t)tmp[j] < v;
                 keys[rank] = (int32_t)v;
-                sl = hs.find_slot(v);
+                if constexpr (!CK) sl = hs.find_slot(v);
+            }
+            if constexpr (!CK) {
+                __syncwarp();
+                if (sl >= 0) hs.set_slot_rank(sl, v, (uint32_t)rank);
             }
             __syncwarp();
-            if (sl >= 0) hs.set_slot_rank(sl, v, (uint32_t)rank);
+        }
+        // ---- CK: re-lay the hash words as two one-slot cuckoo tables of
+        // (vertex, rank) from the sorted keys; if a chain exceeds its bound,
+        // the 4-slot table is rebuilt with final entries instead
+        const uint32_t H = (uint32_t)nslots >> 1;
+        bool ck = false;
+        if constexpr (CK) {
+            hs.clear(nslots);
             __syncwarp();
+            bool ok = true;
+            for (int i = lane; i < U; i += 32) ok = hs.insert_cuckoo((uint32_t)keys[i], (uint32_t)i, H, p.ck_iters) && ok;
+            ck = __all_sync(kFull, ok);
+            __syncwarp();
+            if (!ck) {
+                hs.clear(nslots);
+                __syncwarp();
+                for (int i = lane; i < U; i += 32) hs.insert_entry((uint32_t)keys[i], (uint32_t)i);
+                __syncwarp();
+            }
         }
 
         // ---- sorted set back to global; nonempty A rows in local order
@@ -414,11 +481,13 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 *dst = make_int2(rowsh | (int)d, HAS_GID ? __ldg(p.a_gid + kk) : kk);
             edc += __popc(hb);
         };
-        auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G], auto at_home) {
-            if constexpr (decltype(at_home)::value) {
+        // mode: 2 = cuckoo tables, 1 = home bucket only, 0 = bucket chain walk
+        auto consume = [&](const int (&rs)[G], const int (&kk)[G], const uint32_t (&v)[G], auto mode) {
+            if constexpr (decltype(mode)::value > 0) {
                 uint32_t d[G];
 #pragma unroll
-                for (int u = 0; u < G; ++u) d[u] = hs.probe_home(v[u]);
+                for (int u = 0; u < G; ++u)
+                    d[u] = decltype(mode)::value == 2 ? hs.probe_cuckoo(v[u], H) : hs.probe_home(v[u]);
                 if (edc + 32 * G <= ed_end) {
 #pragma unroll
                     for (int u = 0; u < G; ++u) emit_d(d[u], rs[u], kk[u], std::false_type{});
@@ -457,21 +526,17 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             const int wfull = min(we, S >> 5);  // windows of the pass with 32 entries
             const int nfg = max(0, wfull - wb) / G;
             int w = wb;
-            if (home) {
+            auto groups = [&](auto mode) {
                 for (int gi = 0; gi < nfg; ++gi) {
                     int rsA[G], kkA[G];
                     uint32_t vA[G];
                     fetch(wb + gi * G, rsA, kkA, vA);
-                    consume(rsA, kkA, vA, std::true_type{});
+                    consume(rsA, kkA, vA, mode);
                 }
-            } else {
-                for (int gi = 0; gi < nfg; ++gi) {
-                    int rsA[G], kkA[G];
-                    uint32_t vA[G];
-                    fetch(wb + gi * G, rsA, kkA, vA);
-                    consume(rsA, kkA, vA, std::false_type{});
-                }
-            }
+            };
+            if (CK && ck) groups(std::integral_constant<int, 2>{});
+            else if (home) groups(std::integral_constant<int, 1>{});
+            else groups(std::integral_constant<int, 0>{});
             w = wb + nfg * G;
             for (; w < we; ++w) {  // < G trailing windows, the last one possibly partial
                 const int base = w << 5;
@@ -479,8 +544,13 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
                 const int own = min((int)wi.y + __popc(wi.x & le), NR - 1);
                 const int2 ri = rinfo[own];
                 const int kk = base + lane < S ? base + lane + ri.x : -1;
-                const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
-                emit(j, ri.y, kk, std::true_type{});
+                if (CK && ck) {
+                    const uint32_t d = kk >= 0 ? hs.probe_cuckoo((uint32_t)__ldg(p.a_ci + kk), H) : ~0u;
+                    emit_d(d, ri.y, kk, std::true_type{});
+                } else {
+                    const int j = kk >= 0 ? hs.find_rank((uint32_t)__ldg(p.a_ci + kk)) : -1;
+                    emit(j, ri.y, kk, std::true_type{});
+                }
             }
             __syncwarp();
         }
@@ -488,7 +558,16 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
         if (lane == 0) {
             p.root_nv[r] = U;
             p.root_ne[r] = count;
-            p.root_rloc[r] = T > 0 ? hs.find_rank((uint32_t)root) : -1;
+            int rl = -1;
+            if (T > 0) {
+                if (CK && ck) {
+                    const uint32_t d = hs.probe_cuckoo((uint32_t)root, H);
+                    rl = d <= hs.rmask ? (int)d : -1;
+                } else {
+                    rl = hs.find_rank((uint32_t)root);
+                }
+            }
+            p.root_rloc[r] = rl;
             p.root_scan[r] = S;
             if (count > (int)(ed_end - ed)) {
                 atomicMax(&p.ticket[4], count);

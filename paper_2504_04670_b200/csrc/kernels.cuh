@@ -94,6 +94,7 @@ struct ExtractParams {
     unsigned char* gscratch;            // nullable: per-warp working sets in global memory
     int32_t lnb;                        // k_extract_dir: log2 of the rank-directory buckets
     const int32_t* __restrict__ e_off;  // nullable: exact edge-slot offsets [R+1] (re-run after overflow)
+    int32_t ck_iters;                   // k_extract: cuckoo insert chain bound (beyond it: 4-slot table)
     int32_t tab_n;                      // k_extract_bm: directory words (multiple of 32, > n / 16)
     const int4* __restrict__ a_q;       // k_extract_bm: A in 4-entry quads (DevGraph::a_q)
     const int4* __restrict__ a_qid;     // k_extract_bm: edge ids of the a_q entries

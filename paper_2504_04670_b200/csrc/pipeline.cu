@@ -316,6 +316,8 @@ void sample_enqueue(hgs_sample* s, const hgs_config& cfg, const CallInputs& in, 
     xp.root_nv = s->root_nv.p; xp.root_ne = s->root_ne.p; xp.root_rloc = s->root_rloc.p;
     xp.root_scan = s->root_scan.p; xp.escratch = s->escratch.p; xp.e_stride = s->e_stride;
     xp.e_off = rerun && s->exact_slots ? s->eoff_exact.p : nullptr;
+    xp.ck_iters = 64;  // cuckoo chain bound of the hash kernel's scan tables
+    if (const char* e = getenv("HGS_K2_CK_ITERS")) xp.ck_iters = atoi(e);  // test hook: 0 forces the fallback
     xp.ticket = s->ticket.p;
     auto set_layout = [&]() {
         xp.n_buckets = c.n_buckets; xp.set_cap = c.set_cap; xp.row_cap = c.row_cap;

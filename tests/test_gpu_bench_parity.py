@@ -172,6 +172,25 @@ def test_fuzz_slice():
     assert cases == 120 and mism == 0, log
 
 
+@pytest.mark.parametrize("iters", [0, 1, 2])
+def test_k2_cuckoo_fallback(monkeypatch, iters):
+    """The hash kernel's scan probes a cuckoo re-layout of its table; a root
+    whose insert chain exceeds the bound rebuilds the 4-slot table instead
+    (HGS_K2_CK_ITERS: 0 forces the fallback on every root, 1-2 on a mix of
+    roots). Outputs stay equal to the reference digests on C1 (both RNGs)."""
+    monkeypatch.setenv("HGS_K2_CK_ITERS", str(iters))
+    hg = H()
+    c1 = load_json("c1.json")
+    ev = W().preset_event("C1")
+    roots, boff, seeds = W().bench_roots(ev.n, 256, 16, seed=1, rep=0)
+    S = hg.Sampler(hg.Graph(ev.rp, ev.ci).attach_features(ev.node_feat, ev.edge_feat, ev.labels))
+    for run in c1["runs"]:
+        S.bulk_shadow(roots, boff, seeds, rng=run["rng"], depth=run["depth"], fanout=6, gather=True)
+        dev = S.to_host()
+        for f in INT_FIELDS:
+            assert sha(np.asarray(dev[f]).astype(np.int64)) == run["digests"][f], (f, iters)
+
+
 @pytest.mark.parametrize("case", ["random", "clustered", "c1"])
 @pytest.mark.parametrize("kernel", ["dir", "bm"])
 def test_k2_alternative_kernels(monkeypatch, case, kernel):
