@@ -453,9 +453,11 @@ __global__ void __launch_bounds__(128, HGS_K2_MINB) k_extract(ExtractParams p) {
             edc += __popc(hb);
         };
 // Windows per group: swept on B200 at C2 (G = 2 and 4 double-buffered,
-// 5-8 single-buffered): 6 single-buffered groups are best.
+// 5-8 single-buffered): 6 single-buffered groups were best with 16-byte
+// bucket probes; with the cuckoo probes 7 is (K2 0.678 vs 0.700 ms; 4: 0.707,
+// 5: 0.680, 8: 0.692).
 #ifndef HGS_K2_G
-#define HGS_K2_G 6
+#define HGS_K2_G 7
 #endif
         constexpr int G = HGS_K2_G;  // windows in flight per group
         int wb = 0;  // first window of the current pass (window info is pass-local)

@@ -104,7 +104,10 @@ bool plan_extract(CallPlan& c, int64_t bound, int64_t n) {
     c.win_cap = c.set_cap / 2;  // windows per pass: (u32 mask, u32 cursor) each, in the set array
     const size_t rest = 4 * (size_t)c.set_cap + 4 * (size_t)(c.row_cap + 36) + 8 * (size_t)c.row_cap;
     const size_t bucket_bytes = c.packed ? 16 : 32;
-    const size_t budget = (233472 / 6 - 1024) / 4 / 16 * 16;  // per warp, 6 CTAs of 4 warps
+#ifndef HGS_K2_MINB
+#define HGS_K2_MINB 6  // K2 CTAs per SM (extract.cu's launch bound)
+#endif
+    const size_t budget = (233472 / HGS_K2_MINB - 1024) / 4 / 16 * 16;  // per warp, HGS_K2_MINB CTAs of 4 warps
     int64_t nb = budget > rest ? (int64_t)((budget - rest) / bucket_bytes) : 0;
     if (const char* e = getenv("HGS_HASH_SLOTS_PER_KEY")) nb = (atoi(e) * bound + 3) / 4;
     if (4 * nb * 2 < 5 * bound) nb = (3 * bound + 3) / 4;
