@@ -2,15 +2,17 @@
 // scan, K3 (block-diagonal packing + feature/label gather) and small helpers.
 //
 // K2 k_extract, one warp per root:
-//   sorted_vertex_set (sampler.cpp:48-53): the touched list is inserted into a
-//   shared-memory hash set (4-slot buckets probed with one 16-byte LDS), the
-//   unique vertices are bitonic-sorted in registers and written back over the
-//   touched slot; ranks (local ids) go into the table.
+//   sorted_vertex_set (sampler.cpp:48-53): the touched list is deduplicated
+//   through a shared-memory hash set (4-slot buckets, CAS inserts), the unique
+//   vertices are sorted by an order-preserving bucket sort and written back
+//   over the touched slot; their ranks are the local ids.
+//   The hash words are then re-laid as two one-slot cuckoo tables of packed
+//   (vertex, rank) entries, so a scan probe is two independent 4-byte loads.
 //   induced_subgraph = S·A·Sᵀ (sparse.cpp:177-191) on the directed edge-id
 //   matrix A: the A rows of the set, in local order, are flattened into one
 //   index space and scanned in 32-wide coalesced windows (row owner of every
-//   lane from a __reduce_or_sync bitmask of row starts), each column probed in
-//   the hash set; hits come out row-major with ascending columns, i.e. in the
+//   lane from a bitmask of row starts per window), each column probed in the
+//   cuckoo tables; hits come out row-major with ascending columns, i.e. in the
 //   reference's CSR order, and are appended to the root's edge slot.
 // Offsets: exclusive scan of (V_r, E_r) over roots (block_diag offsets,
 //   sparse.cpp:245-258) — three small launches.
