@@ -26,14 +26,18 @@ for cub in os.listdir(tmp):
         if m:
             lines[int(m.group(1), 16)] = cur
     break
-src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass", "-k", kern],
+src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass", "--kernel-name-base", "mangled", "-k", kern],
                      capture_output=True, text=True).stdout
 if not src.strip():
     src = subprocess.run(["ncu", "-i", rep, "--page", "source", "--csv", "--print-source=sass"],
                          capture_output=True, text=True).stdout
 r = csv.reader(io.StringIO(src))
 next(r); hdr = next(r)
-rows = [dict(zip(hdr, x)) for x in r]
+rows = []
+for x in r:  # first launch only (a report may hold several blocks)
+    if x and x[0] == "Kernel Name":
+        break
+    rows.append(dict(zip(hdr, x)))
 base = int(rows[0]["Address"], 16)
 agg = collections.defaultdict(lambda: [0, 0, collections.Counter()])
 stall_cols = [h for h in hdr if h.startswith("stall_") and "Not Issued" not in h]
