@@ -787,17 +787,27 @@ bool launch_scan_small(const int32_t* nv, const int32_t* ne, int32_t R, int32_t*
 // K3
 // ===========================================================================
 
+constexpr int kPackSmemBatches = 2048;  // batch offsets staged in shared memory up to this k
+
 __global__ void __launch_bounds__(256) k_pack(PackParams p) {
     const int lane = lane_id();
     const int nwarps = gridDim.x * (blockDim.x >> 5);
     constexpr int U = 8;  // independent loads in flight per lane
+    // the batch of each root by binary search over batch_off: staged in
+    // shared memory (one load per entry per CTA instead of ~log2(k)
+    // dependent global loads per root)
+    __shared__ int32_t sbo[kPackSmemBatches + 1];
+    const bool staged = p.k <= kPackSmemBatches;
+    if (staged)
+        for (int i = threadIdx.x; i <= p.k; i += blockDim.x) sbo[i] = (int32_t)p.batch_off[i];
+    __syncthreads();
     for (int r = p.r0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5); r < p.R; r += nwarps) {
         int b;
         {
             int lo = 0, hi = p.k;  // largest b with batch_off[b] <= r
             while (lo < hi) {
                 const int mid = (lo + hi + 1) >> 1;
-                if (p.batch_off[mid] <= r) lo = mid; else hi = mid - 1;
+                if ((staged ? (int64_t)sbo[mid] : p.batch_off[mid]) <= r) lo = mid; else hi = mid - 1;
             }
             b = lo;
         }
